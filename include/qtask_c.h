@@ -1,0 +1,222 @@
+/*
+ * qtask_c.h -- C ABI of the B200-native qTask hot path (libqtask_b200.so).
+ *
+ * Drop-in boundary for the reference's data-parallel core:
+ * the reference has no FFI; its hot path sits behind the C++ class
+ * qtask::Simulator (/root/reference/proj/include/qtask/engine.hpp:46-151),
+ * whose private kernels run_permute_tasks / run_mxv_partition
+ * (engine.hpp:129-135, engine.cpp:315-383) and scheduler TaskPool
+ * (executor.hpp:18-48) this library replaces.  Two layers are exported:
+ *
+ *  1. qt_state_*  -- a device-resident 2^n complex128 state vector and
+ *     stateless gate application (the replacement for the two CPU kernels
+ *     plus the COW block stores, engine.hpp:18-29).
+ *  2. qt_sim_*    -- the incremental simulator with the reference's
+ *     programming model (modifiers, update_state, readout), one entry point
+ *     per public member of qtask::Simulator. include/qtask/engine.hpp wraps
+ *     these in the reference's C++ API and exception types.
+ *
+ * Conventions: index bit t <-> qubit t; amplitudes are
+ * interleaved (re, im) doubles, bit-compatible with std::complex<double>.
+ * Every function returns QT_OK (0) or a negative QT_ERR_* code; the message
+ * of the last failure on the calling thread is qt_last_error().
+ * Handles are single-writer (engine.hpp:41-45): one host thread at a time.
+ */
+#ifndef QTASK_C_H_
+#define QTASK_C_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: one per reference exception type (types.hpp:21-64) -- */
+#define QT_OK 0
+#define QT_ERR_ARG (-1)              /* qtask::Error                      */
+#define QT_ERR_NET_CONFLICT (-2)     /* qtask::NetConflictError           */
+#define QT_ERR_UNKNOWN_NET (-3)      /* qtask::UnknownNetError            */
+#define QT_ERR_UNKNOWN_GATE (-4)     /* qtask::UnknownGateError           */
+#define QT_ERR_BAD_QUBIT (-5)        /* qtask::BadQubitError              */
+#define QT_ERR_INVALID_POSITION (-6) /* qtask::InvalidPositionError       */
+#define QT_ERR_STALE_STATE (-7)      /* qtask::StaleStateError            */
+#define QT_ERR_NUMERIC (-8)          /* qtask::NumericError               */
+#define QT_ERR_SUPERPOSITION (-9)    /* qtask::SuperpositionGateError     */
+#define QT_ERR_CUDA (-20)            /* CUDA runtime failure              */
+#define QT_ERR_OOM (-21)             /* device allocation failed          */
+#define QT_ERR_NCCL (-22)            /* NCCL failure                      */
+#define QT_ERR_NO_DEVICE (-23)       /* no CUDA device visible            */
+
+/* ---- gate kinds: reference GateKind order (gate.hpp:13-27) + additive -- */
+enum qt_gate_kind {
+  QT_CNOT = 0, QT_X = 1, QT_Y = 2, QT_Z = 3, QT_H = 4, QT_S = 5, QT_SDG = 6,
+  QT_T = 7, QT_TDG = 8, QT_RX = 9, QT_RY = 10, QT_RZ = 11, QT_SWAP = 12,
+  /* additive; same phase convention as their lowering: */
+  QT_U3 = 13, /* == RZ(phi) * RY(theta) * RZ(lambda)  (time order RZ(l),RY,RZ(p)) */
+  QT_CZ = 14  /* == H(t) CX(c->t) H(t) = diag(1,1,1,-1)                         */
+};
+
+/* One gate. Reference Gate record (circuit.hpp:14-21) as POD:
+ * control is -1 for 1-qubit kinds; for CNOT/CZ it is the control qubit, for
+ * SWAP the second swapped qubit. theta is the rotation angle of RX/RY/RZ;
+ * U3 uses (theta, phi, lambda). 40 bytes. */
+typedef struct qt_gate {
+  int32_t kind;
+  int32_t target;
+  int32_t control;
+  int32_t reserved; /* must be 0 */
+  double theta;
+  double phi;
+  double lambda;
+} qt_gate;
+
+/* Engine configuration. The first two fields are the reference Config
+ * (plan.hpp:17-20: power-of-two block_size >= 2, threads 0 = auto); on the
+ * GPU block_size is the partition-block granularity of UpdateStats and
+ * threads is accepted and ignored. The rest are GPU knobs (0 = auto). */
+typedef struct qt_config {
+  uint64_t block_size;
+  uint32_t threads;
+  int32_t device;            /* CUDA ordinal; -1 = current device          */
+  int32_t tile_qubits;       /* qubits per shared-memory tile (0 = auto)   */
+  int32_t max_checkpoints;   /* incremental checkpoint slots (0 = auto)    */
+  double checkpoint_fraction;/* share of free HBM for checkpoints (0=auto) */
+  int32_t segment_gates;     /* gates per checkpoint segment (0 = auto)    */
+  int32_t reserved[3];
+} qt_config;
+
+/* Result of the last qt_apply / update (UpdateStats, engine.hpp:32-39, in
+ * GPU terms plus the bytes the roofline is computed from). */
+typedef struct qt_run_stats {
+  int32_t full;                 /* reference UpdateStats::full             */
+  int32_t reserved0;
+  uint64_t executed_partitions; /* partition blocks rewritten (ref. sem.)  */
+  uint64_t rewritten_amplitudes;/* amplitudes rewritten                    */
+  uint64_t gates;               /* gates applied (after lowering)          */
+  uint64_t passes;              /* fused tile passes launched              */
+  uint64_t kernel_launches;     /* all kernels launched by the call        */
+  uint64_t hbm_bytes;           /* algorithmic bytes: 16 B*(R+W) per pass  */
+  uint64_t exchanged_bytes;     /* bytes sent over the interconnect        */
+  uint64_t swaps;               /* global<->local qubit exchanges          */
+  uint64_t restart_gate;        /* first gate re-simulated (incremental)   */
+  uint64_t segments;            /* checkpoint segments executed            */
+  double device_ms;             /* device time of the call (CUDA events)   */
+  double plan_ms;               /* host planning time                      */
+} qt_run_stats;
+
+const char* qt_last_error(void);
+int qt_device_count(int* out);
+/* Library version string, e.g. "qtask-b200 0.1 sm_100a". */
+const char* qt_version(void);
+
+/* ======================================================================= */
+/* 1. State vector: stateless gate application                             */
+/* ======================================================================= */
+typedef struct qt_state qt_state;
+
+/* |0...0> on one GPU. cfg may be NULL. n in [1, 40] (no n <= 30 cap,
+ * circuit.cpp:9-11 is lifted; limited by HBM). */
+int qt_state_create(int num_qubits, const qt_config* cfg, qt_state** out);
+/* One shard of a state sharded on its top log2(world) qubits across
+ * `world` ranks (one process per GPU). nccl_id is the 128-byte
+ * ncclUniqueId made by qt_nccl_unique_id on rank 0 and broadcast by the
+ * caller. */
+int qt_state_create_sharded(int num_qubits, int rank, int world,
+                            const void* nccl_id, const qt_config* cfg,
+                            qt_state** out);
+/* `shards` emulated ranks held as slices of one GPU's memory, exchanged
+ * with device copies -- exercises the sharded scheduler bit-exactly on
+ * one GPU ("loopback comm backend"). */
+int qt_state_create_loopback(int num_qubits, int shards,
+                             const qt_config* cfg, qt_state** out);
+int qt_nccl_unique_id(void* out128);
+int qt_state_destroy(qt_state* st);
+
+int qt_state_num_qubits(const qt_state* st);
+/* Sets |index> (logical basis index). */
+int qt_set_basis(qt_state* st, uint64_t index);
+/* Writes / reads amplitudes [first, first+count) in logical index order,
+ * interleaved doubles, host memory. Reads synchronise. Sharded states read
+ * and write only the amplitudes this rank owns when `count` spans other
+ * ranks' ranges, unless the loopback backend holds them all. */
+int qt_write(qt_state* st, uint64_t first, uint64_t count,
+             const double* interleaved);
+int qt_read(qt_state* st, uint64_t first, uint64_t count, double* interleaved);
+/* Applies gates in order. The array is copied; stream-ordered (returns
+ * before the device finishes). Fails with QT_ERR_NUMERIC at the next
+ * synchronising call if an amplitude became non-finite. */
+int qt_apply(qt_state* st, const qt_gate* gates, size_t count);
+/* Sum |a|^2 by a deterministic tree reduction (fixed order, bit-stable
+ * across runs); sharded: fixed-order combine over ranks. */
+int qt_norm_squared(qt_state* st, double* out);
+int qt_sync(qt_state* st);
+int qt_last_stats(const qt_state* st, qt_run_stats* out);
+/* Device-resident checkpoint slots (HBM copies of the state). */
+int qt_checkpoint_save(qt_state* st, int slot);
+int qt_checkpoint_restore(qt_state* st, int slot);
+/* Pass plan of a gate list for this state as JSON (per pass: tile qubits,
+ * rounds, ops, R/W amplitudes) for roofline auditing. Writes at most cap
+ * bytes (NUL-terminated); *needed gets the full size. Host-only. */
+int qt_plan_json(const qt_state* st, const qt_gate* gates, size_t count,
+                 char* buf, size_t cap, size_t* needed);
+
+/* Host-only planner probe (no device needed): plans `gates` for an n-qubit
+ * state with `global_qubits` sharded bits and writes the JSON plan. */
+int qt_plan_probe(int num_qubits, int global_qubits, int tile_qubits,
+                  const qt_gate* gates, size_t count, char* buf, size_t cap,
+                  size_t* needed);
+
+/* ======================================================================= */
+/* 2. Incremental simulator: qtask::Simulator (engine.hpp:46-100)          */
+/* ======================================================================= */
+typedef struct qt_sim qt_sim;
+
+int qt_sim_create(int num_qubits, const qt_config* cfg, qt_sim** out);
+int qt_sim_destroy(qt_sim* sim);
+int qt_sim_num_qubits(const qt_sim* sim);
+/* Effective block size (plan.hpp:26-35) and block count. */
+uint64_t qt_sim_block_size(const qt_sim* sim);
+uint64_t qt_sim_total_blocks(const qt_sim* sim);
+
+/* Modifiers (engine.hpp:57-64). Net and gate ids are never reused; 0 is
+ * "none" (types.hpp:13-18). */
+int qt_sim_insert_net_front(qt_sim* sim, uint32_t* net);
+int qt_sim_insert_net_back(qt_sim* sim, uint32_t* net);
+int qt_sim_insert_net_after(qt_sim* sim, uint32_t after, uint32_t* net);
+int qt_sim_remove_net(qt_sim* sim, uint32_t net);
+/* control = -1 for 1-qubit kinds. params = (theta, phi, lambda) or NULL. */
+int qt_sim_insert_gate(qt_sim* sim, int kind, const double* params,
+                       uint32_t net, int target, int control, uint32_t* gate);
+int qt_sim_remove_gate(qt_sim* sim, uint32_t gate);
+
+/* engine.hpp:71. First call simulates everything; later calls re-simulate
+ * from the last valid device checkpoint at or before the earliest edit. */
+int qt_sim_update_state(qt_sim* sim);
+int qt_sim_pending(const qt_sim* sim); /* 1 if modifiers are pending */
+
+/* Queries (engine.hpp:77-80): QT_ERR_STALE_STATE while modifiers pend. */
+int qt_sim_amplitude(qt_sim* sim, uint64_t index, double* out2);
+int qt_sim_amplitudes(qt_sim* sim, uint64_t first, uint64_t last,
+                      double* interleaved);
+int qt_sim_norm_squared(qt_sim* sim, double* out);
+int qt_sim_last_update(const qt_sim* sim, qt_run_stats* out);
+
+/* Circuit introspection (Circuit, circuit.hpp:32-66): counts and the
+ * flattened gate list in simulation order (nets in order, gates in
+ * insertion order within a net). */
+size_t qt_sim_num_gates(const qt_sim* sim);
+size_t qt_sim_num_nets(const qt_sim* sim);
+int qt_sim_net_order(const qt_sim* sim, uint32_t* out, size_t cap);
+int qt_sim_net_gates(const qt_sim* sim, uint32_t net, uint32_t* out,
+                     size_t cap, size_t* count);
+int qt_sim_gate_info(const qt_sim* sim, uint32_t gate, qt_gate* out,
+                     uint32_t* net);
+int qt_sim_export_gates(const qt_sim* sim, qt_gate* out, size_t cap,
+                        size_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QTASK_C_H_ */

@@ -1,0 +1,379 @@
+// qt_capi.cpp -- extern "C" entry points of include/qtask_c.h.
+//
+// Every entry point converts internal failures (QtError, std::bad_alloc,
+// anything else) into a QT_ERR_* status and a thread-local message, so no
+// C++ exception crosses the C ABI. include/qtask/engine.hpp maps the codes
+// back onto the reference exception types (types.hpp:21-64).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "qt_gates.hpp"
+#include "qt_kernels.hpp"
+#include "qt_plan.hpp"
+#include "qt_sim.hpp"
+#include "qt_state.hpp"
+#include "qtask_c.h"
+
+struct qt_state {
+  qtb::State* s;
+};
+struct qt_sim {
+  qtb::Sim* s;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return QT_OK;
+  } catch (const qtb::QtError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return QT_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return QT_ERR_ARG;
+  } catch (...) {
+    g_err = "unknown failure";
+    return QT_ERR_ARG;
+  }
+}
+
+int null_arg() {
+  g_err = "null argument";
+  return QT_ERR_ARG;
+}
+
+int copy_out(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap > 0) {
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return QT_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int qt_plan_probe_ex(int num_qubits, int global_qubits, int tile_qubits, int detail,
+                     const qt_gate* gates, size_t count, char* buf, size_t cap,
+                     size_t* needed);
+
+const char* qt_last_error(void) { return g_err.c_str(); }
+
+const char* qt_version(void) { return "qtask-b200 0.1 sm_100a"; }
+
+int qt_device_count(int* out) {
+  if (!out) return null_arg();
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *out = n;
+  return QT_OK;
+}
+
+// ---- state ------------------------------------------------------------------
+
+int qt_state_create(int num_qubits, const qt_config* cfg, qt_state** out) {
+  if (!out) return null_arg();
+  return guard([&] {
+    *out = new qt_state{new qtb::State(num_qubits, qtb::Mode::Single, 1, 0, nullptr, cfg)};
+  });
+}
+
+int qt_state_create_sharded(int num_qubits, int rank, int world,
+                            const void* nccl_id, const qt_config* cfg,
+                            qt_state** out) {
+  if (!out || !nccl_id) return null_arg();
+  return guard([&] {
+    *out = new qt_state{new qtb::State(num_qubits, qtb::Mode::Nccl, world, rank, nccl_id, cfg)};
+  });
+}
+
+int qt_state_create_loopback(int num_qubits, int shards, const qt_config* cfg,
+                             qt_state** out) {
+  if (!out) return null_arg();
+  return guard([&] {
+    *out = new qt_state{new qtb::State(num_qubits, qtb::Mode::Loopback, shards, 0, nullptr, cfg)};
+  });
+}
+
+int qt_nccl_unique_id(void* out128) {
+  if (!out128) return null_arg();
+  return guard([&] {
+    std::string err;
+    if (!qtb::Comm::unique_id(out128, &err)) qtb::fail(QT_ERR_NCCL, err);
+  });
+}
+
+int qt_state_destroy(qt_state* st) {
+  if (!st) return QT_OK;
+  return guard([&] {
+    delete st->s;
+    delete st;
+  });
+}
+
+int qt_state_num_qubits(const qt_state* st) { return st ? st->s->nqubits() : -1; }
+
+int qt_set_basis(qt_state* st, uint64_t index) {
+  if (!st) return null_arg();
+  return guard([&] { st->s->set_basis(index); });
+}
+
+int qt_write(qt_state* st, uint64_t first, uint64_t count, const double* in) {
+  if (!st || (!in && count)) return null_arg();
+  return guard([&] { st->s->write(first, count, in); });
+}
+
+int qt_read(qt_state* st, uint64_t first, uint64_t count, double* outp) {
+  if (!st || (!outp && count)) return null_arg();
+  return guard([&] { st->s->read(first, count, outp); });
+}
+
+int qt_apply(qt_state* st, const qt_gate* gates, size_t count) {
+  if (!st || (!gates && count)) return null_arg();
+  return guard([&] { st->s->apply(gates, count); });
+}
+
+int qt_norm_squared(qt_state* st, double* outp) {
+  if (!st || !outp) return null_arg();
+  return guard([&] { *outp = st->s->norm_squared(); });
+}
+
+int qt_sync(qt_state* st) {
+  if (!st) return null_arg();
+  return guard([&] { st->s->sync(); });
+}
+
+int qt_last_stats(const qt_state* st, qt_run_stats* outp) {
+  if (!st || !outp) return null_arg();
+  *outp = st->s->stats;
+  return QT_OK;
+}
+
+int qt_checkpoint_save(qt_state* st, int slot) {
+  if (!st) return null_arg();
+  return guard([&] { st->s->checkpoint_save(slot); });
+}
+
+int qt_checkpoint_restore(qt_state* st, int slot) {
+  if (!st) return null_arg();
+  return guard([&] { st->s->checkpoint_restore(slot); });
+}
+
+int qt_plan_json(const qt_state* st, const qt_gate* gates, size_t count,
+                 char* buf, size_t cap, size_t* needed) {
+  if (!st || (!gates && count)) return null_arg();
+  return guard([&] {
+    std::vector<qtb::LOp> ops;
+    std::string err;
+    const int n = st->s->nqubits();
+    for (size_t i = 0; i < count; ++i) {
+      const int rc = qtb::lower_gate(gates[i], n, static_cast<uint32_t>(i), ops, &err);
+      if (rc != QT_OK) qtb::fail(rc, err);
+    }
+    qtb::fuse_ops(ops, n);
+    copy_out(qtb::plan_to_json(st->s->plan(ops)), buf, cap, needed);
+  });
+}
+
+int qt_plan_probe(int num_qubits, int global_qubits, int tile_qubits,
+                  const qt_gate* gates, size_t count, char* buf, size_t cap,
+                  size_t* needed) {
+  return qt_plan_probe_ex(num_qubits, global_qubits, tile_qubits, 0, gates, count,
+                          buf, cap, needed);
+}
+
+// detail != 0: the JSON carries every round's register bits and encoded ops
+// (tests/test_planner.py replays them with an independent numpy emulator).
+int qt_plan_probe_ex(int num_qubits, int global_qubits, int tile_qubits, int detail,
+                     const qt_gate* gates, size_t count, char* buf, size_t cap,
+                     size_t* needed) {
+  if (!gates && count) return null_arg();
+  return guard([&] {
+    if (num_qubits < 1 || num_qubits > 40 || global_qubits < 0 ||
+        global_qubits >= num_qubits)
+      qtb::fail(QT_ERR_BAD_QUBIT, "bad qubit counts");
+    std::vector<qtb::LOp> ops;
+    std::string err;
+    for (size_t i = 0; i < count; ++i) {
+      const int rc = qtb::lower_gate(gates[i], num_qubits, static_cast<uint32_t>(i), ops, &err);
+      if (rc != QT_OK) qtb::fail(rc, err);
+    }
+    qtb::fuse_ops(ops, num_qubits);
+    qtb::PlanOptions opt;
+    if (tile_qubits > 0) opt.tile_bits = tile_qubits < qtb::kMaxTileBits ? tile_qubits : qtb::kMaxTileBits;
+    std::vector<int> perm(num_qubits);
+    for (int q = 0; q < num_qubits; ++q) perm[q] = q;
+    const qtb::Plan p = qtb::make_plan(ops, num_qubits, num_qubits - global_qubits, perm, opt);
+    copy_out(qtb::plan_to_json(p, detail != 0), buf, cap, needed);
+  });
+}
+
+// ---- extensions used by the Python host layer / bench ------------------------
+
+// cudaStream_t of the state (events recorded on it time the passes).
+void* qt_state_stream(qt_state* st) { return st ? static_cast<void*>(st->s->stream()) : nullptr; }
+
+int qt_set_timing(qt_state* st, int on) {
+  if (!st) return null_arg();
+  st->s->set_timing(on != 0);
+  return QT_OK;
+}
+
+// Per-launch device ms of the last apply: kinds[i] 0 = tile pass, 1 = exchange.
+int qt_last_timings(qt_state* st, int* kinds, float* ms, size_t cap, size_t* count) {
+  if (!st) return null_arg();
+  return guard([&] {
+    const auto t = st->s->last_timings(kinds != nullptr || ms != nullptr);
+    if (count) *count = t.size();
+    for (size_t i = 0; i < t.size() && i < cap; ++i) {
+      if (kinds) kinds[i] = t[i].first;
+      if (ms) ms[i] = t[i].second;
+    }
+  });
+}
+
+// FP64 pipe probe: returns DFMA/s measured with CUDA events.
+int qt_probe_fp64(int device, double* dfma_per_s) {
+  if (!dfma_per_s) return null_arg();
+  return guard([&] {
+    qtb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    double* d = nullptr;
+    qtb::cuda_check(cudaMalloc(&d, sizeof(double)), "probe alloc");
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int grid = sms * 4, block = 256, iters = 4096;
+    qtb::cuda_check(qtb::launch_fp64_probe(d, grid, block, iters, 0), "probe");
+    cudaEventRecord(a, 0);
+    qtb::cuda_check(qtb::launch_fp64_probe(d, grid, block, iters, 0), "probe");
+    cudaEventRecord(b, 0);
+    qtb::cuda_check(cudaEventSynchronize(b), "probe sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    *dfma_per_s = double(grid) * block * iters * 16.0 / (ms * 1e-3);
+  });
+}
+
+// ---- incremental simulator ----------------------------------------------------
+
+int qt_sim_create(int num_qubits, const qt_config* cfg, qt_sim** out) {
+  if (!out) return null_arg();
+  return guard([&] { *out = new qt_sim{new qtb::Sim(num_qubits, cfg)}; });
+}
+
+int qt_sim_destroy(qt_sim* sim) {
+  if (!sim) return QT_OK;
+  return guard([&] {
+    delete sim->s;
+    delete sim;
+  });
+}
+
+int qt_sim_num_qubits(const qt_sim* sim) { return sim ? sim->s->nqubits() : -1; }
+uint64_t qt_sim_block_size(const qt_sim* sim) { return sim ? sim->s->block_size() : 0; }
+uint64_t qt_sim_total_blocks(const qt_sim* sim) { return sim ? sim->s->total_blocks() : 0; }
+
+int qt_sim_insert_net_front(qt_sim* sim, uint32_t* net) {
+  if (!sim || !net) return null_arg();
+  return guard([&] { *net = sim->s->insert_net_front(); });
+}
+int qt_sim_insert_net_back(qt_sim* sim, uint32_t* net) {
+  if (!sim || !net) return null_arg();
+  return guard([&] { *net = sim->s->insert_net_back(); });
+}
+int qt_sim_insert_net_after(qt_sim* sim, uint32_t after, uint32_t* net) {
+  if (!sim || !net) return null_arg();
+  return guard([&] { *net = sim->s->insert_net_after(after); });
+}
+int qt_sim_remove_net(qt_sim* sim, uint32_t net) {
+  if (!sim) return null_arg();
+  return guard([&] { sim->s->remove_net(net); });
+}
+int qt_sim_insert_gate(qt_sim* sim, int kind, const double* params, uint32_t net,
+                       int target, int control, uint32_t* gate) {
+  if (!sim || !gate) return null_arg();
+  return guard([&] { *gate = sim->s->insert_gate(kind, params, net, target, control); });
+}
+int qt_sim_remove_gate(qt_sim* sim, uint32_t gate) {
+  if (!sim) return null_arg();
+  return guard([&] { sim->s->remove_gate(gate); });
+}
+int qt_sim_update_state(qt_sim* sim) {
+  if (!sim) return null_arg();
+  return guard([&] { sim->s->update_state(); });
+}
+int qt_sim_pending(const qt_sim* sim) { return sim && sim->s->pending() ? 1 : 0; }
+
+int qt_sim_amplitude(qt_sim* sim, uint64_t index, double* out2) {
+  if (!sim || !out2) return null_arg();
+  return guard([&] { sim->s->amplitudes(index, index, out2); });
+}
+int qt_sim_amplitudes(qt_sim* sim, uint64_t first, uint64_t last, double* outp) {
+  if (!sim || !outp) return null_arg();
+  return guard([&] { sim->s->amplitudes(first, last, outp); });
+}
+int qt_sim_norm_squared(qt_sim* sim, double* outp) {
+  if (!sim || !outp) return null_arg();
+  return guard([&] { *outp = sim->s->norm_squared(); });
+}
+int qt_sim_last_update(const qt_sim* sim, qt_run_stats* outp) {
+  if (!sim || !outp) return null_arg();
+  *outp = sim->s->last_update();
+  return QT_OK;
+}
+
+size_t qt_sim_num_gates(const qt_sim* sim) { return sim ? sim->s->num_gates() : 0; }
+size_t qt_sim_num_nets(const qt_sim* sim) { return sim ? sim->s->net_order().size() : 0; }
+
+int qt_sim_net_order(const qt_sim* sim, uint32_t* outp, size_t cap) {
+  if (!sim || (!outp && cap)) return null_arg();
+  const auto& o = sim->s->net_order();
+  for (size_t i = 0; i < o.size() && i < cap; ++i) outp[i] = o[i];
+  return QT_OK;
+}
+
+int qt_sim_net_gates(const qt_sim* sim, uint32_t net, uint32_t* outp, size_t cap,
+                     size_t* count) {
+  if (!sim) return null_arg();
+  return guard([&] {
+    const auto& gs = sim->s->net_gates(net);
+    if (count) *count = gs.size();
+    for (size_t i = 0; i < gs.size() && i < cap && outp; ++i) outp[i] = gs[i];
+  });
+}
+
+int qt_sim_gate_info(const qt_sim* sim, uint32_t gate, qt_gate* outp, uint32_t* net) {
+  if (!sim) return null_arg();
+  return guard([&] { sim->s->gate_info(gate, outp, net); });
+}
+
+int qt_sim_export_gates(const qt_sim* sim, qt_gate* outp, size_t cap, size_t* count) {
+  if (!sim) return null_arg();
+  return guard([&] {
+    const auto gs = sim->s->flatten();
+    if (count) *count = gs.size();
+    for (size_t i = 0; i < gs.size() && i < cap && outp; ++i) outp[i] = gs[i];
+  });
+}
+
+}  // extern "C"

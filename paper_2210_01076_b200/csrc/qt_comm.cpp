@@ -1,0 +1,148 @@
+// qt_comm.cpp -- NCCL over NVLink for global<->local qubit exchanges.
+//
+// The reference is single-process (executor.hpp:40-47); sharding the state
+// on its top qubits across GPUs is new in this build.
+// NCCL is resolved with dlopen so the library has no link-time NCCL
+// dependency and picks up the libnccl.so.2 torch already loaded.
+#include "qt_comm.hpp"
+
+#include <dlfcn.h>
+
+#include <cstring>
+
+namespace qtb {
+
+namespace {
+// ABI subset of nccl.h (stable across NCCL 2.x)
+using ncclResult_t = int;
+using ncclComm_t = void*;
+struct ncclUniqueId {
+  char internal[128];
+};
+constexpr int ncclUint8 = 1;
+constexpr int ncclFloat64 = 8;
+}  // namespace
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* load_api(std::string* err) {
+  static NcclApi api;
+  static bool tried = false, ok = false;
+  if (tried) {
+    if (!ok && err) *err = "libnccl.so.2 unavailable";
+    return ok ? &api : nullptr;
+  }
+  tried = true;
+  api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!api.h) api.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!api.h) {
+    if (err) *err = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+    return nullptr;
+  }
+#define QT_SYM(field, name)                                              \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(api.h, name)); \
+  if (!api.field) {                                                      \
+    if (err) *err = std::string("missing NCCL symbol ") + name;          \
+    return nullptr;                                                      \
+  }
+  QT_SYM(GetUniqueId, "ncclGetUniqueId");
+  QT_SYM(CommInitRank, "ncclCommInitRank");
+  QT_SYM(CommDestroy, "ncclCommDestroy");
+  QT_SYM(Send, "ncclSend");
+  QT_SYM(Recv, "ncclRecv");
+  QT_SYM(GroupStart, "ncclGroupStart");
+  QT_SYM(GroupEnd, "ncclGroupEnd");
+  QT_SYM(AllGather, "ncclAllGather");
+  QT_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+  QT_SYM(GetErrorString, "ncclGetErrorString");
+#undef QT_SYM
+  ok = true;
+  return &api;
+}
+
+static bool nccl_ok(NcclApi* api, ncclResult_t r, const char* what,
+                    std::string* err) {
+  if (r == 0) return true;
+  if (err) *err = std::string(what) + ": " + api->GetErrorString(r);
+  return false;
+}
+
+bool Comm::unique_id(void* out128, std::string* err) {
+  NcclApi* api = load_api(err);
+  if (!api) return false;
+  ncclUniqueId id;
+  if (!nccl_ok(api, api->GetUniqueId(&id), "ncclGetUniqueId", err)) return false;
+  std::memcpy(out128, id.internal, 128);
+  return true;
+}
+
+Comm* Comm::create(const void* unique_id, int rank, int world, int device,
+                   std::string* err) {
+  NcclApi* api = load_api(err);
+  if (!api) return nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    if (err) *err = "cudaSetDevice failed";
+    return nullptr;
+  }
+  ncclUniqueId id;
+  std::memcpy(id.internal, unique_id, 128);
+  ncclComm_t c = nullptr;
+  if (!nccl_ok(api, api->CommInitRank(&c, world, id, rank), "ncclCommInitRank",
+               err))
+    return nullptr;
+  Comm* cm = new Comm();
+  cm->api_ = api;
+  cm->comm_ = c;
+  cm->rank_ = rank;
+  cm->world_ = world;
+  return cm;
+}
+
+Comm::~Comm() {
+  if (api_ && comm_) api_->CommDestroy(comm_);
+}
+
+bool Comm::sendrecv(int npeers, const int* peers, const void* const* sends,
+                    void* const* recvs, size_t bytes, cudaStream_t s,
+                    std::string* err) {
+  if (!nccl_ok(api_, api_->GroupStart(), "ncclGroupStart", err)) return false;
+  for (int i = 0; i < npeers; ++i) {
+    if (!nccl_ok(api_, api_->Send(sends[i], bytes, ncclUint8, peers[i], comm_, s),
+                 "ncclSend", err) ||
+        !nccl_ok(api_, api_->Recv(recvs[i], bytes, ncclUint8, peers[i], comm_, s),
+                 "ncclRecv", err)) {
+      api_->GroupEnd();
+      return false;
+    }
+  }
+  return nccl_ok(api_, api_->GroupEnd(), "ncclGroupEnd", err);
+}
+
+bool Comm::allgather_double(const double* in, double* out, cudaStream_t s,
+                            std::string* err) {
+  return nccl_ok(api_, api_->AllGather(in, out, 1, ncclFloat64, comm_, s),
+                 "ncclAllGather", err);
+}
+
+bool Comm::check_async(std::string* err) {
+  ncclResult_t r = 0;
+  api_->CommGetAsyncError(comm_, &r);
+  return nccl_ok(api_, r, "NCCL async error", err);
+}
+
+}  // namespace qtb

@@ -1,0 +1,63 @@
+// qt_kernels.hpp -- host-callable launchers of the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qt_ir.hpp"
+
+namespace qtb {
+
+struct KPass {
+  uint32_t k;        // tile bits
+  uint32_t nouter;   // local bits outside the tile
+  uint32_t nrounds;
+  uint32_t reg_bits; // R
+  uint64_t ntiles;
+  uint64_t gbase_hi; // shard offset in the global index (rank << nlocal)
+  const double2* src; // tiles are read from src and written to psi (may alias)
+  const DRound* rounds;
+  const DOp* ops;
+  int* flag;         // set to 1 if any written amplitude is non-finite
+  uint64_t lo_mask;    // physical bits of tile bits [0, k-R)  (thread bits)
+  uint64_t hi_mask;    // physical bits of tile bits [k-R, k)  (load slots)
+  uint64_t outer_mask; // local physical bits outside the tile
+};
+
+// Fused tile pass over a state of 2^nlocal amplitudes.
+cudaError_t launch_tile_pass(double2* psi, const KPass& p, int grid,
+                             cudaStream_t s);
+// Max resident CTAs per SM of the tile-pass kernel for (k, R).
+int tile_pass_occupancy(int k, int R);
+
+// Sets every amplitude to 0 and amplitude `index` to 1.
+cudaError_t launch_set_basis(double2* psi, uint64_t n, uint64_t index,
+                             cudaStream_t s);
+// Deterministic sum of |a|^2 in two fixed-shape levels; result to *out
+// (device). scratch must hold kNormBlocks doubles.
+constexpr int kNormBlocks = 1184;  // 8 x 148 SMs
+cudaError_t launch_norm(const double2* psi, uint64_t n, double* scratch,
+                        double* out, cudaStream_t s);
+// Swaps physical index bits b1 < b2 of a 2^nbits vector in place.
+cudaError_t launch_bitswap(double2* psi, int nbits, int b1, int b2,
+                           cudaStream_t s);
+// out[i] = psi[phys(first + i)] where phys permutes logical index bits by
+// perm (logical bit q -> physical bit perm[q]); nq <= 64.
+cudaError_t launch_gather(const double2* psi, double2* out, uint64_t first,
+                          uint64_t count, const uint8_t* perm_host, int nq,
+                          cudaStream_t s);
+// Sharded variant: physical index ph = perm(l); out = psi[ph & local mask]
+// if ph >> nlocal == rank, else 0.
+cudaError_t launch_gather_shard(const double2* psi, double2* out,
+                                uint64_t first, uint64_t count,
+                                const uint8_t* perm_host, int nq, int nlocal,
+                                uint64_t rank, cudaStream_t s);
+// FP64 throughput probe: iters x 16 independent FMA chains per thread.
+cudaError_t launch_fp64_probe(double* out, int grid, int block, int iters,
+                              cudaStream_t s);
+// Checks a range for non-finite values (flag |= 1).
+cudaError_t launch_check_finite(const double2* psi, uint64_t n, int* flag,
+                                cudaStream_t s);
+
+}  // namespace qtb

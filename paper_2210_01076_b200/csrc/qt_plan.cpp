@@ -1,0 +1,473 @@
+// qt_plan.cpp -- gate fusion and the fused-pass planner (host).
+//
+// Replaces the reference's per-net stage planner (plan.cpp:100-163), task
+// chunking / partition forming (plan.cpp:26-89) and the per-update job DAG
+// (engine.cpp:392-491). Where the reference materialises one stage per gate
+// (one full read+write of the touched blocks per gate), the planner packs
+// gates into PASSES: each pass streams the state through shared-memory
+// tiles of 2^k amplitudes exactly once and applies every gate whose
+// non-diagonal targets lie in the tile's qubit set. Inside a tile, gates are
+// grouped into ROUNDS of R register qubits (each thread holds 2^R amplitudes
+// in registers while the round's gates are applied).
+//
+// Legality: an op may be hoisted over earlier, not-yet-scheduled ops only if
+// it commutes with them qubit by qubit: two ops commute on a shared qubit
+// when both act diagonally there (diagonal targets, controls); see roles().
+#include "qt_plan.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <limits>
+#include <sstream>
+#include <stdexcept>
+
+namespace qtb {
+
+namespace {
+
+enum Role : uint8_t { ZRole = 1, XRole = 2 };
+
+struct QR {
+  int q;
+  Role r;
+};
+
+// Qubits an op touches with their roles (<= 3).
+inline int roles(const LOp& op, QR* out) {
+  int n = 0;
+  switch (op.kind) {
+    case LKind::Dense:
+    case LKind::Anti:
+      out[n++] = {op.target, XRole};
+      break;
+    case LKind::Diag:
+      out[n++] = {op.target, ZRole};
+      break;
+    case LKind::Swap:
+      out[n++] = {op.target, XRole};
+      out[n++] = {op.target2, XRole};
+      break;
+  }
+  if (op.control >= 0) out[n++] = {op.control, ZRole};
+  return n;
+}
+
+inline bool is_one(cplx c) { return c.re == 1.0 && c.im == 0.0; }
+inline bool is_zero(cplx c) { return c.re == 0.0 && c.im == 0.0; }
+
+void reclassify(LOp& op) {
+  const bool off0 = is_zero(op.m[1]) && is_zero(op.m[2]);
+  const bool diag0 = is_zero(op.m[0]) && is_zero(op.m[3]);
+  op.kind = off0 ? LKind::Diag : (diag0 ? LKind::Anti : LKind::Dense);
+}
+
+LOp to_phys(const LOp& op, const std::vector<int>& cur) {
+  LOp p = op;
+  p.target = cur[op.target];
+  if (op.target2 >= 0) p.target2 = cur[op.target2];
+  if (op.control >= 0) p.control = cur[op.control];
+  return p;
+}
+
+}  // namespace
+
+uint32_t dtype_of(const LOp& op) {
+  switch (op.kind) {
+    case LKind::Swap:
+      return D_SWAP2;
+    case LKind::Anti:
+      if (is_one(op.m[1]) && is_one(op.m[2])) return D_XPERM;
+      return D_ANTI;
+    case LKind::Diag:
+      if (is_one(op.m[0])) {
+        if (op.m[3].re == -1.0 && op.m[3].im == 0.0) return D_SIGN;
+        return D_PHASE1;
+      }
+      return D_DIAG;
+    case LKind::Dense: {
+      bool real = true;
+      for (int k = 0; k < 4; ++k) real = real && op.m[k].im == 0.0;
+      return real ? D_REAL : D_DENSE;
+    }
+  }
+  return D_DENSE;
+}
+
+double op_fp64_per_amp(const LOp& op) {
+  switch (dtype_of(op)) {
+    case D_DENSE: return 8.0;
+    case D_REAL: return 4.0;
+    case D_DIAG: return 4.0;
+    case D_PHASE1: return 4.0;
+    case D_ANTI: return 4.0;
+    default: return 0.0;
+  }
+}
+
+void fuse_ops(std::vector<LOp>& ops, int nqubits) {
+  std::vector<LOp> out;
+  out.reserve(ops.size());
+  std::vector<int> last(nqubits, -1);  // index in out of the latest op on q
+  std::vector<char> dead;
+  dead.reserve(ops.size());
+  for (const LOp& op : ops) {
+    const bool single = op.kind != LKind::Swap && op.control < 0;
+    if (single) {
+      const int p = last[op.target];
+      if (p >= 0 && !dead[p]) {
+        LOp& prev = out[p];
+        if (prev.kind != LKind::Swap && prev.control < 0 &&
+            prev.target == op.target) {
+          // apply prev first, then op: M = op.m * prev.m
+          cplx r[4];
+          r[0] = cadd(cmul(op.m[0], prev.m[0]), cmul(op.m[1], prev.m[2]));
+          r[1] = cadd(cmul(op.m[0], prev.m[1]), cmul(op.m[1], prev.m[3]));
+          r[2] = cadd(cmul(op.m[2], prev.m[0]), cmul(op.m[3], prev.m[2]));
+          r[3] = cadd(cmul(op.m[2], prev.m[1]), cmul(op.m[3], prev.m[3]));
+          for (int k = 0; k < 4; ++k) prev.m[k] = r[k];
+          reclassify(prev);
+          continue;
+        }
+      }
+    }
+    out.push_back(op);
+    dead.push_back(0);
+    const int idx = static_cast<int>(out.size()) - 1;
+    last[op.target] = idx;
+    if (op.target2 >= 0) last[op.target2] = idx;
+    if (op.control >= 0) last[op.control] = idx;
+  }
+  // drop exact identities (e.g. RZ(0), merged X.X)
+  std::vector<LOp> kept;
+  kept.reserve(out.size());
+  for (const LOp& op : out) {
+    if (op.kind == LKind::Diag && is_one(op.m[0]) && is_one(op.m[3])) continue;
+    kept.push_back(op);
+  }
+  ops.swap(kept);
+}
+
+DOp encode_op(const LOp& op, const std::vector<int>& tile_phys,
+              const std::vector<int>& reg) {
+  DOp d{};
+  d.type = dtype_of(op);
+  auto tile_index = [&](int phys) -> int {
+    for (size_t i = 0; i < tile_phys.size(); ++i)
+      if (tile_phys[i] == phys) return static_cast<int>(i);
+    return -1;
+  };
+  auto reg_slot = [&](int phys) -> int {
+    const int ti = tile_index(phys);
+    for (size_t i = 0; i < reg.size(); ++i)
+      if (reg[i] == ti) return static_cast<int>(i);
+    return -1;
+  };
+  if (op.kind == LKind::Diag) {
+    const int ti = tile_index(op.target);
+    if (ti >= 0) d.dl = 1u << ti;
+    else d.dg = 1ull << op.target;
+  } else {
+    d.a = static_cast<uint32_t>(reg_slot(op.target));
+    if (op.kind == LKind::Swap) d.b = static_cast<uint32_t>(reg_slot(op.target2));
+  }
+  if (op.control >= 0) {
+    const int ti = tile_index(op.control);
+    if (ti >= 0) d.lmask = 1u << ti;
+    else d.gmask = 1ull << op.control;
+  }
+  for (int k = 0; k < 4; ++k) {
+    d.m[2 * k] = op.m[k].re;
+    d.m[2 * k + 1] = op.m[k].im;
+  }
+  return d;
+}
+
+namespace {
+
+// Splits the ops of one pass (physical qubits, application order) into
+// register rounds of R tile bits.
+void make_rounds(PlanPass& pass, int R, int nphys) {
+  const int k = static_cast<int>(pass.tile_phys.size());
+  std::vector<int> tix(nphys, -1);
+  for (int i = 0; i < k; ++i) tix[pass.tile_phys[i]] = i;
+  std::vector<int> remaining(pass.ops.size());
+  for (size_t i = 0; i < remaining.size(); ++i) remaining[i] = static_cast<int>(i);
+  std::vector<char> blockAll(nphys), blockX(nphys);
+  std::vector<char> inReg(k);
+  while (!remaining.empty()) {
+    std::fill(blockAll.begin(), blockAll.end(), 0);
+    std::fill(blockX.begin(), blockX.end(), 0);
+    std::fill(inReg.begin(), inReg.end(), 0);
+    PlanRound round;
+    std::vector<int> rest;
+    QR rl[3];
+    for (int idx : remaining) {
+      const LOp& op = pass.ops[idx];
+      const int nr = roles(op, rl);
+      bool can = true;
+      for (int t = 0; t < nr; ++t) {
+        if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
+      }
+      if (can) {
+        int need[2], nn = 0;
+        for (int t = 0; t < nr; ++t) {
+          if (rl[t].r != XRole) continue;
+          const int ti = tix[rl[t].q];
+          if (!inReg[ti]) {
+            bool dup = false;
+            for (int u = 0; u < nn; ++u) dup = dup || need[u] == ti;
+            if (!dup) need[nn++] = ti;
+          }
+        }
+        if (static_cast<int>(round.reg.size()) + nn <= R) {
+          for (int u = 0; u < nn; ++u) {
+            inReg[need[u]] = 1;
+            round.reg.push_back(need[u]);
+          }
+          round.ops.push_back(idx);
+        } else {
+          can = false;
+        }
+      }
+      if (!can) {
+        rest.push_back(idx);
+        for (int t = 0; t < nr; ++t) {
+          if (rl[t].r == XRole) blockAll[rl[t].q] = 1;
+          else blockX[rl[t].q] = 1;
+        }
+      }
+    }
+    // pad the register set with the highest unused tile bits
+    for (int ti = k - 1; static_cast<int>(round.reg.size()) < R && ti >= 0; --ti) {
+      if (!inReg[ti]) {
+        inReg[ti] = 1;
+        round.reg.push_back(ti);
+      }
+    }
+    pass.rounds.push_back(std::move(round));
+    remaining.swap(rest);
+  }
+}
+
+}  // namespace
+
+Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
+               const std::vector<int>& perm, const PlanOptions& opt) {
+  Plan plan;
+  plan.nqubits = nqubits;
+  plan.nlocal = nlocal;
+  plan.perm_before = perm;
+  std::vector<int> cur = perm;  // logical -> physical
+  std::vector<int> inv(nqubits);
+  for (int q = 0; q < nqubits; ++q) inv[cur[q]] = q;
+
+  const int K = std::min(opt.tile_bits, nlocal);
+  // keep at least two free tile slots so any op (SWAP: two targets) fits
+  const int m = std::max(0, std::min(opt.low_bits, K - 2));
+  const int R = std::min(opt.reg_bits, K);
+  const size_t nops = ops.size();
+  std::vector<char> done(nops, 0);
+  size_t first = 0;
+  QR rl[3];
+
+  std::vector<char> blockAll(nqubits), blockX(nqubits), inQ(nlocal);
+  while (true) {
+    while (first < nops && done[first]) ++first;
+    if (first >= nops) break;
+
+    // ---- exchange when the head op needs a global (sharded) qubit --------
+    bool head_global = false;
+    {
+      const int nr = roles(ops[first], rl);
+      for (int t = 0; t < nr; ++t)
+        if (rl[t].r == XRole && cur[rl[t].q] >= nlocal) head_global = true;
+    }
+    if (head_global) {
+      // global physical bits with upcoming X-role use, in order of need
+      std::vector<int> need_g;
+      std::vector<size_t> next_x(nqubits, std::numeric_limits<size_t>::max());
+      size_t scanned = 0;
+      for (size_t i = first; i < nops && scanned < static_cast<size_t>(opt.lookahead); ++i) {
+        if (done[i]) continue;
+        ++scanned;
+        const int nr = roles(ops[i], rl);
+        for (int t = 0; t < nr; ++t) {
+          if (rl[t].r != XRole) continue;
+          const int q = rl[t].q;
+          if (next_x[q] == std::numeric_limits<size_t>::max()) next_x[q] = i;
+          const int p = cur[q];
+          if (p >= nlocal && std::find(need_g.begin(), need_g.end(), p) == need_g.end())
+            need_g.push_back(p);
+        }
+      }
+      const int g = nqubits - nlocal;
+      if (static_cast<int>(need_g.size()) > g) need_g.resize(g);
+      // victims: among the top local bits, the furthest next X use first
+      const int ncand = std::min(nlocal, std::max(4, static_cast<int>(need_g.size())));
+      std::vector<int> cand;
+      for (int p = nlocal - 1; p >= nlocal - ncand; --p) cand.push_back(p);
+      std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {
+        return next_x[inv[a]] > next_x[inv[b]];
+      });
+      PlanPass ex;
+      ex.kind = PlanPass::Exchange;
+      for (size_t i = 0; i < need_g.size(); ++i) {
+        const int G = need_g[i], V = cand[i];
+        ex.exchange.emplace_back(G, V);
+        const int qg = inv[G], qv = inv[V];
+        cur[qg] = V;
+        cur[qv] = G;
+        inv[V] = qg;
+        inv[G] = qv;
+      }
+      plan.passes.push_back(std::move(ex));
+      continue;
+    }
+
+    // ---- tile pass --------------------------------------------------------
+    std::fill(blockAll.begin(), blockAll.end(), 0);
+    std::fill(blockX.begin(), blockX.end(), 0);
+    std::fill(inQ.begin(), inQ.end(), 0);
+    for (int b = 0; b < m; ++b) inQ[b] = 1;
+    int qcount = m;
+    int nblocked = 0;
+    PlanPass pass;
+    size_t scanned = 0;
+    for (size_t i = first; i < nops && scanned < static_cast<size_t>(opt.lookahead); ++i) {
+      if (done[i]) continue;
+      ++scanned;
+      const LOp& op = ops[i];
+      const int nr = roles(op, rl);
+      bool can = true;
+      for (int t = 0; t < nr; ++t) {
+        if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
+      }
+      if (can) {
+        int need[2], nn = 0;
+        for (int t = 0; t < nr; ++t) {
+          if (rl[t].r != XRole) continue;
+          const int p = cur[rl[t].q];
+          if (p >= nlocal) {
+            can = false;
+            break;
+          }
+          if (!inQ[p]) {
+            bool dup = false;
+            for (int u = 0; u < nn; ++u) dup = dup || need[u] == p;
+            if (!dup) need[nn++] = p;
+          }
+        }
+        if (can && qcount + nn <= K) {
+          for (int u = 0; u < nn; ++u) inQ[need[u]] = 1;
+          qcount += nn;
+        } else {
+          can = false;
+        }
+      }
+      if (can) {
+        done[i] = 1;
+        pass.ops.push_back(to_phys(op, cur));
+      } else {
+        for (int t = 0; t < nr; ++t) {
+          if (rl[t].r == XRole) {
+            if (!blockAll[rl[t].q]) {
+              blockAll[rl[t].q] = 1;
+              ++nblocked;
+            }
+          } else {
+            blockX[rl[t].q] = 1;
+          }
+        }
+        if (nblocked == nqubits) break;
+      }
+    }
+    // complete the tile to K bits with the lowest unused local bits
+    for (int p = 0; p < nlocal && qcount < K; ++p) {
+      if (!inQ[p]) {
+        inQ[p] = 1;
+        ++qcount;
+      }
+    }
+    for (int p = 0; p < nlocal; ++p)
+      if (inQ[p]) pass.tile_phys.push_back(p);
+    if (pass.ops.empty()) throw std::logic_error("planner made no progress");
+    make_rounds(pass, R, nqubits);
+    plan.passes.push_back(std::move(pass));
+  }
+  plan.perm_after = cur;
+  plan.gates = nops;
+  return plan;
+}
+
+std::string plan_to_json(const Plan& p, bool detail) {
+  std::ostringstream os;
+  const unsigned long long amps = 1ull << p.nlocal;
+  os << "{\"nqubits\":" << p.nqubits << ",\"nlocal\":" << p.nlocal
+     << ",\"ops\":" << p.gates << ",\"passes\":[";
+  for (size_t i = 0; i < p.passes.size(); ++i) {
+    const PlanPass& ps = p.passes[i];
+    if (i) os << ",";
+    if (ps.kind == PlanPass::Exchange) {
+      os << "{\"kind\":\"exchange\",\"swap\":[";
+      for (size_t e = 0; e < ps.exchange.size(); ++e) {
+        if (e) os << ",";
+        os << "[" << ps.exchange[e].first << "," << ps.exchange[e].second << "]";
+      }
+      os << "]}";
+      continue;
+    }
+    double fp = 0.0;
+    for (const LOp& op : ps.ops) fp += op_fp64_per_amp(op);
+    os << "{\"kind\":\"tile\",\"tile\":[";
+    for (size_t t = 0; t < ps.tile_phys.size(); ++t) {
+      if (t) os << ",";
+      os << ps.tile_phys[t];
+    }
+    os << "],\"rounds\":" << ps.rounds.size() << ",\"ops\":" << ps.ops.size()
+       << ",\"gates\":[";
+    std::vector<uint32_t> gs;
+    for (const LOp& op : ps.ops) gs.push_back(op.gate);
+    std::sort(gs.begin(), gs.end());
+    gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+    for (size_t t = 0; t < gs.size(); ++t) {
+      if (t) os << ",";
+      os << gs[t];
+    }
+    os << "],\"read_amps\":" << amps << ",\"write_amps\":" << amps
+       << ",\"fp64_per_amp\":" << fp;
+    if (detail) {
+      os << ",\"round_detail\":[";
+      char num[64];
+      for (size_t r = 0; r < ps.rounds.size(); ++r) {
+        const PlanRound& pr = ps.rounds[r];
+        if (r) os << ",";
+        os << "{\"reg\":[";
+        for (size_t i = 0; i < pr.reg.size(); ++i) os << (i ? "," : "") << pr.reg[i];
+        os << "],\"ops\":[";
+        for (size_t o = 0; o < pr.ops.size(); ++o) {
+          const DOp d = encode_op(ps.ops[pr.ops[o]], ps.tile_phys, pr.reg);
+          if (o) os << ",";
+          os << "[" << d.type << "," << d.a << "," << d.b << "," << d.lmask << ","
+             << d.gmask << "," << d.dl << "," << d.dg;
+          for (int k = 0; k < 8; ++k) {
+            std::snprintf(num, sizeof(num), ",%.17g", d.m[k]);
+            os << num;
+          }
+          os << "]";
+        }
+        os << "]}";
+      }
+      os << "]";
+    }
+    os << "}";
+  }
+  os << "],\"perm_after\":[";
+  for (size_t q = 0; q < p.perm_after.size(); ++q) {
+    if (q) os << ",";
+    os << p.perm_after[q];
+  }
+  os << "]}";
+  return os.str();
+}
+
+}  // namespace qtb

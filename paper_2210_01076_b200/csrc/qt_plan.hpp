@@ -1,0 +1,43 @@
+// qt_plan.hpp -- fusion and pass planning (host).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "qt_ir.hpp"
+
+namespace qtb {
+
+struct PlanOptions {
+  int tile_bits = 12;  // qubits per shared-memory tile
+  int low_bits = 4;    // lowest physical bits always in the tile (coalescing)
+  int reg_bits = 3;    // qubits per register round (2^reg amplitudes/thread)
+  int lookahead = 4096;// ops scanned per pass
+};
+
+// Merges runs of uncontrolled single-qubit ops on the same qubit into one
+// 2x2 (matrix product) and drops exact identities. Order-preserving:
+// an op merges into the latest op touching its qubit only.
+void fuse_ops(std::vector<LOp>& ops, int nqubits);
+
+// Plans `ops` (logical qubits) for a state of nqubits bits of which the top
+// nqubits - nlocal are sharded (global). perm maps logical -> physical and
+// is updated by the exchanges the plan inserts.
+Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
+               const std::vector<int>& perm, const PlanOptions& opt);
+
+// Device op for `op` (physical qubits) inside a pass whose tile holds the
+// physical bits tile_phys and whose round uses register tile-bits reg.
+DOp encode_op(const LOp& op, const std::vector<int>& tile_phys,
+              const std::vector<int>& reg);
+
+// Kernel-side op type of an LOp.
+uint32_t dtype_of(const LOp& op);
+
+// detail=true adds every round's register bits and encoded device ops.
+std::string plan_to_json(const Plan& p, bool detail = false);
+
+// FP64 pipe operations per amplitude of an op (roofline accounting).
+double op_fp64_per_amp(const LOp& op);
+
+}  // namespace qtb

@@ -1,0 +1,573 @@
+// qt_state.cpp -- device state, plan upload, stream-ordered pass launches,
+// qubit exchanges, readout and checkpoints.
+//
+// Replaces the reference's storage and scheduling layer: per-stage COW
+// block stores (engine.hpp:18-29, resolve_block engine.cpp:291-301,
+// input_block_copy engine.cpp:303-313), the one-shot thread pool spawned per
+// update (executor.cpp:64-89) and the readout (engine.cpp:510-564). The state
+// is one flat HBM buffer of double2 (bit-compatible with
+// std::complex<double>); gate application is a sequence of fused tile passes
+// launched in order on one CUDA stream.
+#include "qt_state.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "qt_gates.hpp"
+#include "qt_kernels.hpp"
+
+namespace qtb {
+
+void fail(int code, const std::string& msg) { throw QtError{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation)
+    fail(QT_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+    fail(QT_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+  fail(QT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+int ilog2(uint64_t x) {
+  int r = 0;
+  while ((1ull << r) < x) ++r;
+  return r;
+}
+}  // namespace
+
+State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
+             const qt_config* cfg)
+    : n_(nqubits), mode_(mode), rank_(rank), world_(shards) {
+  if (nqubits < 1 || nqubits > 40) fail(QT_ERR_BAD_QUBIT, "qubit count must be in [1, 40]");
+  if (shards < 1 || (shards & (shards - 1)) != 0)
+    fail(QT_ERR_ARG, "shard count must be a power of two");
+  const int g = ilog2(static_cast<uint64_t>(shards));
+  nlocal_ = n_ - g;
+  if (mode != Mode::Single && nlocal_ < 4)
+    fail(QT_ERR_ARG, "too many shards for this qubit count");
+  buf_bits_ = mode == Mode::Loopback ? n_ : nlocal_;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    fail(QT_ERR_NO_DEVICE, "no CUDA device visible");
+  device_ = (cfg && cfg->device >= 0) ? cfg->device : 0;
+  if (!(cfg && cfg->device >= 0)) cudaGetDevice(&device_);
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_);
+
+  if (cfg && cfg->tile_qubits > 0)
+    opt_.tile_bits = std::min(cfg->tile_qubits, kMaxTileBits);
+  opt_.reg_bits = kMaxRegBits;
+
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaMalloc(&psi_, sizeof(double2) << buf_bits_), "state allocation");
+  pool_.push_back(psi_);
+  cuda_check(cudaMalloc(&d_scratch_, sizeof(double) * (kNormBlocks + 64)), "scratch");
+  cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
+  cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "flag init");
+  cuda_check(cudaMallocHost(&h_flag_, sizeof(int)), "pinned flag");
+  cuda_check(cudaEventCreateWithFlags(&stage_free_, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreate(&ev0_), "event");
+  cuda_check(cudaEventCreate(&ev1_), "event");
+  perm_.resize(n_);
+  for (int q = 0; q < n_; ++q) perm_[q] = q;
+
+  if (mode == Mode::Nccl) {
+    std::string err;
+    comm_.reset(Comm::create(nccl_id, rank, shards, device_, &err));
+    if (!comm_) fail(QT_ERR_NCCL, err);
+  }
+  set_basis(0);
+}
+
+State::~State() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& kv : ckpt_) cudaFree(kv.second.first);
+  for (auto& t : timings_) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  comm_.reset();
+  for (double2* b : pool_) cudaFree(b);
+  cudaFree(d_scratch_);
+  cudaFree(d_flag_);
+  cudaFree(d_plan_);
+  cudaFree(d_tmp_);
+  if (h_flag_) cudaFreeHost(h_flag_);
+  if (h_stage_) cudaFreeHost(h_stage_);
+  if (stage_free_) cudaEventDestroy(stage_free_);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void State::set_basis(uint64_t index) {
+  if (n_ < 64 && index >= (1ull << n_)) fail(QT_ERR_ARG, "basis index out of range");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  for (int q = 0; q < n_; ++q) perm_[q] = q;
+  uint64_t local = index;
+  uint64_t target = ~0ull;  // index within this buffer, or none
+  if (mode_ == Mode::Nccl) {
+    const uint64_t owner = index >> nlocal_;
+    local = index & ((1ull << nlocal_) - 1);
+    if (owner == static_cast<uint64_t>(rank_)) target = local;
+  } else {
+    target = local;
+  }
+  cuda_check(launch_set_basis(psi_, buffer_amps(), target, stream_), "set_basis");
+}
+
+void State::write(uint64_t first, uint64_t count, const double* src) {
+  if (n_ < 64 && (first > (1ull << n_) || count > (1ull << n_) - first))
+    fail(QT_ERR_ARG, "amplitude range out of bounds");
+  for (int q = 0; q < n_; ++q)
+    if (perm_[q] != q) fail(QT_ERR_ARG, "write needs the canonical qubit order (call set_basis)");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  uint64_t lo = first, hi = first + count;
+  if (mode_ == Mode::Nccl) {
+    const uint64_t s0 = static_cast<uint64_t>(rank_) << nlocal_;
+    const uint64_t s1 = s0 + (1ull << nlocal_);
+    lo = std::max(lo, s0);
+    hi = std::min(hi, s1);
+    if (lo >= hi) return;
+    cuda_check(cudaMemcpyAsync(psi_ + (lo - s0), src + 2 * (lo - first),
+                               (hi - lo) * sizeof(double2),
+                               cudaMemcpyHostToDevice, stream_),
+               "write");
+  } else {
+    cuda_check(cudaMemcpyAsync(psi_ + lo, src, count * sizeof(double2),
+                               cudaMemcpyHostToDevice, stream_),
+               "write");
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "write sync");
+}
+
+void State::read(uint64_t first, uint64_t count, double* dst) {
+  if (n_ < 64 && (first > (1ull << n_) || count > (1ull << n_) - first))
+    fail(QT_ERR_ARG, "amplitude range out of bounds");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  bool identity = true;
+  for (int q = 0; q < n_; ++q) identity = identity && perm_[q] == q;
+  if (identity && mode_ != Mode::Nccl) {
+    cuda_check(cudaMemcpyAsync(dst, psi_ + first, count * sizeof(double2),
+                               cudaMemcpyDeviceToHost, stream_),
+               "read");
+    sync();
+    return;
+  }
+  // gather through the logical->physical map, in device-sized chunks
+  const uint64_t chunk = 1ull << 22;
+  if (d_tmp_amps_ < std::min(count, chunk)) {
+    cudaFree(d_tmp_);
+    d_tmp_ = nullptr;
+    d_tmp_amps_ = std::min(count, chunk);
+    cuda_check(cudaMalloc(&d_tmp_, d_tmp_amps_ * sizeof(double2)), "gather buffer");
+  }
+  std::vector<uint8_t> pm(n_);
+  for (int q = 0; q < n_; ++q) pm[q] = static_cast<uint8_t>(perm_[q]);
+  for (uint64_t off = 0; off < count; off += chunk) {
+    const uint64_t c = std::min(chunk, count - off);
+    if (mode_ == Mode::Nccl) {
+      cuda_check(launch_gather_shard(psi_, d_tmp_, first + off, c, pm.data(), n_,
+                                     nlocal_, static_cast<uint64_t>(rank_), stream_),
+                 "gather");
+    } else {
+      cuda_check(launch_gather(psi_, d_tmp_, first + off, c, pm.data(), n_, stream_),
+                 "gather");
+    }
+    cuda_check(cudaMemcpyAsync(dst + 2 * off, d_tmp_, c * sizeof(double2),
+                               cudaMemcpyDeviceToHost, stream_),
+               "read");
+  }
+  sync();
+}
+
+Plan State::plan(const std::vector<LOp>& ops) const {
+  return make_plan(ops, n_, nlocal_, perm_, opt_);
+}
+
+void State::apply(const qt_gate* gates, size_t count) {
+  std::vector<LOp> ops;
+  ops.reserve(count);
+  std::string err;
+  for (size_t i = 0; i < count; ++i) {
+    const int rc = lower_gate(gates[i], n_, static_cast<uint32_t>(i), ops, &err);
+    if (rc != QT_OK) fail(rc, err);
+  }
+  fuse_ops(ops, n_);
+  apply_ops(ops, count);
+}
+
+int State::grow_pool(int count, double max_fraction_of_free) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const size_t bytes = sizeof(double2) * buffer_amps();
+  while (static_cast<int>(pool_.size()) < count) {
+    size_t fre = 0, tot = 0;
+    cudaMemGetInfo(&fre, &tot);
+    // keep a reserve for plan / exchange buffers and the caller
+    const size_t reserve = std::max<size_t>(tot / 50, size_t(2) << 30);
+    if (fre < reserve + bytes) break;
+    if (static_cast<double>(bytes) > max_fraction_of_free * static_cast<double>(fre)) break;
+    double2* b = nullptr;
+    if (cudaMalloc(&b, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      break;
+    }
+    pool_.push_back(b);
+  }
+  return static_cast<int>(pool_.size());
+}
+
+void State::bind(int i, const std::vector<int>& perm) {
+  if (i < 0 || i >= static_cast<int>(pool_.size())) fail(QT_ERR_ARG, "bad buffer");
+  bound_ = i;
+  psi_ = pool_[i];
+  perm_ = perm;
+}
+
+void State::apply_ops(const std::vector<LOp>& ops, uint64_t ngates,
+                      const double2* src, const std::vector<int>* src_perm) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  if (src == psi_) src = nullptr;
+  if (src && src_perm) perm_ = *src_perm;
+  const auto t0 = std::chrono::steady_clock::now();
+  const Plan p = plan(ops);
+  const auto t1 = std::chrono::steady_clock::now();
+  stats = qt_run_stats{};
+  stats.gates = ngates;
+  stats.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  upload_and_launch(p, src);
+  perm_ = p.perm_after;
+}
+
+void State::ensure_device_bytes(size_t bytes) {
+  if (bytes <= d_plan_cap_) return;
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  cudaFree(d_plan_);
+  d_plan_ = nullptr;
+  d_plan_cap_ = std::max(bytes, d_plan_cap_ * 2);
+  cuda_check(cudaMalloc(&d_plan_, d_plan_cap_), "plan buffer");
+}
+
+void State::upload_and_launch(const Plan& plan, const double2* src) {
+  // ---- flatten rounds + ops --------------------------------------------
+  std::vector<DRound> rounds;
+  std::vector<DOp> dops;
+  struct PassRef {
+    size_t round_first, round_count;
+  };
+  std::vector<PassRef> refs(plan.passes.size());
+  for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
+    const PlanPass& ps = plan.passes[pi];
+    refs[pi].round_first = rounds.size();
+    refs[pi].round_count = 0;
+    if (ps.kind != PlanPass::Tile) continue;
+    for (const PlanRound& pr : ps.rounds) {
+      DRound dr{};
+      dr.nreg = static_cast<uint8_t>(pr.reg.size());
+      for (size_t i = 0; i < pr.reg.size() && i < kMaxRegBits; ++i)
+        dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
+      dr.op_first = static_cast<uint32_t>(dops.size());
+      dr.op_count = static_cast<uint32_t>(pr.ops.size());
+      for (int idx : pr.ops) dops.push_back(encode_op(ps.ops[idx], ps.tile_phys, pr.reg));
+      rounds.push_back(dr);
+      refs[pi].round_count++;
+    }
+  }
+  const size_t rbytes = (rounds.size() * sizeof(DRound) + 255) & ~size_t(255);
+  const size_t total = rbytes + dops.size() * sizeof(DOp);
+  if (total > 0) {
+    ensure_device_bytes(total);
+    if (total > h_stage_cap_) {
+      cuda_check(cudaEventSynchronize(stage_free_), "stage sync");
+      if (h_stage_) cudaFreeHost(h_stage_);
+      h_stage_cap_ = std::max(total, h_stage_cap_ * 2);
+      cuda_check(cudaMallocHost(&h_stage_, h_stage_cap_), "pinned stage");
+    } else {
+      cuda_check(cudaEventSynchronize(stage_free_), "stage sync");
+    }
+    std::memcpy(h_stage_, rounds.data(), rounds.size() * sizeof(DRound));
+    std::memcpy(static_cast<char*>(h_stage_) + rbytes, dops.data(),
+                dops.size() * sizeof(DOp));
+    cuda_check(cudaMemcpyAsync(d_plan_, h_stage_, total, cudaMemcpyHostToDevice, stream_),
+               "plan upload");
+    cuda_check(cudaEventRecord(stage_free_, stream_), "event");
+  }
+  const DRound* d_rounds = static_cast<const DRound*>(d_plan_);
+  const DOp* d_ops = reinterpret_cast<const DOp*>(static_cast<char*>(d_plan_) + rbytes);
+
+  // ---- launch -------------------------------------------------------------
+  cuda_check(cudaEventRecord(ev0_, stream_), "event");
+  // per-launch events accumulate until last_timings() collects them
+  size_t timing_idx = timings_used_;
+  auto tstart = [&](int kind) {
+    if (!timing_) return;
+    if (timing_idx >= timings_.size()) {
+      PassTiming t;
+      cudaEventCreate(&t.start);
+      cudaEventCreate(&t.stop);
+      timings_.push_back(t);
+    }
+    timings_[timing_idx].kind = kind;
+    cudaEventRecord(timings_[timing_idx].start, stream_);
+  };
+  auto tstop = [&]() {
+    if (!timing_) return;
+    cudaEventRecord(timings_[timing_idx].stop, stream_);
+    ++timing_idx;
+  };
+  const uint64_t buf_mask = buffer_amps() - 1;
+  // out-of-place start: the first tile pass reads src; otherwise copy
+  if (src && (plan.passes.empty() || plan.passes[0].kind != PlanPass::Tile)) {
+    cuda_check(cudaMemcpyAsync(psi_, src, sizeof(double2) * buffer_amps(),
+                               cudaMemcpyDeviceToDevice, stream_),
+               "state copy");
+    stats.kernel_launches += 1;
+    stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
+    src = nullptr;
+  }
+  for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
+    const PlanPass& ps = plan.passes[pi];
+    if (ps.kind == PlanPass::Exchange) {
+      tstart(1);
+      exchange(ps);
+      tstop();
+      stats.swaps += 1;
+      stats.kernel_launches += ps.exchange.size();
+      continue;
+    }
+    const int k = static_cast<int>(ps.tile_phys.size());
+    const int R = std::min(opt_.reg_bits, k);
+    KPass kp{};
+    kp.k = static_cast<uint32_t>(k);
+    kp.reg_bits = static_cast<uint32_t>(R);
+    kp.nrounds = static_cast<uint32_t>(refs[pi].round_count);
+    kp.rounds = d_rounds + refs[pi].round_first;
+    kp.ops = d_ops;
+    kp.flag = d_flag_;
+    kp.src = src ? src : psi_;
+    src = nullptr;
+    uint64_t tile_mask = 0;
+    for (int i = 0; i < k; ++i) {
+      const uint64_t b = 1ull << ps.tile_phys[i];
+      tile_mask |= b;
+      if (i < k - R) kp.lo_mask |= b;
+      else kp.hi_mask |= b;
+    }
+    kp.outer_mask = buf_mask & ~tile_mask;
+    kp.nouter = static_cast<uint32_t>(buf_bits_ - k);
+    kp.ntiles = 1ull << (buf_bits_ - k);
+    kp.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
+    const int occ = std::max(1, tile_pass_occupancy(k, R));
+    const uint64_t cap = static_cast<uint64_t>(occ) * sms_;
+    const int grid = static_cast<int>(std::min<uint64_t>(kp.ntiles, cap));
+    tstart(0);
+    cuda_check(launch_tile_pass(psi_, kp, grid, stream_), "tile pass launch");
+    tstop();
+    stats.passes += 1;
+    stats.kernel_launches += 1;
+    stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
+  }
+  cuda_check(cudaEventRecord(ev1_, stream_), "event");
+  timings_used_ = timing_idx;
+  stats.rewritten_amplitudes = plan.passes.empty() ? 0 : (1ull << n_);
+}
+
+void State::exchange(const PlanPass& pass) {
+  if (mode_ == Mode::Loopback) {
+    for (const auto& gv : pass.exchange)
+      cuda_check(launch_bitswap(psi_, buf_bits_, gv.first, gv.second, stream_),
+                 "bitswap");
+    stats.exchanged_bytes += pass.exchange.size() * (buffer_amps() / 2) * sizeof(double2);
+    return;
+  }
+  if (mode_ != Mode::Nccl) fail(QT_ERR_ARG, "exchange on an unsharded state");
+  const int k = static_cast<int>(pass.exchange.size());
+  std::vector<int> gbit(k), vbit(k);
+  uint64_t vmask = 0;
+  int minv = nlocal_;
+  for (int j = 0; j < k; ++j) {
+    gbit[j] = pass.exchange[j].first - nlocal_;
+    vbit[j] = pass.exchange[j].second;
+    vmask |= 1ull << vbit[j];
+    minv = std::min(minv, vbit[j]);
+  }
+  int rho = 0;
+  for (int j = 0; j < k; ++j) rho |= ((rank_ >> gbit[j]) & 1) << j;
+  const uint64_t run_len = 1ull << minv;
+  const uint64_t region = 1ull << (nlocal_ - k);
+  const uint64_t runs = region / run_len;
+  const int npeer = (1 << k) - 1;
+  // receive buffer: at most 1/8 of the shard, split across the peers
+  uint64_t want = std::max<uint64_t>(1, (1ull << nlocal_) / 8);
+  want = std::min<uint64_t>(want, 1ull << 27);  // 2 GiB
+  if (d_tmp_amps_ < want) {
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    cudaFree(d_tmp_);
+    d_tmp_ = nullptr;
+    d_tmp_amps_ = want;
+    cuda_check(cudaMalloc(&d_tmp_, d_tmp_amps_ * sizeof(double2)), "exchange buffer");
+  }
+  uint64_t piece = run_len;
+  while (piece * npeer > d_tmp_amps_ && piece > 1) piece >>= 1;
+  const uint64_t per_run = run_len / piece;
+  // bits >= minv that are not V bits enumerate the runs of a region
+  uint64_t above = 0;
+  for (int b = minv; b < nlocal_; ++b)
+    if (!((vmask >> b) & 1)) above |= 1ull << b;
+  auto pdep = [](uint64_t x, uint64_t mask) {
+    uint64_t r = 0;
+    for (uint64_t b = 1; mask; b <<= 1) {
+      const uint64_t low = mask & (~mask + 1);
+      if (x & b) r |= low;
+      mask ^= low;
+    }
+    return r;
+  };
+  std::vector<int> peers;
+  std::vector<int> cval;
+  for (int c = 0; c < (1 << k); ++c) {
+    if (c == rho) continue;
+    int pr = rank_;
+    for (int j = 0; j < k; ++j) {
+      pr &= ~(1 << gbit[j]);
+      pr |= ((c >> j) & 1) << gbit[j];
+    }
+    peers.push_back(pr);
+    cval.push_back(c);
+  }
+  std::vector<const void*> sends(npeer);
+  std::vector<void*> recvs(npeer);
+  std::string err;
+  for (uint64_t r = 0; r < runs; ++r) {
+    const uint64_t run_base = pdep(r, above);
+    for (uint64_t w = 0; w < per_run; ++w) {
+      for (int i = 0; i < npeer; ++i) {
+        uint64_t vb = 0;
+        for (int j = 0; j < k; ++j) vb |= static_cast<uint64_t>((cval[i] >> j) & 1) << vbit[j];
+        sends[i] = psi_ + (run_base | vb) + w * piece;
+        recvs[i] = d_tmp_ + static_cast<uint64_t>(i) * piece;
+      }
+      if (!comm_->sendrecv(npeer, peers.data(), sends.data(), recvs.data(),
+                           piece * sizeof(double2), stream_, &err))
+        fail(QT_ERR_NCCL, err);
+      for (int i = 0; i < npeer; ++i)
+        cuda_check(cudaMemcpyAsync(const_cast<void*>(sends[i]), recvs[i],
+                                   piece * sizeof(double2),
+                                   cudaMemcpyDeviceToDevice, stream_),
+                   "exchange copy");
+    }
+  }
+  stats.exchanged_bytes += static_cast<uint64_t>(npeer) * region * sizeof(double2);
+}
+
+double State::norm_squared() {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  double* out = d_scratch_ + kNormBlocks;
+  cuda_check(launch_norm(psi_, buffer_amps(), d_scratch_, out, stream_), "norm");
+  std::vector<double> parts(world_, 0.0);
+  if (mode_ == Mode::Nccl) {
+    std::string err;
+    double* gathered = d_scratch_ + kNormBlocks + 1;
+    if (!comm_->allgather_double(out, gathered, stream_, &err)) fail(QT_ERR_NCCL, err);
+    cuda_check(cudaMemcpyAsync(parts.data(), gathered, sizeof(double) * world_,
+                               cudaMemcpyDeviceToHost, stream_),
+               "norm readback");
+  } else {
+    cuda_check(cudaMemcpyAsync(parts.data(), out, sizeof(double),
+                               cudaMemcpyDeviceToHost, stream_),
+               "norm readback");
+  }
+  sync();
+  double acc = 0.0;
+  for (int r = 0; r < (mode_ == Mode::Nccl ? world_ : 1); ++r) acc += parts[r];
+  return acc;
+}
+
+void State::sync() {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaMemcpyAsync(h_flag_, d_flag_, sizeof(int), cudaMemcpyDeviceToHost, stream_),
+             "flag readback");
+  cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+  if (comm_) {
+    std::string err;
+    if (!comm_->check_async(&err)) fail(QT_ERR_NCCL, err);
+  }
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, ev0_, ev1_) == cudaSuccess) stats.device_ms = ms;
+  cudaGetLastError();  // an unrecorded event pair is not an error here
+  if (*h_flag_) {
+    *h_flag_ = 0;
+    cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "flag reset");
+    cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+    fail(QT_ERR_NUMERIC, "non-finite amplitude");
+  }
+}
+
+std::vector<std::pair<int, float>> State::last_timings(bool consume) {
+  sync();
+  std::vector<std::pair<int, float>> out;
+  for (size_t i = 0; i < timings_used_; ++i) {
+    float ms = -1.f;
+    if (cudaEventElapsedTime(&ms, timings_[i].start, timings_[i].stop) != cudaSuccess) {
+      cudaGetLastError();
+      ms = -1.f;
+    }
+    out.emplace_back(timings_[i].kind, ms);
+  }
+  if (consume) timings_used_ = 0;
+  return out;
+}
+
+void State::checkpoint_save(int slot) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  auto it = ckpt_.find(slot);
+  if (it == ckpt_.end()) {
+    double2* buf = nullptr;
+    cuda_check(cudaMalloc(&buf, sizeof(double2) * buffer_amps()), "checkpoint allocation");
+    it = ckpt_.emplace(slot, std::make_pair(buf, perm_)).first;
+  }
+  cuda_check(cudaMemcpyAsync(it->second.first, psi_, sizeof(double2) * buffer_amps(),
+                             cudaMemcpyDeviceToDevice, stream_),
+             "checkpoint save");
+  it->second.second = perm_;
+}
+
+void State::checkpoint_restore(int slot) {
+  auto it = ckpt_.find(slot);
+  if (it == ckpt_.end()) fail(QT_ERR_ARG, "unknown checkpoint slot");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaMemcpyAsync(psi_, it->second.first, sizeof(double2) * buffer_amps(),
+                             cudaMemcpyDeviceToDevice, stream_),
+             "checkpoint restore");
+  perm_ = it->second.second;
+}
+
+void State::checkpoint_drop_all() {
+  cudaStreamSynchronize(stream_);
+  for (auto& kv : ckpt_) cudaFree(kv.second.first);
+  ckpt_.clear();
+}
+
+void State::checkpoint_drop(int slot) {
+  auto it = ckpt_.find(slot);
+  if (it == ckpt_.end()) return;
+  cudaStreamSynchronize(stream_);
+  cudaFree(it->second.first);
+  ckpt_.erase(it);
+}
+
+void State::copy_from(const State& other) {
+  if (other.buf_bits_ != buf_bits_) fail(QT_ERR_ARG, "geometry mismatch");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cuda_check(cudaMemcpyAsync(psi_, other.psi_, sizeof(double2) * buffer_amps(),
+                             cudaMemcpyDeviceToDevice, stream_),
+             "state copy");
+  perm_ = other.perm_;
+}
+
+}  // namespace qtb

@@ -1,0 +1,120 @@
+// qt_state.hpp -- device-resident state vector + stateless gate application.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "qt_comm.hpp"
+#include "qt_ir.hpp"
+#include "qt_plan.hpp"
+#include "qtask_c.h"
+
+namespace qtb {
+
+// Thrown inside the library; the C API converts it to a status code.
+struct QtError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+
+enum class Mode { Single, Loopback, Nccl };
+
+// Per-pass timing record (when timing is enabled).
+struct PassTiming {
+  cudaEvent_t start = nullptr, stop = nullptr;
+  int kind = 0;  // 0 tile, 1 exchange
+};
+
+class State {
+ public:
+  State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
+        const qt_config* cfg);
+  ~State();
+
+  int nqubits() const { return n_; }
+  int nlocal() const { return nlocal_; }
+  Mode mode() const { return mode_; }
+  cudaStream_t stream() const { return stream_; }
+  double2* data() { return psi_; }
+  uint64_t buffer_amps() const { return 1ull << buf_bits_; }
+  const std::vector<int>& perm() const { return perm_; }
+
+  void set_basis(uint64_t index);
+  void write(uint64_t first, uint64_t count, const double* src);
+  void read(uint64_t first, uint64_t count, double* dst);
+  // Applies pre-lowered logical ops (already fused). If src is given (a
+  // buffer of the same geometry, perm src_perm), the state is computed from
+  // src out of place: the first pass reads src and writes the bound buffer.
+  void apply_ops(const std::vector<LOp>& ops, uint64_t ngates,
+                 const double2* src = nullptr,
+                 const std::vector<int>* src_perm = nullptr);
+
+  // Extra full-state buffers (the incremental engine's checkpoint chain).
+  // Buffer 0 is the one allocated at construction. Returns how many exist.
+  int grow_pool(int count, double max_fraction_of_free);
+  int pool_size() const { return static_cast<int>(pool_.size()); }
+  double2* buffer(int i) const { return pool_[i]; }
+  int bound() const { return bound_; }
+  void bind(int i, const std::vector<int>& perm);
+  void apply(const qt_gate* gates, size_t count);
+  double norm_squared();
+  void sync();  // also raises QT_ERR_NUMERIC if a pass saw a non-finite value
+
+  void checkpoint_save(int slot);
+  void checkpoint_restore(int slot);
+  void checkpoint_drop(int slot);
+  void checkpoint_drop_all();
+  bool has_checkpoint(int slot) const { return ckpt_.count(slot) != 0; }
+  // D2D copy of the whole local buffer + perm between two states of the same
+  // geometry (used by the incremental engine's checkpoint chain).
+  void copy_from(const State& other);
+
+  Plan plan(const std::vector<LOp>& ops) const;
+  const PlanOptions& options() const { return opt_; }
+  void set_timing(bool on) { timing_ = on; }
+  // Device ms of every launch of the last apply (timing enabled).
+  std::vector<std::pair<int, float>> last_timings(bool consume = true);
+
+  qt_run_stats stats{};
+
+ private:
+  void upload_and_launch(const Plan& plan, const double2* src);
+  void exchange(const PlanPass& pass);
+  void ensure_device_bytes(size_t bytes);
+
+  int n_ = 0, nlocal_ = 0, buf_bits_ = 0;
+  Mode mode_ = Mode::Single;
+  int rank_ = 0, world_ = 1, device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  double2* psi_ = nullptr;
+  double* d_scratch_ = nullptr;   // norm partials + result + gather
+  int* d_flag_ = nullptr;
+  int* h_flag_ = nullptr;         // pinned
+  void* d_plan_ = nullptr;        // rounds + ops
+  size_t d_plan_cap_ = 0;
+  void* h_stage_ = nullptr;       // pinned staging for the plan upload
+  size_t h_stage_cap_ = 0;
+  cudaEvent_t stage_free_ = nullptr;
+  double2* d_tmp_ = nullptr;      // exchange receive buffer
+  size_t d_tmp_amps_ = 0;
+  std::vector<int> perm_;         // logical -> physical
+  std::vector<double2*> pool_;
+  int bound_ = 0;
+  std::map<int, std::pair<double2*, std::vector<int>>> ckpt_;
+  std::unique_ptr<Comm> comm_;
+  PlanOptions opt_;
+  int occupancy_ = 1, sms_ = 148;
+  bool timing_ = false;
+  std::vector<PassTiming> timings_;
+  size_t timings_used_ = 0;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+};
+
+}  // namespace qtb

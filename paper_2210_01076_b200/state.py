@@ -1,0 +1,133 @@
+"""Device-resident state vector (qt_state_* of include/qtask_c.h)."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _ffi
+from ._ffi import check, lib
+
+
+class StateVector:
+    """2^n complex128 amplitudes in HBM, gates applied by fused sm_100a tile
+    passes.
+
+    mode: "single" (one GPU), "loopback" (``shards`` emulated ranks on one
+    GPU, exchanges by device copies) or "sharded" (one rank of a
+    ``world``-GPU state, NCCL exchanges; pass ``rank``, ``world``, ``nccl_id``).
+    """
+
+    def __init__(self, num_qubits: int, mode: str = "single", shards: int = 1,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 device: int = -1, tile_qubits: int = 0):
+        self._h = ctypes.c_void_p()
+        cfg = _ffi.make_config(device=device, tile_qubits=tile_qubits)
+        if mode == "single":
+            check(lib().qt_state_create(num_qubits, ctypes.byref(cfg), ctypes.byref(self._h)))
+        elif mode == "loopback":
+            check(lib().qt_state_create_loopback(num_qubits, shards, ctypes.byref(cfg),
+                                                 ctypes.byref(self._h)))
+        elif mode == "sharded":
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValueError("sharded mode needs the 128-byte NCCL unique id")
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            check(lib().qt_state_create_sharded(num_qubits, rank, world, idbuf,
+                                                ctypes.byref(cfg), ctypes.byref(self._h)))
+        else:
+            raise ValueError(mode)
+        self.n = num_qubits
+        self.mode = mode
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().qt_state_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream_ptr(self) -> int:
+        return lib().qt_state_stream(self._h) or 0
+
+    def set_basis(self, index: int = 0):
+        check(lib().qt_set_basis(self._h, index))
+
+    def apply(self, gates: np.ndarray):
+        g = _ffi.gates_array(gates)
+        check(lib().qt_apply(self._h, g.ctypes.data, len(g)))
+
+    def write(self, amps: np.ndarray, first: int = 0):
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        check(lib().qt_write(self._h, first, len(a), a.ctypes.data))
+
+    def read(self, first: int = 0, count: int | None = None, out: np.ndarray | None = None):
+        if count is None:
+            count = (1 << self.n) - first
+        if out is None:
+            out = np.empty(count, dtype=np.complex128)
+        check(lib().qt_read(self._h, first, count, out.ctypes.data))
+        return out
+
+    def norm_squared(self) -> float:
+        v = ctypes.c_double(0.0)
+        check(lib().qt_norm_squared(self._h, ctypes.byref(v)))
+        return v.value
+
+    def sync(self):
+        check(lib().qt_sync(self._h))
+
+    def stats(self) -> dict:
+        s = _ffi.QtRunStats()
+        check(lib().qt_last_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def set_timing(self, on: bool = True):
+        check(lib().qt_set_timing(self._h, 1 if on else 0))
+
+    def last_timings(self):
+        """[(kind, ms)] per launch of the last apply (0 = tile pass,
+        1 = exchange); needs set_timing(True) before the apply."""
+        cnt = ctypes.c_size_t(0)
+        check(lib().qt_last_timings(self._h, None, None, 0, ctypes.byref(cnt)))
+        kinds = np.zeros(cnt.value, dtype=np.int32)
+        ms = np.zeros(cnt.value, dtype=np.float32)
+        check(lib().qt_last_timings(self._h, kinds.ctypes.data, ms.ctypes.data, cnt.value,
+                                    ctypes.byref(cnt)))
+        return list(zip(kinds.tolist(), ms.tolist()))
+
+    def checkpoint_save(self, slot: int):
+        check(lib().qt_checkpoint_save(self._h, slot))
+
+    def checkpoint_restore(self, slot: int):
+        check(lib().qt_checkpoint_restore(self._h, slot))
+
+    def plan_json(self, gates: np.ndarray) -> str:
+        g = _ffi.gates_array(gates)
+        need = ctypes.c_size_t(0)
+        check(lib().qt_plan_json(self._h, g.ctypes.data, len(g), None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        check(lib().qt_plan_json(self._h, g.ctypes.data, len(g), buf, need.value,
+                                 ctypes.byref(need)))
+        return buf.value.decode()
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().qt_nccl_unique_id(buf))
+    return buf.raw
+
+
+def probe_fp64(device: int = 0) -> float:
+    """Measured FP64 FMA instructions per second of the device."""
+    v = ctypes.c_double(0.0)
+    check(lib().qt_probe_fp64(device, ctypes.byref(v)))
+    return v.value

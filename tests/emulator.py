@@ -1,0 +1,96 @@
+"""Test-only numpy replay of a detailed pass plan (qt_plan_probe_ex JSON).
+
+Independent of the CUDA kernels: it re-derives each encoded device op's
+physical action from the tile / register-slot encoding and applies it to a
+full state vector, so planner legality (hoisting, rounds) and op encoding
+are checked against the dense oracle on the CPU. Exchanges are bit swaps.
+"""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1 = range(8)
+
+
+def _bit(idx, pos):
+    return (idx >> np.uint64(pos)) & np.uint64(1)
+
+
+def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
+    plan = json.loads(plan_json) if isinstance(plan_json, str) else plan_json
+    psi = state.copy()
+    n = int(len(psi)).bit_length() - 1
+    idx = np.arange(1 << n, dtype=np.uint64)
+    for ps in plan["passes"]:
+        if ps["kind"] == "exchange":
+            for g, v in ps["swap"]:
+                sel = (_bit(idx, g) == 1) & (_bit(idx, v) == 0)
+                a = idx[sel]
+                b = a ^ np.uint64((1 << g) | (1 << v))
+                psi[a], psi[b] = psi[b].copy(), psi[a].copy()
+            continue
+        tile = ps["tile"]
+        for rd in ps["round_detail"]:
+            reg = rd["reg"]
+            for op in rd["ops"]:
+                typ, a, b, lmask, gmask, dl, dg = (int(x) for x in op[:7])
+                m = np.array(op[7:15], dtype=np.float64)
+                m = m[0::2] + 1j * m[1::2]
+                # control predicate over physical bits
+                ok = np.ones(len(psi), dtype=bool)
+                for tb in range(len(tile)):
+                    if (lmask >> tb) & 1:
+                        ok &= _bit(idx, tile[tb]) == 1
+                for p in range(64):
+                    if (gmask >> p) & 1:
+                        ok &= _bit(idx, p) == 1
+                if typ in (D_DENSE, D_REAL, D_XPERM, D_ANTI):
+                    t = tile[reg[a]]
+                    lo = idx[(_bit(idx, t) == 0) & ok]
+                    hi = lo | np.uint64(1 << t)
+                    x, y = psi[lo].copy(), psi[hi].copy()
+                    if typ in (D_DENSE, D_REAL):
+                        if typ == D_REAL:
+                            m = m.real.astype(np.complex128)
+                        psi[lo] = m[0] * x + m[1] * y
+                        psi[hi] = m[2] * x + m[3] * y
+                    elif typ == D_XPERM:
+                        psi[lo], psi[hi] = y, x
+                    else:
+                        psi[lo] = m[1] * y
+                        psi[hi] = m[2] * x
+                elif typ in (D_DIAG, D_SIGN, D_PHASE1):
+                    if dl:
+                        tb = int(dl).bit_length() - 1
+                        bit = _bit(idx, tile[tb]) == 1
+                    else:
+                        bit = _bit(idx, int(dg).bit_length() - 1) == 1
+                    if typ == D_SIGN:
+                        f = np.where(bit, -1.0, 1.0)
+                    elif typ == D_PHASE1:
+                        f = np.where(bit, m[3], 1.0)
+                    else:
+                        f = np.where(bit, m[3], m[0])
+                    psi = np.where(ok, psi * f, psi)
+                elif typ == D_SWAP2:
+                    ta, tb2 = tile[reg[a]], tile[reg[b]]
+                    sel = (_bit(idx, ta) == 1) & (_bit(idx, tb2) == 0)
+                    p0 = idx[sel]
+                    p1 = p0 ^ np.uint64((1 << ta) | (1 << tb2))
+                    psi[p0], psi[p1] = psi[p1].copy(), psi[p0].copy()
+                else:
+                    raise ValueError(f"unknown op type {typ}")
+    return psi
+
+
+def logical_view(psi: np.ndarray, perm_after) -> np.ndarray:
+    """Maps a physical state (logical qubit q at physical bit perm[q]) back to
+    logical index order."""
+    n = int(len(psi)).bit_length() - 1
+    idx = np.arange(1 << n, dtype=np.uint64)
+    phys = np.zeros_like(idx)
+    for q in range(n):
+        phys |= _bit(idx, q) << np.uint64(perm_after[q])
+    return psi[phys]

@@ -1,0 +1,295 @@
+"""GPU tests of the incremental drop-in (qt_sim_*), mirroring the reference's
+engine tests (proj/tests/test_engine.cpp) and acceptance criteria
+(proj/tests/acceptance.cpp: 1 full oracle, 2 incremental oracle, 6 norm,
+7 determinism, 8 locality)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2210_01076_b200 import Config, Simulator, workloads as W
+from paper_2210_01076_b200.errors import (BadQubitError, InvalidPositionError,
+                                          NetConflictError, StaleStateError,
+                                          UnknownGateError, UnknownNetError)
+from paper_2210_01076_b200.gates import GateKind as K
+
+pytestmark = pytest.mark.gpu
+TWO = {K.Cnot, K.Swap, K.Cz}
+
+
+def ref_state(sim):
+    c = sim.circuit()
+    return oracle.simulate(c.num_qubits(), c.gates())
+
+
+def max_dev(sim):
+    want = ref_state(sim)
+    got = sim.amplitudes(0, len(want) - 1)
+    return float(np.abs(got - want).max())
+
+
+class Entangle5:
+    """Listing-1 circuit (acceptance.cpp:43-63)."""
+
+    def __init__(self, cfg=None):
+        self.sim = Simulator(5, cfg or Config(4, 1))
+        s = self.sim
+        self.n = [s.insert_net_back() for _ in range(5)]
+        for q in range(4, -1, -1):
+            s.insert_gate(K.H, self.n[0], q)
+        self.g6 = s.insert_gate(K.Cnot, self.n[1], 3, 4)
+        self.g7 = s.insert_gate(K.Cnot, self.n[2], 1, 4)
+        self.g8 = s.insert_gate(K.Cnot, self.n[3], 2, 3)
+        self.g9 = s.insert_gate(K.Cnot, self.n[4], 0, 2)
+
+
+def random_gate_desc(rng, n):
+    """test_support.hpp:137-167 distribution (all 13 reference kinds;
+    rotations at pi, pi/2, 0 or U(-2pi, 2pi))."""
+    kinds = list(K)[:13]
+    kind = kinds[int(rng.integers(13 if n >= 2 else 12))]
+    if n < 2 and kind in TWO:
+        kind = K.H
+    t = int(rng.integers(n))
+    c = -1
+    if kind in TWO:
+        c = t
+        while c == t:
+            c = int(rng.integers(n))
+    th = 0.0
+    if kind in (K.Rx, K.Ry, K.Rz):
+        th = [math.pi, math.pi / 2, 0.0, float(rng.uniform(-2 * math.pi, 2 * math.pi))][
+            int(rng.integers(4))]
+    return kind, t, c, th
+
+
+def insert(sim, net, desc):
+    kind, t, c, th = desc
+    if kind in TWO:
+        return sim.insert_gate(kind, net, t, c)
+    if kind in (K.Rx, K.Ry, K.Rz):
+        return sim.insert_gate(kind, th, net, t)
+    return sim.insert_gate(kind, net, t)
+
+
+def test_fresh_simulator_reads_initial_state(gpu):
+    sim = Simulator(3)
+    assert sim.amplitude(0) == 1 and sim.amplitude(5) == 0
+    assert abs(sim.norm_squared() - 1) < 1e-12
+
+
+def test_modifier_errors(gpu):
+    sim = Simulator(3)
+    with pytest.raises(InvalidPositionError):
+        sim.insert_net_after(99)
+    with pytest.raises(UnknownNetError):
+        sim.remove_net(7)
+    with pytest.raises(UnknownGateError):
+        sim.remove_gate(7)
+    net = sim.insert_net_back()
+    with pytest.raises(UnknownNetError):
+        sim.insert_gate(K.H, 42, 0)
+    with pytest.raises(BadQubitError):
+        sim.insert_gate(K.H, net, 3)
+    with pytest.raises(BadQubitError):
+        sim.insert_gate(K.Cnot, net, 1, 1)
+    sim.insert_gate(K.Cnot, net, 1, 2)
+    with pytest.raises(NetConflictError):
+        sim.insert_gate(K.X, net, 2)
+    with pytest.raises(NetConflictError):
+        sim.insert_gate(K.Cnot, net, 0, 1)
+    stale = sim.insert_net_back()
+    sim.remove_net(stale)
+    with pytest.raises(InvalidPositionError):
+        sim.insert_net_after(stale)
+
+
+def test_queries_require_clean_state(gpu):
+    sim = Simulator(2)
+    net = sim.insert_net_back()
+    with pytest.raises(StaleStateError):
+        sim.amplitude(0)
+    sim.update_state()
+    assert sim.amplitude(0) == 1
+    sim.insert_gate(K.X, net, 0)
+    with pytest.raises(StaleStateError):
+        sim.amplitudes(0, 3)
+    sim.update_state()
+    assert sim.amplitude(1) == 1
+
+
+def test_entangle5_full_and_incremental(gpu):
+    lc = Entangle5()
+    lc.sim.update_state()
+    want = 1 / math.sqrt(32)
+    amps = lc.sim.amplitudes(0, 31)
+    assert np.abs(amps - want).max() < 1e-12
+    assert lc.sim.last_update().full
+    lc.sim.remove_gate(lc.g8)
+    lc.sim.insert_gate(K.Cnot, lc.n[3], 1, 2)  # g10
+    lc.sim.update_state()
+    assert not lc.sim.last_update().full
+    assert max_dev(lc.sim) <= 1e-10
+    assert abs(lc.sim.norm_squared() - 1) < 1e-9
+
+
+def test_noop_and_idempotent_updates(gpu):
+    lc = Entangle5()
+    lc.sim.update_state()
+    a = lc.sim.amplitudes(0, 31)
+    lc.sim.update_state()
+    assert lc.sim.last_update().executed_partitions == 0
+    b = lc.sim.amplitudes(0, 31)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_identity_gates_and_removal(gpu):
+    sim = Simulator(3, Config(4, 1))
+    net = sim.insert_net_back()
+    g = sim.insert_gate(K.Rz, 0.0, net, 0)
+    sim.update_state()
+    assert sim.amplitude(0) == 1
+    sim.remove_gate(g)
+    sim.update_state()
+    assert sim.amplitude(0) == 1
+
+
+def test_remove_whole_net(gpu):
+    lc = Entangle5()
+    lc.sim.update_state()
+    lc.sim.remove_net(lc.n[4])
+    lc.sim.update_state()
+    assert max_dev(lc.sim) <= 1e-10
+    assert len(lc.sim.circuit().net_order()) == 4
+
+
+def test_superposition_add_remove(gpu):
+    sim = Simulator(3, Config(4, 1))
+    net = sim.insert_net_back()
+    h0 = sim.insert_gate(K.H, net, 0)
+    sim.update_state()
+    h1 = sim.insert_gate(K.H, net, 1)
+    sim.update_state()
+    assert max_dev(sim) <= 1e-10
+    sim.remove_gate(h0)
+    sim.update_state()
+    assert max_dev(sim) <= 1e-10
+    sim.remove_gate(h1)
+    sim.update_state()
+    assert sim.amplitude(0) == 1
+
+
+def build(sim, rng, max_qubits, max_gates):
+    """random_circuit (test_support.hpp:171-195)."""
+    n = sim.num_qubits()
+    count = 1 + int(rng.integers(max_gates))
+    nets = [sim.insert_net_back()]
+    used = set()
+    for _ in range(count):
+        d = random_gate_desc(rng, n)
+        qs = {d[1]} | ({d[2]} if d[2] >= 0 else set())
+        if qs & used or rng.integers(3) == 0:
+            nets.append(sim.insert_net_back())
+            used = set()
+        insert(sim, nets[-1], d)
+        used |= qs
+
+
+def test_acceptance_oracle_full(gpu):
+    rng = np.random.default_rng(20240501)
+    worst = 0.0
+    for _ in range(100):
+        n = 1 + int(rng.integers(10))
+        block = 1 << (1 + int(rng.integers(10)))
+        sim = Simulator(n, Config(block, 1 + int(rng.integers(4)), max_checkpoints=4))
+        build(sim, rng, 10, 60)
+        sim.update_state()
+        assert abs(sim.norm_squared() - 1) <= 1e-9
+        worst = max(worst, max_dev(sim))
+        sim.close()
+    assert worst <= 1e-10
+
+
+def test_acceptance_oracle_incremental(gpu):
+    rng = np.random.default_rng(87123)
+    worst = 0.0
+    for _ in range(100):
+        n = 1 + int(rng.integers(10))
+        sim = Simulator(n, Config(1 << (1 + int(rng.integers(9))), 1, max_checkpoints=3,
+                                  segment_gates=int(rng.integers(1, 8))))
+        nets, gates = [], []
+        for _ in range(10 + int(rng.integers(50))):
+            roll = int(rng.integers(12))
+            if roll < 3 or not nets:
+                if not nets or rng.integers(2) == 0:
+                    nets.append(sim.insert_net_back())
+                else:
+                    nets.append(sim.insert_net_after(nets[int(rng.integers(len(nets)))]))
+            elif roll < 9:
+                try:
+                    gates.append(insert(sim, nets[int(rng.integers(len(nets)))],
+                                        random_gate_desc(rng, n)))
+                except NetConflictError:
+                    pass
+            elif roll < 10 and gates:
+                sim.remove_gate(gates.pop(int(rng.integers(len(gates)))))
+            elif roll < 11 and len(nets) > 1 and rng.integers(4) == 0:
+                at = int(rng.integers(len(nets)))
+                for g in sim.circuit().net(nets[at]):
+                    gates.remove(g)
+                sim.remove_net(nets.pop(at))
+            else:
+                sim.update_state()
+                assert abs(sim.norm_squared() - 1) <= 1e-9
+                worst = max(worst, max_dev(sim))
+        sim.update_state()
+        worst = max(worst, max_dev(sim))
+        sim.close()
+    assert worst <= 1e-10
+
+
+def test_acceptance_locality(gpu):
+    """Criterion 8: editing the last net re-executes <= 10% of the work an
+    edit of the first net does."""
+    n = 15
+    sim = Simulator(n, Config(256, 2, segment_gates=8))
+    nets, gates, qs = [], [], []
+    for i in range(100):
+        c = i % (n - 1)
+        net = sim.insert_net_back()
+        nets.append(net)
+        gates.append(sim.insert_gate(K.Cnot, net, c + 1, c))
+        qs.append((c, c + 1))
+    sim.update_state()
+
+    def touch(at):
+        sim.remove_gate(gates[at])
+        gates[at] = sim.insert_gate(K.Cnot, nets[at], qs[at][1], qs[at][0])
+        sim.update_state()
+        return sim.last_update().gates
+
+    last = touch(99)
+    first = touch(0)
+    assert first > 0 and last * 10 <= first
+    assert max_dev(sim) <= 1e-10
+
+
+def test_config5_shape_incremental(gpu):
+    """C5 workload shape at n=14: 400 gates, 60 alternating modifiers
+    (uniform / last-10% positions), oracle after every update."""
+    w = W.config5(n=14, ngates=400, nmods=60)
+    sim = Simulator(14, Config(256, 0, max_checkpoints=8))
+    drv = W.NetDriver(sim)
+    drv.build(w.gates)
+    sim.update_state()
+    gates = w.gates
+    for m, mod in enumerate(w.modifiers):
+        drv.modify(mod)
+        gates = W.apply_modifier(gates, mod)
+        sim.update_state()
+        if m % 6 == 0:
+            want = oracle.simulate(14, gates)
+            got = sim.amplitudes(0, (1 << 14) - 1)
+            assert np.abs(got - want).max() <= 1e-10
+            assert abs(sim.norm_squared() - 1) <= 1e-12
