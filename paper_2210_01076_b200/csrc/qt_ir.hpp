@@ -62,44 +62,40 @@ enum DType : uint32_t {
   D_PHASE1 = 7,  // multiply by d1 where bit set (S, T, phase) (4 DFMA/amp)
 };
 
-// 128 bytes, 16-byte aligned: read uniformly by every thread of a CTA.
+// Variant id of a device op: the kernel dispatches on it to a fully
+// specialised code path (register slots known at compile time, no per-slot
+// predication). cs / ds are -1 when the control / diagonal target is not a
+// register bit of the round; SWAP2 stores its second slot in ds.
+constexpr uint32_t vid(uint32_t type, int a, int cs, int ds) {
+  return (type << 9) | (uint32_t(a) << 6) | (uint32_t(cs + 1) << 3) | uint32_t(ds + 1);
+}
+
+// 96 bytes; lives in the kernel-parameter constant bank (read uniformly).
 struct alignas(16) DOp {
-  uint32_t type;
-  uint32_t a;      // reg slot of the (first) target, 0..R-1
-  uint32_t b;      // reg slot of the second target (SWAP2)
-  uint32_t lmask;  // control: ((j & lmask) == lmask) over the tile-local index
-  uint64_t gmask;  // control: ((g & gmask) == gmask) over the tile's global base
-  uint32_t dl;     // diag target as tile-local bit mask (0 if not in tile)
-  uint32_t pad0;
-  uint64_t dg;     // diag target as global-base bit mask (0 if in tile)
-  uint64_t pad1;
-  double m[8];     // interleaved row-major 2x2 (diag: m[0..1]=d0, m[6..7]=d1)
+  uint32_t variant;  // vid(type, a, cs, ds)
+  uint32_t lmask;    // control bits among the round's NON-register tile bits
+  uint32_t dl;       // diag target among non-register tile bits (mask) or 0
+  uint32_t pad;
+  uint64_t gmask;    // control bits outside the tile (global index bits)
+  uint64_t dg;       // diag target outside the tile (mask) or 0
+  double m[8];       // interleaved row-major 2x2 (diag: m[0..1]=d0, m[6..7]=d1)
 };
-static_assert(sizeof(DOp) == 112 || sizeof(DOp) == 128, "DOp layout");
+static_assert(sizeof(DOp) == 96, "DOp layout");
 
 constexpr int kMaxTileBits = 13;  // 2^13 x 16 B = 128 KiB of smem
-constexpr int kMaxRegBits = 3;
-constexpr int kMaxRounds = 96;
+constexpr int kMaxRegBits = 4;
 
 struct DRound {
-  uint8_t nreg;
+  uint16_t op_first;  // into the pass's op array
+  uint16_t op_count;
   uint8_t reg[kMaxRegBits];  // tile-bit indices of the register bits
-  uint32_t op_first;         // into the plan's op array
-  uint32_t op_count;
 };
+static_assert(sizeof(DRound) == 8, "DRound layout");
 
-// Kernel parameters of one pass (passed by value; < 4 KB).
-struct PassParams {
-  uint32_t k;                 // tile bits
-  uint32_t nouter;            // non-tile local bits
-  uint32_t nrounds;
-  uint32_t flags;
-  uint64_t ntiles;            // 2^(nlocal - k)
-  uint64_t gbase_hi;          // rank bits (global index offset of the shard)
-  uint8_t tile_pos[kMaxTileBits];  // physical bit of tile bit i (i < k)
-  uint8_t outer_pos[48];           // physical bit of outer bit i
-  DRound rounds[kMaxRounds];
-};
+// Per-launch capacity of the kernel-parameter block (<= 32764 bytes): a
+// pass with more ops / rounds is split by the planner.
+constexpr int kSmallOps = 32, kSmallRounds = 16;
+constexpr int kLargeOps = 288, kLargeRounds = 96;
 
 // ---------------------------------------------------------------------------
 // Host plan

@@ -9,27 +9,40 @@
 
 namespace qtb {
 
-struct KPass {
-  uint32_t k;        // tile bits
-  uint32_t nouter;   // local bits outside the tile
+// Header of one tile-pass launch.
+struct KPassHead {
+  uint32_t k;          // tile bits
   uint32_t nrounds;
-  uint32_t reg_bits; // R
+  uint32_t nops;
+  uint32_t reg_bits;   // R
   uint64_t ntiles;
-  uint64_t gbase_hi; // shard offset in the global index (rank << nlocal)
-  const double2* src; // tiles are read from src and written to psi (may alias)
-  const DRound* rounds;
-  const DOp* ops;
-  int* flag;         // set to 1 if any written amplitude is non-finite
+  uint64_t gbase_hi;   // shard offset in the global index (rank << nlocal)
   uint64_t lo_mask;    // physical bits of tile bits [0, k-R)  (thread bits)
   uint64_t hi_mask;    // physical bits of tile bits [k-R, k)  (load slots)
-  uint64_t outer_mask; // local physical bits outside the tile
+  uint64_t outer_mask; // buffer bits outside the tile
+  const double2* src;  // tiles are read from src and written to psi (may alias)
+  int* flag;           // set to 1 if any written amplitude is non-finite
 };
 
+// Kernel parameters (passed by value as a __grid_constant__: the rounds and
+// ops are read from the constant bank, uniformly across the CTA).
+template <int OPS, int ROUNDS>
+struct KPass {
+  KPassHead h;
+  DRound rounds[ROUNDS];
+  DOp ops[OPS];
+};
+using KPassSmall = KPass<kSmallOps, kSmallRounds>;
+using KPassLarge = KPass<kLargeOps, kLargeRounds>;
+static_assert(sizeof(KPassLarge) <= 32764, "kernel parameter limit");
+
 // Fused tile pass over a state of 2^nlocal amplitudes.
-cudaError_t launch_tile_pass(double2* psi, const KPass& p, int grid,
+cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid,
+                             cudaStream_t s);
+cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid,
                              cudaStream_t s);
 // Max resident CTAs per SM of the tile-pass kernel for (k, R).
-int tile_pass_occupancy(int k, int R);
+int tile_pass_occupancy(int k, int R, bool large);
 
 // Sets every amplitude to 0 and amplitude `index` to 1.
 cudaError_t launch_set_basis(double2* psi, uint64_t n, uint64_t index,

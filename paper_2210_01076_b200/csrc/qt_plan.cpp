@@ -150,7 +150,7 @@ void fuse_ops(std::vector<LOp>& ops, int nqubits) {
 DOp encode_op(const LOp& op, const std::vector<int>& tile_phys,
               const std::vector<int>& reg) {
   DOp d{};
-  d.type = dtype_of(op);
+  const uint32_t type = dtype_of(op);
   auto tile_index = [&](int phys) -> int {
     for (size_t i = 0; i < tile_phys.size(); ++i)
       if (tile_phys[i] == phys) return static_cast<int>(i);
@@ -158,23 +158,38 @@ DOp encode_op(const LOp& op, const std::vector<int>& tile_phys,
   };
   auto reg_slot = [&](int phys) -> int {
     const int ti = tile_index(phys);
+    if (ti < 0) return -1;
     for (size_t i = 0; i < reg.size(); ++i)
       if (reg[i] == ti) return static_cast<int>(i);
     return -1;
   };
+  int a = 0, cs = -1, ds = -1;
   if (op.kind == LKind::Diag) {
-    const int ti = tile_index(op.target);
-    if (ti >= 0) d.dl = 1u << ti;
-    else d.dg = 1ull << op.target;
+    ds = reg_slot(op.target);
+    if (ds < 0) {
+      const int ti = tile_index(op.target);
+      if (ti >= 0) d.dl = 1u << ti;  // thread-uniform bit
+      else d.dg = 1ull << op.target; // tile-uniform bit
+    }
   } else {
-    d.a = static_cast<uint32_t>(reg_slot(op.target));
-    if (op.kind == LKind::Swap) d.b = static_cast<uint32_t>(reg_slot(op.target2));
+    a = reg_slot(op.target);
+    if (a < 0) throw std::logic_error("op target is not a register bit of its round");
+    if (op.kind == LKind::Swap) {
+      int b = reg_slot(op.target2);
+      if (b < 0) throw std::logic_error("swap target is not a register bit");
+      if (a > b) std::swap(a, b);
+      ds = b;  // SWAP2 carries its second slot in ds
+    }
   }
   if (op.control >= 0) {
-    const int ti = tile_index(op.control);
-    if (ti >= 0) d.lmask = 1u << ti;
-    else d.gmask = 1ull << op.control;
+    cs = reg_slot(op.control);
+    if (cs < 0) {
+      const int ti = tile_index(op.control);
+      if (ti >= 0) d.lmask = 1u << ti;
+      else d.gmask = 1ull << op.control;
+    }
   }
+  d.variant = vid(type, a, cs, ds);
   for (int k = 0; k < 4; ++k) {
     d.m[2 * k] = op.m[k].re;
     d.m[2 * k + 1] = op.m[k].im;
@@ -246,6 +261,50 @@ void make_rounds(PlanPass& pass, int R, int nphys) {
     }
     pass.rounds.push_back(std::move(round));
     remaining.swap(rest);
+  }
+}
+
+// A launch carries at most kLargeOps ops in kLargeRounds rounds (kernel
+// parameter space); deeper passes become consecutive launches on the same
+// tile (only FP64-bound passes are that deep, so the extra HBM sweep hides).
+void split_pass(PlanPass& pass, std::vector<PlanPass>& out) {
+  size_t r = 0;
+  while (r < pass.rounds.size()) {
+    PlanPass part;
+    part.kind = PlanPass::Tile;
+    part.tile_phys = pass.tile_phys;
+    while (r < pass.rounds.size() &&
+           static_cast<int>(part.rounds.size()) < kLargeRounds &&
+           part.ops.size() + pass.rounds[r].ops.size() <= static_cast<size_t>(kLargeOps)) {
+      PlanRound pr;
+      pr.reg = pass.rounds[r].reg;
+      for (int idx : pass.rounds[r].ops) {
+        pr.ops.push_back(static_cast<int>(part.ops.size()));
+        part.ops.push_back(pass.ops[idx]);
+      }
+      part.rounds.push_back(std::move(pr));
+      ++r;
+    }
+    if (part.rounds.empty()) {
+      // a single round with more than kLargeOps ops: split the round itself
+      const PlanRound& big = pass.rounds[r];
+      for (size_t o = 0; o < big.ops.size(); o += kLargeOps) {
+        PlanPass piece;
+        piece.kind = PlanPass::Tile;
+        piece.tile_phys = pass.tile_phys;
+        PlanRound pr;
+        pr.reg = big.reg;
+        for (size_t u = o; u < big.ops.size() && u < o + kLargeOps; ++u) {
+          pr.ops.push_back(static_cast<int>(piece.ops.size()));
+          piece.ops.push_back(pass.ops[big.ops[u]]);
+        }
+        piece.rounds.push_back(std::move(pr));
+        out.push_back(std::move(piece));
+      }
+      ++r;
+      continue;
+    }
+    out.push_back(std::move(part));
   }
 }
 
@@ -392,7 +451,7 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
       if (inQ[p]) pass.tile_phys.push_back(p);
     if (pass.ops.empty()) throw std::logic_error("planner made no progress");
     make_rounds(pass, R, nqubits);
-    plan.passes.push_back(std::move(pass));
+    split_pass(pass, plan.passes);
   }
   plan.perm_after = cur;
   plan.gates = nops;
@@ -447,7 +506,9 @@ std::string plan_to_json(const Plan& p, bool detail) {
         for (size_t o = 0; o < pr.ops.size(); ++o) {
           const DOp d = encode_op(ps.ops[pr.ops[o]], ps.tile_phys, pr.reg);
           if (o) os << ",";
-          os << "[" << d.type << "," << d.a << "," << d.b << "," << d.lmask << ","
+          os << "[" << (d.variant >> 9) << "," << ((d.variant >> 6) & 7) << ","
+             << static_cast<int>((d.variant >> 3) & 7) - 1 << ","
+             << static_cast<int>(d.variant & 7) - 1 << "," << d.lmask << ","
              << d.gmask << "," << d.dl << "," << d.dg;
           for (int k = 0; k < 8; ++k) {
             std::snprintf(num, sizeof(num), ",%.17g", d.m[k]);

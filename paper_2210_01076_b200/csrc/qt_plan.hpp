@@ -11,7 +11,7 @@ namespace qtb {
 struct PlanOptions {
   int tile_bits = 12;  // qubits per shared-memory tile
   int low_bits = 4;    // lowest physical bits always in the tile (coalescing)
-  int reg_bits = 3;    // qubits per register round (2^reg amplitudes/thread)
+  int reg_bits = kMaxRegBits;  // qubits per register round (2^reg amps/thread)
   int lookahead = 4096;// ops scanned per pass
 };
 

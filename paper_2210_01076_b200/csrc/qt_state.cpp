@@ -69,7 +69,6 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   cuda_check(cudaMalloc(&d_flag_, sizeof(int)), "flag");
   cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "flag init");
   cuda_check(cudaMallocHost(&h_flag_, sizeof(int)), "pinned flag");
-  cuda_check(cudaEventCreateWithFlags(&stage_free_, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreate(&ev0_), "event");
   cuda_check(cudaEventCreate(&ev1_), "event");
   perm_.resize(n_);
@@ -95,11 +94,8 @@ State::~State() {
   for (double2* b : pool_) cudaFree(b);
   cudaFree(d_scratch_);
   cudaFree(d_flag_);
-  cudaFree(d_plan_);
   cudaFree(d_tmp_);
   if (h_flag_) cudaFreeHost(h_flag_);
-  if (h_stage_) cudaFreeHost(h_stage_);
-  if (stage_free_) cudaEventDestroy(stage_free_);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -244,66 +240,32 @@ void State::apply_ops(const std::vector<LOp>& ops, uint64_t ngates,
   perm_ = p.perm_after;
 }
 
-void State::ensure_device_bytes(size_t bytes) {
-  if (bytes <= d_plan_cap_) return;
-  cuda_check(cudaStreamSynchronize(stream_), "sync");
-  cudaFree(d_plan_);
-  d_plan_ = nullptr;
-  d_plan_cap_ = std::max(bytes, d_plan_cap_ * 2);
-  cuda_check(cudaMalloc(&d_plan_, d_plan_cap_), "plan buffer");
+namespace {
+
+// Fills a kernel-parameter block for one tile pass: rounds, then the ops of
+// each round in order (encoded against the round's register bits).
+template <typename P>
+void fill_pass(P& kp, const PlanPass& ps) {
+  kp.h.nrounds = static_cast<uint32_t>(ps.rounds.size());
+  uint32_t nops = 0;
+  for (size_t r = 0; r < ps.rounds.size(); ++r) {
+    const PlanRound& pr = ps.rounds[r];
+    DRound& dr = kp.rounds[r];
+    dr = DRound{};
+    dr.op_first = static_cast<uint16_t>(nops);
+    dr.op_count = static_cast<uint16_t>(pr.ops.size());
+    for (size_t i = 0; i < pr.reg.size() && i < static_cast<size_t>(kMaxRegBits); ++i)
+      dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
+    for (int idx : pr.ops) kp.ops[nops++] = encode_op(ps.ops[idx], ps.tile_phys, pr.reg);
+  }
+  kp.h.nops = nops;
 }
 
-void State::upload_and_launch(const Plan& plan, const double2* src) {
-  // ---- flatten rounds + ops --------------------------------------------
-  std::vector<DRound> rounds;
-  std::vector<DOp> dops;
-  struct PassRef {
-    size_t round_first, round_count;
-  };
-  std::vector<PassRef> refs(plan.passes.size());
-  for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
-    const PlanPass& ps = plan.passes[pi];
-    refs[pi].round_first = rounds.size();
-    refs[pi].round_count = 0;
-    if (ps.kind != PlanPass::Tile) continue;
-    for (const PlanRound& pr : ps.rounds) {
-      DRound dr{};
-      dr.nreg = static_cast<uint8_t>(pr.reg.size());
-      for (size_t i = 0; i < pr.reg.size() && i < kMaxRegBits; ++i)
-        dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
-      dr.op_first = static_cast<uint32_t>(dops.size());
-      dr.op_count = static_cast<uint32_t>(pr.ops.size());
-      for (int idx : pr.ops) dops.push_back(encode_op(ps.ops[idx], ps.tile_phys, pr.reg));
-      rounds.push_back(dr);
-      refs[pi].round_count++;
-    }
-  }
-  const size_t rbytes = (rounds.size() * sizeof(DRound) + 255) & ~size_t(255);
-  const size_t total = rbytes + dops.size() * sizeof(DOp);
-  if (total > 0) {
-    ensure_device_bytes(total);
-    if (total > h_stage_cap_) {
-      cuda_check(cudaEventSynchronize(stage_free_), "stage sync");
-      if (h_stage_) cudaFreeHost(h_stage_);
-      h_stage_cap_ = std::max(total, h_stage_cap_ * 2);
-      cuda_check(cudaMallocHost(&h_stage_, h_stage_cap_), "pinned stage");
-    } else {
-      cuda_check(cudaEventSynchronize(stage_free_), "stage sync");
-    }
-    std::memcpy(h_stage_, rounds.data(), rounds.size() * sizeof(DRound));
-    std::memcpy(static_cast<char*>(h_stage_) + rbytes, dops.data(),
-                dops.size() * sizeof(DOp));
-    cuda_check(cudaMemcpyAsync(d_plan_, h_stage_, total, cudaMemcpyHostToDevice, stream_),
-               "plan upload");
-    cuda_check(cudaEventRecord(stage_free_, stream_), "event");
-  }
-  const DRound* d_rounds = static_cast<const DRound*>(d_plan_);
-  const DOp* d_ops = reinterpret_cast<const DOp*>(static_cast<char*>(d_plan_) + rbytes);
+}  // namespace
 
-  // ---- launch -------------------------------------------------------------
+void State::upload_and_launch(const Plan& plan, const double2* src) {
   cuda_check(cudaEventRecord(ev0_, stream_), "event");
-  // per-launch events accumulate until last_timings() collects them
-  size_t timing_idx = timings_used_;
+  size_t timing_idx = timings_used_;  // events accumulate until collected
   auto tstart = [&](int kind) {
     if (!timing_) return;
     if (timing_idx >= timings_.size()) {
@@ -330,6 +292,8 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
     src = nullptr;
   }
+  if (!kp_small_) kp_small_.reset(new KPassSmall);
+  if (!kp_large_) kp_large_.reset(new KPassLarge);
   for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
     const PlanPass& ps = plan.passes[pi];
     if (ps.kind == PlanPass::Exchange) {
@@ -342,31 +306,37 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     }
     const int k = static_cast<int>(ps.tile_phys.size());
     const int R = std::min(opt_.reg_bits, k);
-    KPass kp{};
-    kp.k = static_cast<uint32_t>(k);
-    kp.reg_bits = static_cast<uint32_t>(R);
-    kp.nrounds = static_cast<uint32_t>(refs[pi].round_count);
-    kp.rounds = d_rounds + refs[pi].round_first;
-    kp.ops = d_ops;
-    kp.flag = d_flag_;
-    kp.src = src ? src : psi_;
+    KPassHead h{};
+    h.k = static_cast<uint32_t>(k);
+    h.reg_bits = static_cast<uint32_t>(R);
+    h.flag = d_flag_;
+    h.src = src ? src : psi_;
     src = nullptr;
     uint64_t tile_mask = 0;
     for (int i = 0; i < k; ++i) {
       const uint64_t b = 1ull << ps.tile_phys[i];
       tile_mask |= b;
-      if (i < k - R) kp.lo_mask |= b;
-      else kp.hi_mask |= b;
+      if (i < k - R) h.lo_mask |= b;
+      else h.hi_mask |= b;
     }
-    kp.outer_mask = buf_mask & ~tile_mask;
-    kp.nouter = static_cast<uint32_t>(buf_bits_ - k);
-    kp.ntiles = 1ull << (buf_bits_ - k);
-    kp.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
-    const int occ = std::max(1, tile_pass_occupancy(k, R));
+    h.outer_mask = buf_mask & ~tile_mask;
+    h.ntiles = 1ull << (buf_bits_ - k);
+    h.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
+    const bool large = ps.ops.size() > static_cast<size_t>(kSmallOps) ||
+                       ps.rounds.size() > static_cast<size_t>(kSmallRounds);
+    const int occ = std::max(1, tile_pass_occupancy(k, R, large));
     const uint64_t cap = static_cast<uint64_t>(occ) * sms_;
-    const int grid = static_cast<int>(std::min<uint64_t>(kp.ntiles, cap));
+    const int grid = static_cast<int>(std::min<uint64_t>(h.ntiles, cap));
     tstart(0);
-    cuda_check(launch_tile_pass(psi_, kp, grid, stream_), "tile pass launch");
+    if (large) {
+      kp_large_->h = h;
+      fill_pass(*kp_large_, ps);
+      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, stream_), "tile pass launch");
+    } else {
+      kp_small_->h = h;
+      fill_pass(*kp_small_, ps);
+      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, stream_), "tile pass launch");
+    }
     tstop();
     stats.passes += 1;
     stats.kernel_launches += 1;

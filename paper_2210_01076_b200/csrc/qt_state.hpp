@@ -10,6 +10,7 @@
 
 #include "qt_comm.hpp"
 #include "qt_ir.hpp"
+#include "qt_kernels.hpp"
 #include "qt_plan.hpp"
 #include "qtask_c.h"
 
@@ -87,7 +88,6 @@ class State {
  private:
   void upload_and_launch(const Plan& plan, const double2* src);
   void exchange(const PlanPass& pass);
-  void ensure_device_bytes(size_t bytes);
 
   int n_ = 0, nlocal_ = 0, buf_bits_ = 0;
   Mode mode_ = Mode::Single;
@@ -97,11 +97,9 @@ class State {
   double* d_scratch_ = nullptr;   // norm partials + result + gather
   int* d_flag_ = nullptr;
   int* h_flag_ = nullptr;         // pinned
-  void* d_plan_ = nullptr;        // rounds + ops
-  size_t d_plan_cap_ = 0;
-  void* h_stage_ = nullptr;       // pinned staging for the plan upload
-  size_t h_stage_cap_ = 0;
-  cudaEvent_t stage_free_ = nullptr;
+  // kernel-parameter blocks (ops travel in the launch's constant bank)
+  std::unique_ptr<KPassSmall> kp_small_;
+  std::unique_ptr<KPassLarge> kp_large_;
   double2* d_tmp_ = nullptr;      // exchange receive buffer
   size_t d_tmp_amps_ = 0;
   std::vector<int> perm_;         // logical -> physical

@@ -35,11 +35,17 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
         for rd in ps["round_detail"]:
             reg = rd["reg"]
             for op in rd["ops"]:
-                typ, a, b, lmask, gmask, dl, dg = (int(x) for x in op[:7])
-                m = np.array(op[7:15], dtype=np.float64)
+                # [type, a, cs, ds, lmask, gmask, dl, dg, m0..m7]: a = target
+                # register slot, cs / ds = control / diagonal-target slot (-1:
+                # not a register bit; SWAP2 keeps its second slot in ds)
+                typ, a, cs, ds, lmask, gmask, dl, dg = (int(x) for x in op[:8])
+                b = ds
+                m = np.array(op[8:16], dtype=np.float64)
                 m = m[0::2] + 1j * m[1::2]
                 # control predicate over physical bits
                 ok = np.ones(len(psi), dtype=bool)
+                if cs >= 0:
+                    ok &= _bit(idx, tile[reg[cs]]) == 1
                 for tb in range(len(tile)):
                     if (lmask >> tb) & 1:
                         ok &= _bit(idx, tile[tb]) == 1
@@ -62,7 +68,9 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
                         psi[lo] = m[1] * y
                         psi[hi] = m[2] * x
                 elif typ in (D_DIAG, D_SIGN, D_PHASE1):
-                    if dl:
+                    if ds >= 0:
+                        bit = _bit(idx, tile[reg[ds]]) == 1
+                    elif dl:
                         tb = int(dl).bit_length() - 1
                         bit = _bit(idx, tile[tb]) == 1
                     else:
