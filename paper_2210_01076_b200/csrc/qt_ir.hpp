@@ -52,6 +52,7 @@ struct LOp {
 // ---------------------------------------------------------------------------
 
 enum DType : uint32_t {
+  // single ops (data: one 2x2 matrix, 8 doubles, in the pass pool)
   D_DENSE = 0,   // 2x2 complex on reg slot a                  (8 DFMA/amp)
   D_REAL = 1,    // 2x2 real on reg slot a                     (4 DFMA/amp)
   D_DIAG = 2,    // diag(d0, d1) on a bit anywhere             (4 DFMA/amp)
@@ -60,30 +61,59 @@ enum DType : uint32_t {
   D_ANTI = 5,    // scaled swap [[0,m01],[m10,0]] on slot a    (4 DFMA/amp)
   D_SWAP2 = 6,   // swap qubits on reg slots a and b
   D_PHASE1 = 7,  // multiply by d1 where bit set (S, T, phase) (4 DFMA/amp)
+  // fused layer ops built by the round compiler (qt_plan.cpp)
+  D_MULTI = 8,   // complex 2x2 on every reg slot in mask a, ascending slots
+  D_MULTIR = 9,  // real 2x2 (4 doubles) on every reg slot in mask a
+  D_DTAB = 10,   // per-slot complex factor table (2^R entries)
+  D_STAB = 11,   // sign terms: slot masks negated under thread/tile conditions
 };
 
 // Variant id of a device op: the kernel dispatches on it to a fully
 // specialised code path (register slots known at compile time, no per-slot
 // predication). cs / ds are -1 when the control / diagonal target is not a
-// register bit of the round; SWAP2 stores its second slot in ds.
+// register bit of the round; SWAP2 stores its second slot in ds; MULTI /
+// MULTIR store their slot mask in a.
 constexpr uint32_t vid(uint32_t type, int a, int cs, int ds) {
-  return (type << 9) | (uint32_t(a) << 6) | (uint32_t(cs + 1) << 3) | uint32_t(ds + 1);
+  return (type << 10) | (uint32_t(a) << 6) | (uint32_t(cs + 1) << 3) | uint32_t(ds + 1);
 }
 
-// 96 bytes; lives in the kernel-parameter constant bank (read uniformly).
-struct alignas(16) DOp {
-  uint32_t variant;  // vid(type, a, cs, ds)
+// Header word of a device op: variant id in the low 14 bits, flags above.
+constexpr uint32_t kOpVariantMask = 0x3fff;
+constexpr uint32_t kOpLctl = 1u << 16;  // lmask != 0
+constexpr uint32_t kOpGctl = 1u << 17;  // gmask != 0
+constexpr uint32_t kOpDl = 1u << 18;    // dl != 0
+constexpr uint32_t kOpDg = 1u << 19;    // dg != 0
+constexpr uint32_t kOpFlagMask = kOpLctl | kOpGctl | kOpDl | kOpDg;
+// dense dispatch index of the variant (tools/gen_variants.py) in bits 20..27
+constexpr uint32_t kOpIndexShift = 20;
+
+// 32 bytes; lives in the kernel-parameter constant bank (read uniformly).
+// Matrices / tables / sign terms are in the pass's double pool at `arg`.
+struct alignas(8) DOp {
+  uint32_t hdr;      // vid(type, a, cs, ds) | flags
+  uint32_t arg;      // pool offset (doubles); STAB: offset | nterms << 16
   uint32_t lmask;    // control bits among the round's NON-register tile bits
   uint32_t dl;       // diag target among non-register tile bits (mask) or 0
-  uint32_t pad;
   uint64_t gmask;    // control bits outside the tile (global index bits)
   uint64_t dg;       // diag target outside the tile (mask) or 0
-  double m[8];       // interleaved row-major 2x2 (diag: m[0..1]=d0, m[6..7]=d1)
 };
-static_assert(sizeof(DOp) == 96, "DOp layout");
+static_assert(sizeof(DOp) == 32, "DOp layout");
+
+// One sign term of a D_STAB op (two pool words): negate the register slots
+// in `slots` when (j & lcond) == lcond and (g & gcond) == gcond.
+struct SignTerm {
+  uint32_t slots;    // bit s set: slot s is negated
+  uint32_t lcond;    // non-register tile bits that must be 1
+  uint64_t gcond;    // global bits that must be 1
+};
 
 constexpr int kMaxTileBits = 13;  // 2^13 x 16 B = 128 KiB of smem
 constexpr int kMaxRegBits = 4;
+// Defaults (overridable per state; QTB_TILE_BITS / QTB_REG_BITS for sweeps):
+// 2^11-amplitude tiles (32 KiB smem), 4 register bits -> 128 threads of 16
+// amplitudes, <= 128 registers (measured best on C3, B200).
+constexpr int kDefaultTileBits = 11;
+constexpr int kDefaultRegBits = 4;
 
 struct DRound {
   uint16_t op_first;  // into the pass's op array
@@ -93,9 +123,15 @@ struct DRound {
 static_assert(sizeof(DRound) == 8, "DRound layout");
 
 // Per-launch capacity of the kernel-parameter block (<= 32764 bytes): a
-// pass with more ops / rounds is split by the planner.
-constexpr int kSmallOps = 32, kSmallRounds = 16;
-constexpr int kLargeOps = 288, kLargeRounds = 96;
+// pass with more ops / rounds / pool is split by the planner.
+constexpr int kSmallOps = 32, kSmallRounds = 16, kSmallPool = 320;
+constexpr int kLargeOps = 256, kLargeRounds = 96, kLargePool = 2560;
+
+// A device-encoded round (host side): its ops and their pool data.
+struct EncRound {
+  std::vector<DOp> ops;
+  std::vector<double> pool;  // offsets in ops are relative to this vector
+};
 
 // ---------------------------------------------------------------------------
 // Host plan
@@ -104,6 +140,7 @@ constexpr int kLargeOps = 288, kLargeRounds = 96;
 struct PlanRound {
   std::vector<int> reg;          // tile-bit indices
   std::vector<int> ops;          // indices into the pass op list (LOp order)
+  EncRound enc;                  // device encoding (compile_round)
 };
 
 struct PlanPass {

@@ -26,14 +26,15 @@ struct KPassHead {
 
 // Kernel parameters (passed by value as a __grid_constant__: the rounds and
 // ops are read from the constant bank, uniformly across the CTA).
-template <int OPS, int ROUNDS>
+template <int OPS, int ROUNDS, int POOL>
 struct KPass {
   KPassHead h;
   DRound rounds[ROUNDS];
   DOp ops[OPS];
+  double pool[POOL];  // matrices, diagonal tables, sign terms
 };
-using KPassSmall = KPass<kSmallOps, kSmallRounds>;
-using KPassLarge = KPass<kLargeOps, kLargeRounds>;
+using KPassSmall = KPass<kSmallOps, kSmallRounds, kSmallPool>;
+using KPassLarge = KPass<kLargeOps, kLargeRounds, kLargePool>;
 static_assert(sizeof(KPassLarge) <= 32764, "kernel parameter limit");
 
 // Fused tile pass over a state of 2^nlocal amplitudes.

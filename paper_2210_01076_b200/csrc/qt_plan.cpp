@@ -16,7 +16,9 @@
 #include "qt_plan.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <limits>
 #include <sstream>
 #include <stdexcept>
@@ -147,61 +149,297 @@ void fuse_ops(std::vector<LOp>& ops, int nqubits) {
   ops.swap(kept);
 }
 
-DOp encode_op(const LOp& op, const std::vector<int>& tile_phys,
-              const std::vector<int>& reg) {
-  DOp d{};
-  const uint32_t type = dtype_of(op);
-  auto tile_index = [&](int phys) -> int {
+namespace {
+
+// Placement of a physical qubit in a round: register slot, else tile bit,
+// else outside the tile.
+struct Place {
+  const std::vector<int>& tile_phys;
+  const std::vector<int>& reg;
+  int tile(int phys) const {
     for (size_t i = 0; i < tile_phys.size(); ++i)
       if (tile_phys[i] == phys) return static_cast<int>(i);
     return -1;
-  };
-  auto reg_slot = [&](int phys) -> int {
-    const int ti = tile_index(phys);
+  }
+  int slot(int phys) const {
+    const int ti = tile(phys);
     if (ti < 0) return -1;
     for (size_t i = 0; i < reg.size(); ++i)
       if (reg[i] == ti) return static_cast<int>(i);
     return -1;
-  };
+  }
+};
+
+void push_matrix(std::vector<double>& pool, const cplx* m) {
+  for (int k = 0; k < 4; ++k) {
+    pool.push_back(m[k].re);
+    pool.push_back(m[k].im);
+  }
+}
+
+}  // namespace
+
+void encode_single(const LOp& op, const std::vector<int>& tile_phys,
+                   const std::vector<int>& reg, EncRound& out) {
+  const Place pl{tile_phys, reg};
+  DOp d{};
+  const uint32_t type = dtype_of(op);
   int a = 0, cs = -1, ds = -1;
   if (op.kind == LKind::Diag) {
-    ds = reg_slot(op.target);
+    ds = pl.slot(op.target);
     if (ds < 0) {
-      const int ti = tile_index(op.target);
+      const int ti = pl.tile(op.target);
       if (ti >= 0) d.dl = 1u << ti;  // thread-uniform bit
       else d.dg = 1ull << op.target; // tile-uniform bit
     }
   } else {
-    a = reg_slot(op.target);
+    a = pl.slot(op.target);
     if (a < 0) throw std::logic_error("op target is not a register bit of its round");
     if (op.kind == LKind::Swap) {
-      int b = reg_slot(op.target2);
+      int b = pl.slot(op.target2);
       if (b < 0) throw std::logic_error("swap target is not a register bit");
       if (a > b) std::swap(a, b);
       ds = b;  // SWAP2 carries its second slot in ds
     }
   }
   if (op.control >= 0) {
-    cs = reg_slot(op.control);
+    cs = pl.slot(op.control);
     if (cs < 0) {
-      const int ti = tile_index(op.control);
+      const int ti = pl.tile(op.control);
       if (ti >= 0) d.lmask = 1u << ti;
       else d.gmask = 1ull << op.control;
     }
   }
-  d.variant = vid(type, a, cs, ds);
-  for (int k = 0; k < 4; ++k) {
-    d.m[2 * k] = op.m[k].re;
-    d.m[2 * k + 1] = op.m[k].im;
+  d.hdr = vid(type, a, cs, ds) | (d.lmask ? kOpLctl : 0u) | (d.gmask ? kOpGctl : 0u) |
+          (d.dl ? kOpDl : 0u) | (d.dg ? kOpDg : 0u);
+  d.arg = static_cast<uint32_t>(out.pool.size());
+  push_matrix(out.pool, op.m);
+  out.ops.push_back(d);
+}
+
+// ---------------------------------------------------------------------------
+// Round compiler: turns a round's op sequence into fused LAYERS
+//   [pre diagonal table][pre sign terms][one 2x2 per register slot]
+// Dense single-qubit gates on distinct register slots commute, so each
+// layer's MULTI op applies up to R of them in one dispatch. A well-conditioned
+// complex 2x2 U is factored U = diag(p0,p1) . [[c,-s],[s,c]] . diag(1,q1)
+// (ZYZ with the global phase folded in): the real rotation goes to the layer
+// (4 FP64 ops per amplitude instead of 8) and the diagonals join the
+// neighbouring tables, where every diagonal factor of the round (RZ, S, T,
+// CZ, controlled phases on register slots) is merged into one per-slot
+// multiply or one integer sign flip.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr double kZyzMin = 0.05;  // min(|u00|, |u10|) for the factorisation
+
+struct LayerState {
+  int R, NS;
+  std::vector<cplx> pre, post;
+  bool pre_used = false, post_used = false;
+  std::vector<SignTerm> pre_signs, post_signs;
+  uint32_t post_slots = 0;  // register slots the post factors depend on
+  cplx M[kMaxRegBits][4];
+  uint32_t mmask = 0;
+  bool mreal = true;
+
+  explicit LayerState(int r) : R(r), NS(1 << r), pre(1 << r), post(1 << r) {
+    for (auto& c : pre) c = cplx{1.0, 0.0};
+    for (auto& c : post) c = cplx{1.0, 0.0};
   }
-  return d;
+};
+
+bool table_trivial(const std::vector<cplx>& t) {
+  for (const cplx& c : t)
+    if (c.re != 1.0 || c.im != 0.0) return false;
+  return true;
+}
+
+void emit_table(const std::vector<cplx>& t, EncRound& out) {
+  if (table_trivial(t)) return;
+  DOp d{};
+  d.hdr = vid(D_DTAB, 0, -1, -1);
+  d.arg = static_cast<uint32_t>(out.pool.size());
+  for (const cplx& c : t) {
+    out.pool.push_back(c.re);
+    out.pool.push_back(c.im);
+  }
+  out.ops.push_back(d);
+}
+
+void emit_signs(const std::vector<SignTerm>& terms, EncRound& out) {
+  if (terms.empty()) return;
+  DOp d{};
+  d.hdr = vid(D_STAB, 0, -1, -1);
+  const uint32_t off = static_cast<uint32_t>(out.pool.size());
+  d.arg = off | (static_cast<uint32_t>(terms.size()) << 16);
+  for (const SignTerm& t : terms) {
+    const uint64_t w0 = static_cast<uint64_t>(t.slots) | (static_cast<uint64_t>(t.lcond) << 32);
+    double dw0, dw1;
+    std::memcpy(&dw0, &w0, 8);
+    std::memcpy(&dw1, &t.gcond, 8);
+    out.pool.push_back(dw0);
+    out.pool.push_back(dw1);
+  }
+  out.ops.push_back(d);
+}
+
+void emit_multi(LayerState& L, EncRound& out) {
+  if (!L.mmask) return;
+  DOp d{};
+  d.hdr = vid(L.mreal ? D_MULTIR : D_MULTI, static_cast<int>(L.mmask), -1, -1);
+  d.arg = static_cast<uint32_t>(out.pool.size());
+  for (int i = 0; i < L.R; ++i) {
+    if (!(L.mmask & (1u << i))) continue;
+    if (L.mreal) {
+      for (int k = 0; k < 4; ++k) out.pool.push_back(L.M[i][k].re);
+    } else {
+      push_matrix(out.pool, L.M[i]);
+    }
+  }
+  out.ops.push_back(d);
+  L.mmask = 0;
+  L.mreal = true;
+}
+
+// Emits the pre part and the layer's MULTI; the post part becomes the next
+// layer's pre part.
+void close_layer(LayerState& L, EncRound& out) {
+  emit_table(L.pre, out);
+  emit_signs(L.pre_signs, out);
+  emit_multi(L, out);
+  L.pre.swap(L.post);
+  L.pre_signs.swap(L.post_signs);
+  for (auto& c : L.post) c = cplx{1.0, 0.0};
+  L.post_signs.clear();
+  L.post_slots = 0;
+}
+
+void flush_all(LayerState& L, EncRound& out) {
+  close_layer(L, out);
+  emit_table(L.pre, out);
+  emit_signs(L.pre_signs, out);
+  for (auto& c : L.pre) c = cplx{1.0, 0.0};
+  L.pre_signs.clear();
+}
+
+inline bool bit_of(int s, int slot) { return slot >= 0 && ((s >> slot) & 1); }
+
+#include "qt_variant_ids.inc"
+
+// Stores each op's dense dispatch index (the kernel's switch key).
+void set_dispatch_index(EncRound& out, int R) {
+  for (DOp& d : out.ops) {
+    const uint16_t idx = variant_index(R, d.hdr & kOpVariantMask);
+    if (idx == 0xffff) throw std::logic_error("device op without a kernel variant");
+    d.hdr = (d.hdr & ~(0xffu << kOpIndexShift)) | (static_cast<uint32_t>(idx) << kOpIndexShift);
+  }
+}
+
+}  // namespace
+
+EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse) {
+  EncRound out;
+  const int R = static_cast<int>(round.reg.size());
+  const Place pl{pass.tile_phys, round.reg};
+  if (!fuse) {
+    for (int idx : round.ops) encode_single(pass.ops[idx], pass.tile_phys, round.reg, out);
+    set_dispatch_index(out, R);
+    return out;
+  }
+  LayerState L(R);
+  for (int idx : round.ops) {
+    const LOp& op = pass.ops[idx];
+    const uint32_t type = dtype_of(op);
+    const int cslot = op.control >= 0 ? pl.slot(op.control) : -1;
+    // ---- sign flips (Z, CZ) anywhere: an integer sign term --------------------
+    if (type == D_SIGN) {
+      SignTerm t{};
+      const int tslot = pl.slot(op.target);
+      uint32_t deps = 0;
+      for (int s = 0; s < L.NS; ++s) {
+        const bool tgt = tslot >= 0 ? bit_of(s, tslot) : true;
+        const bool ctl = op.control < 0 || cslot < 0 ? true : bit_of(s, cslot);
+        if (tgt && ctl) t.slots |= 1u << s;
+      }
+      if (tslot >= 0) deps |= 1u << tslot;
+      else if (pl.tile(op.target) >= 0) t.lcond |= 1u << pl.tile(op.target);
+      else t.gcond |= 1ull << op.target;
+      if (op.control >= 0) {
+        if (cslot >= 0) deps |= 1u << cslot;
+        else if (pl.tile(op.control) >= 0) t.lcond |= 1u << pl.tile(op.control);
+        else t.gcond |= 1ull << op.control;
+      }
+      L.post_signs.push_back(t);
+      L.post_slots |= deps;
+      continue;
+    }
+    // ---- diagonal ops living on register slots: one table ----------------------
+    if (type == D_DIAG || type == D_PHASE1) {
+      const int tslot = pl.slot(op.target);
+      if (tslot >= 0 && (op.control < 0 || cslot >= 0)) {
+        for (int s = 0; s < L.NS; ++s) {
+          if (op.control >= 0 && !bit_of(s, cslot)) continue;
+          L.post[s] = cmul(L.post[s], bit_of(s, tslot) ? op.m[3] : op.m[0]);
+        }
+        L.post_slots |= 1u << tslot;
+        if (cslot >= 0) L.post_slots |= 1u << cslot;
+        continue;
+      }
+    }
+    // ---- uncontrolled dense on a register slot: into the layer -----------------
+    if ((type == D_DENSE || type == D_REAL) && op.control < 0) {
+      const int a = pl.slot(op.target);
+      cplx R2[4] = {op.m[0], op.m[1], op.m[2], op.m[3]};
+      cplx d1 = {1.0, 0.0}, p0 = {1.0, 0.0}, p1 = {1.0, 0.0};
+      bool factored = false;
+      bool real = type == D_REAL;
+      if (!real) {
+        const double c = std::hypot(op.m[0].re, op.m[0].im);
+        const double sn = std::hypot(op.m[2].re, op.m[2].im);
+        if (c > kZyzMin && sn > kZyzMin) {
+          // U = diag(p0, p1) . [[c, -s], [s, c]] . diag(1, q1)
+          p0 = cplx{op.m[0].re / c, op.m[0].im / c};
+          p1 = cplx{op.m[2].re / sn, op.m[2].im / sn};
+          // q1 = -u01 / (p0 s) = -u01 conj(p0) / s   (|p0| = 1)
+          const cplx u01 = op.m[1];
+          const cplx pc = {p0.re, -p0.im};
+          const cplx t = cmul(u01, pc);
+          d1 = cplx{-t.re / sn, -t.im / sn};
+          R2[0] = {c, 0.0};
+          R2[1] = {-sn, 0.0};
+          R2[2] = {sn, 0.0};
+          R2[3] = {c, 0.0};
+          factored = true;
+          real = true;
+        }
+      }
+      if ((L.mmask & (1u << a)) || (L.post_slots & (1u << a))) close_layer(L, out);
+      if (factored) {
+        for (int s = 0; s < L.NS; ++s)
+          if (bit_of(s, a)) L.pre[s] = cmul(L.pre[s], d1);
+        for (int s = 0; s < L.NS; ++s) L.post[s] = cmul(L.post[s], bit_of(s, a) ? p1 : p0);
+        L.post_slots |= 1u << a;
+      }
+      for (int k = 0; k < 4; ++k) L.M[a][k] = R2[k];
+      L.mmask |= 1u << a;
+      L.mreal = L.mreal && real;
+      continue;
+    }
+    // ---- anything else: flush, then a single op --------------------------------
+    flush_all(L, out);
+    encode_single(op, pass.tile_phys, round.reg, out);
+  }
+  flush_all(L, out);
+  set_dispatch_index(out, R);
+  return out;
 }
 
 namespace {
 
 // Splits the ops of one pass (physical qubits, application order) into
-// register rounds of R tile bits.
-void make_rounds(PlanPass& pass, int R, int nphys) {
+// register rounds of R tile bits, then device-encodes every round.
+void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt) {
   const int k = static_cast<int>(pass.tile_phys.size());
   std::vector<int> tix(nphys, -1);
   for (int i = 0; i < k; ++i) tix[pass.tile_phys[i]] = i;
@@ -219,8 +457,8 @@ void make_rounds(PlanPass& pass, int R, int nphys) {
     for (int idx : remaining) {
       const LOp& op = pass.ops[idx];
       const int nr = roles(op, rl);
-      bool can = true;
-      for (int t = 0; t < nr; ++t) {
+      bool can = static_cast<int>(round.ops.size()) < opt.max_round_ops;
+      for (int t = 0; t < nr && can; ++t) {
         if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
       }
       if (can) {
@@ -259,51 +497,41 @@ void make_rounds(PlanPass& pass, int R, int nphys) {
         round.reg.push_back(ti);
       }
     }
+    round.enc = compile_round(pass, round, opt.fuse_layers);
     pass.rounds.push_back(std::move(round));
     remaining.swap(rest);
   }
 }
 
-// A launch carries at most kLargeOps ops in kLargeRounds rounds (kernel
-// parameter space); deeper passes become consecutive launches on the same
-// tile (only FP64-bound passes are that deep, so the extra HBM sweep hides).
+// A launch carries at most kLargeOps device ops, kLargeRounds rounds and
+// kLargePool pool doubles (kernel parameter space); deeper passes become
+// consecutive launches on the same tile (only FP64-bound passes are that
+// deep, so the extra HBM sweep hides).
 void split_pass(PlanPass& pass, std::vector<PlanPass>& out) {
   size_t r = 0;
   while (r < pass.rounds.size()) {
     PlanPass part;
     part.kind = PlanPass::Tile;
     part.tile_phys = pass.tile_phys;
+    size_t nops = 0, npool = 0;
     while (r < pass.rounds.size() &&
            static_cast<int>(part.rounds.size()) < kLargeRounds &&
-           part.ops.size() + pass.rounds[r].ops.size() <= static_cast<size_t>(kLargeOps)) {
+           nops + pass.rounds[r].enc.ops.size() <= static_cast<size_t>(kLargeOps) &&
+           npool + pass.rounds[r].enc.pool.size() <= static_cast<size_t>(kLargePool)) {
       PlanRound pr;
       pr.reg = pass.rounds[r].reg;
       for (int idx : pass.rounds[r].ops) {
         pr.ops.push_back(static_cast<int>(part.ops.size()));
         part.ops.push_back(pass.ops[idx]);
       }
+      pr.enc = std::move(pass.rounds[r].enc);
+      nops += pr.enc.ops.size();
+      npool += pr.enc.pool.size();
       part.rounds.push_back(std::move(pr));
       ++r;
     }
-    if (part.rounds.empty()) {
-      // a single round with more than kLargeOps ops: split the round itself
-      const PlanRound& big = pass.rounds[r];
-      for (size_t o = 0; o < big.ops.size(); o += kLargeOps) {
-        PlanPass piece;
-        piece.kind = PlanPass::Tile;
-        piece.tile_phys = pass.tile_phys;
-        PlanRound pr;
-        pr.reg = big.reg;
-        for (size_t u = o; u < big.ops.size() && u < o + kLargeOps; ++u) {
-          pr.ops.push_back(static_cast<int>(piece.ops.size()));
-          piece.ops.push_back(pass.ops[big.ops[u]]);
-        }
-        piece.rounds.push_back(std::move(pr));
-        out.push_back(std::move(piece));
-      }
-      ++r;
-      continue;
-    }
+    if (part.rounds.empty())
+      throw std::logic_error("a register round exceeds the kernel parameter space");
     out.push_back(std::move(part));
   }
 }
@@ -450,7 +678,7 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
     for (int p = 0; p < nlocal; ++p)
       if (inQ[p]) pass.tile_phys.push_back(p);
     if (pass.ops.empty()) throw std::logic_error("planner made no progress");
-    make_rounds(pass, R, nqubits);
+    make_rounds(pass, R, nqubits, opt);
     split_pass(pass, plan.passes);
   }
   plan.perm_after = cur;
@@ -475,9 +703,25 @@ std::string plan_to_json(const Plan& p, bool detail) {
       os << "]}";
       continue;
     }
+    // FP64-pipe instructions per amplitude of the encoded (fused) ops
     double fp = 0.0;
-    for (const LOp& op : ps.ops) fp += op_fp64_per_amp(op);
-    os << "{\"kind\":\"tile\",\"tile\":[";
+    size_t ndev = 0;
+    for (const PlanRound& pr : ps.rounds) {
+      ndev += pr.enc.ops.size();
+      for (const DOp& d : pr.enc.ops) {
+        const uint32_t v = d.hdr & kOpVariantMask, type = v >> 10, a = (v >> 6) & 15;
+        const bool ctl = ((v >> 3) & 7) != 0;
+        switch (type) {
+          case D_DENSE: fp += ctl ? 4.0 : 8.0; break;
+          case D_REAL: case D_ANTI: fp += ctl ? 2.0 : 4.0; break;
+          case D_DIAG: case D_PHASE1: case D_DTAB: fp += 4.0; break;
+          case D_MULTI: fp += 8.0 * __builtin_popcount(a); break;
+          case D_MULTIR: fp += 4.0 * __builtin_popcount(a); break;
+          default: break;
+        }
+      }
+    }
+    os << "{\"kind\":\"tile\",\"device_ops\":" << ndev << ",\"tile\":[";
     for (size_t t = 0; t < ps.tile_phys.size(); ++t) {
       if (t) os << ",";
       os << ps.tile_phys[t];
@@ -503,18 +747,36 @@ std::string plan_to_json(const Plan& p, bool detail) {
         os << "{\"reg\":[";
         for (size_t i = 0; i < pr.reg.size(); ++i) os << (i ? "," : "") << pr.reg[i];
         os << "],\"ops\":[";
-        for (size_t o = 0; o < pr.ops.size(); ++o) {
-          const DOp d = encode_op(ps.ops[pr.ops[o]], ps.tile_phys, pr.reg);
+        const int NS = 1 << pr.reg.size();
+        for (size_t o = 0; o < pr.enc.ops.size(); ++o) {
+          const DOp& d = pr.enc.ops[o];
           if (o) os << ",";
-          os << "[" << (d.variant >> 9) << "," << ((d.variant >> 6) & 7) << ","
-             << static_cast<int>((d.variant >> 3) & 7) - 1 << ","
-             << static_cast<int>(d.variant & 7) - 1 << "," << d.lmask << ","
-             << d.gmask << "," << d.dl << "," << d.dg;
-          for (int k = 0; k < 8; ++k) {
-            std::snprintf(num, sizeof(num), ",%.17g", d.m[k]);
+          const uint32_t v = d.hdr & kOpVariantMask;
+          const uint32_t type = v >> 10, a = (v >> 6) & 15;
+          os << "[" << type << "," << a << "," << static_cast<int>((v >> 3) & 7) - 1
+             << "," << static_cast<int>(v & 7) - 1 << "," << d.lmask << "," << d.gmask
+             << "," << d.dl << "," << d.dg << ",[";
+          size_t off = d.arg & 0xffff, len = 8;
+          if (type == D_STAB) {
+            const uint32_t nt = d.arg >> 16;
+            for (uint32_t t = 0; t < nt; ++t) {
+              uint64_t w0, w1;
+              std::memcpy(&w0, &pr.enc.pool[off + 2 * t], 8);
+              std::memcpy(&w1, &pr.enc.pool[off + 2 * t + 1], 8);
+              os << (t ? "," : "") << "[" << (w0 & 0xffffffffull) << "," << (w0 >> 32) << ","
+                 << w1 << "]";
+            }
+            os << "]]";
+            continue;
+          }
+          if (type == D_MULTI) len = 8 * __builtin_popcount(a);
+          else if (type == D_MULTIR) len = 4 * __builtin_popcount(a);
+          else if (type == D_DTAB) len = 2 * NS;
+          for (size_t k = 0; k < len; ++k) {
+            std::snprintf(num, sizeof(num), "%s%.17g", k ? "," : "", pr.enc.pool[off + k]);
             os << num;
           }
-          os << "]";
+          os << "]]";
         }
         os << "]}";
       }

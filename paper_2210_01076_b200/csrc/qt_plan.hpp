@@ -9,10 +9,12 @@
 namespace qtb {
 
 struct PlanOptions {
-  int tile_bits = 12;  // qubits per shared-memory tile
+  int tile_bits = kDefaultTileBits;  // qubits per shared-memory tile
   int low_bits = 4;    // lowest physical bits always in the tile (coalescing)
-  int reg_bits = kMaxRegBits;  // qubits per register round (2^reg amps/thread)
+  int reg_bits = kDefaultRegBits;    // qubits per register round (2^R amps/thread)
   int lookahead = 4096;// ops scanned per pass
+  bool fuse_layers = true;  // round compiler: MULTI / diagonal-table layers
+  int max_round_ops = 48;   // logical ops per register round (param space)
 };
 
 // Merges runs of uncontrolled single-qubit ops on the same qubit into one
@@ -28,8 +30,12 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
 
 // Device op for `op` (physical qubits) inside a pass whose tile holds the
 // physical bits tile_phys and whose round uses register tile-bits reg.
-DOp encode_op(const LOp& op, const std::vector<int>& tile_phys,
-              const std::vector<int>& reg);
+void encode_single(const LOp& op, const std::vector<int>& tile_phys,
+                   const std::vector<int>& reg, EncRound& out);
+
+// Device encoding of one round (fuse: build MULTI / table / sign layers;
+// otherwise one device op per logical op).
+EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse);
 
 // Kernel-side op type of an LOp.
 uint32_t dtype_of(const LOp& op);

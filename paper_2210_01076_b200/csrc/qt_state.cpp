@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "qt_gates.hpp"
@@ -58,9 +59,14 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_);
 
+  opt_.reg_bits = kDefaultRegBits;
+  opt_.tile_bits = kDefaultTileBits;
   if (cfg && cfg->tile_qubits > 0)
     opt_.tile_bits = std::min(cfg->tile_qubits, kMaxTileBits);
-  opt_.reg_bits = kMaxRegBits;
+  // tuning overrides (benchmark sweeps only)
+  if (const char* e = std::getenv("QTB_REG_BITS")) opt_.reg_bits = std::max(1, std::min(kMaxRegBits, std::atoi(e)));
+  if (const char* e = std::getenv("QTB_TILE_BITS")) opt_.tile_bits = std::max(2, std::min(kMaxTileBits, std::atoi(e)));
+  if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
 
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaMalloc(&psi_, sizeof(double2) << buf_bits_), "state allocation");
@@ -247,16 +253,23 @@ namespace {
 template <typename P>
 void fill_pass(P& kp, const PlanPass& ps) {
   kp.h.nrounds = static_cast<uint32_t>(ps.rounds.size());
-  uint32_t nops = 0;
+  uint32_t nops = 0, npool = 0;
   for (size_t r = 0; r < ps.rounds.size(); ++r) {
     const PlanRound& pr = ps.rounds[r];
     DRound& dr = kp.rounds[r];
     dr = DRound{};
     dr.op_first = static_cast<uint16_t>(nops);
-    dr.op_count = static_cast<uint16_t>(pr.ops.size());
+    dr.op_count = static_cast<uint16_t>(pr.enc.ops.size());
     for (size_t i = 0; i < pr.reg.size() && i < static_cast<size_t>(kMaxRegBits); ++i)
       dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
-    for (int idx : pr.ops) kp.ops[nops++] = encode_op(ps.ops[idx], ps.tile_phys, pr.reg);
+    for (DOp d : pr.enc.ops) {
+      // pool offsets are round-relative: rebase onto the launch's pool
+      const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
+      if (type == D_STAB) d.arg = ((d.arg & 0xffff) + npool) | (d.arg & 0xffff0000u);
+      else d.arg += npool;
+      kp.ops[nops++] = d;
+    }
+    for (double x : pr.enc.pool) kp.pool[npool++] = x;
   }
   kp.h.nops = nops;
 }
@@ -322,7 +335,13 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     h.outer_mask = buf_mask & ~tile_mask;
     h.ntiles = 1ull << (buf_bits_ - k);
     h.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
-    const bool large = ps.ops.size() > static_cast<size_t>(kSmallOps) ||
+    size_t nops = 0, npool = 0;
+    for (const PlanRound& pr : ps.rounds) {
+      nops += pr.enc.ops.size();
+      npool += pr.enc.pool.size();
+    }
+    const bool large = nops > static_cast<size_t>(kSmallOps) ||
+                       npool > static_cast<size_t>(kSmallPool) ||
                        ps.rounds.size() > static_cast<size_t>(kSmallRounds);
     const int occ = std::max(1, tile_pass_occupancy(k, R, large));
     const uint64_t cap = static_cast<uint64_t>(occ) * sms_;

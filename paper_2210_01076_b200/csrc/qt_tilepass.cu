@@ -12,16 +12,20 @@
 //   HBM --(16-B coalesced loads)--> smem tile of 2^k amplitudes
 //       --> R-qubit register rounds: each thread holds 2^R amplitudes (indices
 //           differing in the round's R tile bits) in registers and applies
-//           every op of the round
+//           the round's device ops
 //       --> smem --> HBM
 // so a pass costs 32 B of HBM traffic per amplitude however many gates it
-// carries. Ops live in the kernel-parameter constant bank and each op is
-// dispatched (one switch per op) to a fully specialised variant: target,
-// control and diagonal-target register slots are template parameters, so no
-// per-amplitude predication is executed; controls / diagonal bits outside the
-// register slots are thread- or tile-uniform predicates. Tensor cores do not
-// apply (2x2 complex FP64 operands): a pass is bounded by HBM when shallow
-// and by the FP64 pipe when deep ("Rooflines").
+// carries. Device ops live in the kernel-parameter constant bank (headers +
+// a pool of matrices / diagonal tables / sign terms). The host round
+// compiler (qt_plan.cpp) fuses each round into layers: one MULTI op applies
+// a 2x2 on every register slot (real rotations after the ZYZ split), one
+// DTAB op multiplies every amplitude by its merged diagonal factor, one STAB
+// op applies all sign flips (CZ, Z) with integer XORs. Each op is dispatched
+// (one switch per op) to a fully specialised variant: register slots are
+// template parameters, so no per-amplitude predication is executed; controls
+// / diagonal bits outside the register slots are thread- or tile-uniform
+// predicates. Tensor cores do not apply (2x2 complex FP64 operands): a pass
+// is bounded by HBM when shallow and by the FP64 pipe when deep.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,43 +37,84 @@ namespace qtb {
 
 namespace {
 
-// ---- op variants (R register bits, NS = 2^R slots per thread) -------------
-
-#define QT_LD_M                                            \
-  const double m0r = op.m[0], m0i = op.m[1], m1r = op.m[2], \
-               m1i = op.m[3], m2r = op.m[4], m2i = op.m[5], \
-               m3r = op.m[6], m3i = op.m[7]
+// ---- op variants (R register bits, 2^R slots per thread) -------------------
+//
+// Register discipline: every output of a pair is written by ONE final FMA
+// that reads its own input register last (partial sums of the other terms
+// are formed first), so ptxas can allocate each result into the input's
+// register and the dispatch switch needs no phi moves for the 2^R
+// loop-carried amplitudes.
 
 template <int R, int A, int CS>
-__device__ __forceinline__ void k_dense(double2 (&v)[1 << R], const DOp& op) {
-  QT_LD_M;
+__device__ __forceinline__ void pair_dense(double2 (&v)[1 << R], double m0r, double m0i,
+                                           double m1r, double m1i, double m2r, double m2i,
+                                           double m3r, double m3i) {
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
     if (s & (1 << A)) continue;
     if (CS >= 0 && !(s & (1 << CS))) continue;
     const int s1 = s | (1 << A);
-    const double2 a = v[s], b = v[s1];
-    v[s].x = m0r * a.x - m0i * a.y + m1r * b.x - m1i * b.y;
-    v[s].y = m0r * a.y + m0i * a.x + m1r * b.y + m1i * b.x;
-    v[s1].x = m2r * a.x - m2i * a.y + m3r * b.x - m3i * b.y;
-    v[s1].y = m2r * a.y + m2i * a.x + m3r * b.y + m3i * b.x;
+    // na = m00 a + m01 b, nb = m10 a + m11 b (complex)
+    const double p0 = fma(m1r, v[s1].x, fma(-m1i, v[s1].y, -m0i * v[s].y));
+    const double p1 = fma(m1r, v[s1].y, fma(m1i, v[s1].x, m0i * v[s].x));
+    const double p2 = fma(m2r, v[s].x, fma(-m2i, v[s].y, -m3i * v[s1].y));
+    const double p3 = fma(m2r, v[s].y, fma(m2i, v[s].x, m3i * v[s1].x));
+    v[s].x = fma(m0r, v[s].x, p0);
+    v[s].y = fma(m0r, v[s].y, p1);
+    v[s1].x = fma(m3r, v[s1].x, p2);
+    v[s1].y = fma(m3r, v[s1].y, p3);
   }
 }
 
 template <int R, int A, int CS>
-__device__ __forceinline__ void k_real(double2 (&v)[1 << R], const DOp& op) {
-  const double m0 = op.m[0], m1 = op.m[2], m2 = op.m[4], m3 = op.m[6];
+__device__ __forceinline__ void pair_real(double2 (&v)[1 << R], double m0, double m1,
+                                          double m2, double m3) {
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
     if (s & (1 << A)) continue;
     if (CS >= 0 && !(s & (1 << CS))) continue;
     const int s1 = s | (1 << A);
-    const double2 a = v[s], b = v[s1];
-    v[s].x = m0 * a.x + m1 * b.x;
-    v[s].y = m0 * a.y + m1 * b.y;
-    v[s1].x = m2 * a.x + m3 * b.x;
-    v[s1].y = m2 * a.y + m3 * b.y;
+    const double p0 = m1 * v[s1].x, p1 = m1 * v[s1].y;
+    const double p2 = m2 * v[s].x, p3 = m2 * v[s].y;
+    v[s].x = fma(m0, v[s].x, p0);
+    v[s].y = fma(m0, v[s].y, p1);
+    v[s1].x = fma(m3, v[s1].x, p2);
+    v[s1].y = fma(m3, v[s1].y, p3);
   }
+}
+
+template <int R, int A, int CS, typename P>
+__device__ __forceinline__ void k_dense(double2 (&v)[1 << R], const P& p, uint32_t o) {
+  pair_dense<R, A, CS>(v, p.pool[o], p.pool[o + 1], p.pool[o + 2], p.pool[o + 3],
+                       p.pool[o + 4], p.pool[o + 5], p.pool[o + 6], p.pool[o + 7]);
+}
+
+template <int R, int A, int CS, typename P>
+__device__ __forceinline__ void k_real(double2 (&v)[1 << R], const P& p, uint32_t o) {
+  pair_real<R, A, CS>(v, p.pool[o], p.pool[o + 2], p.pool[o + 4], p.pool[o + 6]);
+}
+
+// Register-identity-preserving swap: XOR swap on the bit patterns, so no
+// amplitude changes register (a plain swap makes ptxas insert a copy of all
+// 2^R loop-carried amplitudes at the op-loop head for every op).
+__device__ __forceinline__ void xswap(double& a, double& b) {
+  // opaque to NVVM / ptxas: a source-level XOR swap is folded back into a
+  // renaming, which is exactly what must not happen
+  long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  asm volatile(
+      "{\n\t"
+      "xor.b64 %0, %0, %1;\n\t"
+      "xor.b64 %1, %1, %0;\n\t"
+      "xor.b64 %0, %0, %1;\n\t"
+      "}"
+      : "+l"(x), "+l"(y));
+  a = __longlong_as_double(x);
+  b = __longlong_as_double(y);
+}
+
+__device__ __forceinline__ void xswap2(double2& a, double2& b) {
+  xswap(a.x, b.x);
+  xswap(a.y, b.y);
 }
 
 template <int R, int A, int CS>
@@ -78,57 +123,63 @@ __device__ __forceinline__ void k_xperm(double2 (&v)[1 << R]) {
   for (int s = 0; s < (1 << R); ++s) {
     if (s & (1 << A)) continue;
     if (CS >= 0 && !(s & (1 << CS))) continue;
-    const int s1 = s | (1 << A);
-    const double2 t = v[s];
-    v[s] = v[s1];
-    v[s1] = t;
+    xswap2(v[s], v[s | (1 << A)]);
   }
 }
 
-template <int R, int A, int CS>
-__device__ __forceinline__ void k_anti(double2 (&v)[1 << R], const DOp& op) {
-  const double m1r = op.m[2], m1i = op.m[3], m2r = op.m[4], m2i = op.m[5];
+// in-place complex scale: the final FMA of each part reads its own input
+__device__ __forceinline__ void cscale(double2& x, double br, double bi) {
+  const double p0 = -bi * x.y, p1 = bi * x.x;
+  x.x = fma(br, x.x, p0);
+  x.y = fma(br, x.y, p1);
+}
+
+template <int R, int A, int CS, typename P>
+__device__ __forceinline__ void k_anti(double2 (&v)[1 << R], const P& p, uint32_t o) {
+  const double m1r = p.pool[o + 2], m1i = p.pool[o + 3];
+  const double m2r = p.pool[o + 4], m2i = p.pool[o + 5];
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
     if (s & (1 << A)) continue;
     if (CS >= 0 && !(s & (1 << CS))) continue;
     const int s1 = s | (1 << A);
-    const double2 a = v[s], b = v[s1];
-    v[s] = cmulz(b, m1r, m1i);
-    v[s1] = cmulz(a, m2r, m2i);
+    xswap2(v[s], v[s1]);  // then scale in place: (m01 b, m10 a)
+    cscale(v[s], m1r, m1i);
+    cscale(v[s1], m2r, m2i);
   }
 }
 
 // diag(d0, d1) on a bit: DS >= 0 -> register slot bit DS (compile-time
 // choice per slot); DS < 0 -> the thread-uniform bit `bit`.
-template <int R, int CS, int DS>
-__device__ __forceinline__ void k_diag(double2 (&v)[1 << R], const DOp& op,
+template <int R, int CS, int DS, typename P>
+__device__ __forceinline__ void k_diag(double2 (&v)[1 << R], const P& p, uint32_t o,
                                        bool bit) {
-  const double d0r = op.m[0], d0i = op.m[1], d1r = op.m[6], d1i = op.m[7];
+  const double d0r = p.pool[o], d0i = p.pool[o + 1];
+  const double d1r = p.pool[o + 6], d1i = p.pool[o + 7];
   const double ur = bit ? d1r : d0r, ui = bit ? d1i : d0i;
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
     if (CS >= 0 && !(s & (1 << CS))) continue;
     if (DS >= 0) {
-      if (s & (1 << DS)) v[s] = cmulz(v[s], d1r, d1i);
-      else v[s] = cmulz(v[s], d0r, d0i);
+      if (s & (1 << DS)) cscale(v[s], d1r, d1i);
+      else cscale(v[s], d0r, d0i);
     } else {
-      v[s] = cmulz(v[s], ur, ui);
+      cscale(v[s], ur, ui);
     }
   }
 }
 
 // diag(1, d1): only amplitudes whose bit is set are touched
-template <int R, int CS, int DS>
-__device__ __forceinline__ void k_phase1(double2 (&v)[1 << R], const DOp& op,
+template <int R, int CS, int DS, typename P>
+__device__ __forceinline__ void k_phase1(double2 (&v)[1 << R], const P& p, uint32_t o,
                                          bool bit) {
-  const double d1r = op.m[6], d1i = op.m[7];
+  const double d1r = p.pool[o + 6], d1i = p.pool[o + 7];
   if (DS < 0 && !bit) return;
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
     if (CS >= 0 && !(s & (1 << CS))) continue;
     if (DS >= 0 && !(s & (1 << DS))) continue;
-    v[s] = cmulz(v[s], d1r, d1i);
+    cscale(v[s], d1r, d1i);
   }
 }
 
@@ -148,44 +199,105 @@ template <int R, int A, int B>
 __device__ __forceinline__ void k_swap2(double2 (&v)[1 << R]) {
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
-    if ((s & (1 << A)) && !(s & (1 << B))) {
-      const int s2 = s ^ (1 << A) ^ (1 << B);
-      const double2 t = v[s];
-      v[s] = v[s2];
-      v[s2] = t;
+    if ((s & (1 << A)) && !(s & (1 << B))) xswap2(v[s], v[s ^ (1 << A) ^ (1 << B)]);
+  }
+}
+
+// One 2x2 per register slot in MASK, ascending slots (they commute exactly,
+// so one fixed order); complex: 8 pool doubles per slot, real: 4.
+template <int R, int MASK, typename P>
+__device__ __forceinline__ void k_multi(double2 (&v)[1 << R], const P& p, uint32_t o) {
+#pragma unroll
+  for (int a = 0; a < R; ++a) {
+    if (!(MASK & (1 << a))) continue;
+    if (a == 0) k_dense<R, 0, -1>(v, p, o);
+    if (a == 1) k_dense<R, (R > 1 ? 1 : 0), -1>(v, p, o);
+    if (a == 2) k_dense<R, (R > 2 ? 2 : 0), -1>(v, p, o);
+    if (a == 3) k_dense<R, (R > 3 ? 3 : 0), -1>(v, p, o);
+    o += 8;
+  }
+}
+
+template <int R, int MASK, typename P>
+__device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, uint32_t o) {
+#pragma unroll
+  for (int a = 0; a < R; ++a) {
+    if (!(MASK & (1 << a))) continue;
+    const double m0 = p.pool[o], m1 = p.pool[o + 1], m2 = p.pool[o + 2], m3 = p.pool[o + 3];
+    if (a == 0) pair_real<R, 0, -1>(v, m0, m1, m2, m3);
+    if (a == 1) pair_real<R, (R > 1 ? 1 : 0), -1>(v, m0, m1, m2, m3);
+    if (a == 2) pair_real<R, (R > 2 ? 2 : 0), -1>(v, m0, m1, m2, m3);
+    if (a == 3) pair_real<R, (R > 3 ? 3 : 0), -1>(v, m0, m1, m2, m3);
+    o += 4;
+  }
+}
+
+// per-slot complex factor table (all merged diagonal gates of a layer)
+template <int R, typename P>
+__device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, uint32_t o) {
+#pragma unroll
+  for (int s = 0; s < (1 << R); ++s) cscale(v[s], p.pool[o + 2 * s], p.pool[o + 2 * s + 1]);
+}
+
+// sign terms: mask of negated slots from thread/tile conditions, then one
+// integer XOR per negated component
+template <int R, typename P>
+__device__ __forceinline__ void k_stab(double2 (&v)[1 << R], const P& p, uint32_t arg,
+                                       uint32_t jb, const uint64_t* sg) {
+  const uint32_t o = arg & 0xffffu, nt = arg >> 16;
+  uint32_t mask = 0;
+  for (uint32_t t = 0; t < nt; ++t) {
+    const uint64_t w0 = static_cast<uint64_t>(__double_as_longlong(p.pool[o + 2 * t]));
+    const uint64_t gc = static_cast<uint64_t>(__double_as_longlong(p.pool[o + 2 * t + 1]));
+    const uint32_t lc = static_cast<uint32_t>(w0 >> 32);
+    bool on = (jb & lc) == lc;
+    if (gc) on = on && (*sg & gc) == gc;
+    if (on) mask ^= static_cast<uint32_t>(w0);
+  }
+  if (!mask) return;
+#pragma unroll
+  for (int s = 0; s < (1 << R); ++s) {
+    const uint32_t sb = ((mask >> s) & 1u) << 31;
+    v[s] = make_double2(__hiloint2double(__double2hiint(v[s].x) ^ sb, __double2loint(v[s].x)),
+                        __hiloint2double(__double2hiint(v[s].y) ^ sb, __double2loint(v[s].y)));
+  }
+}
+
+// Applies one device op. `jb` = the thread's tile-local index with the
+// register bits cleared; `sg` = the tile's global base index (smem).
+// Controls / diagonal bits outside the register slots are only evaluated for
+// ops whose header flags say they have them.
+template <int R, typename P>
+__device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const DOp& d,
+                                         uint32_t jb, const uint64_t* sg) {
+  const uint32_t hdr = d.hdr;
+  bool bit = false;
+  if (hdr & kOpFlagMask) {
+    if ((hdr & kOpLctl) && (jb & d.lmask) != d.lmask) return;
+    if (hdr & kOpDl) bit = (jb & d.dl) != 0;
+    if (hdr & (kOpGctl | kOpDg)) {
+      const uint64_t g = *sg;
+      if ((g & d.gmask) != d.gmask) return;
+      bit = bit || (g & d.dg) != 0;
     }
   }
-}
-
-// Applies one op. `jb` = the thread's tile-local index with the register
-// bits cleared, `g` = the tile's global base index.
-template <int R>
-__device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const DOp& op,
-                                         uint32_t jb, const uint64_t* sg) {
-  // thread-uniform control predicate (controls outside the register slots);
-  // the tile's global base is read from smem only by ops that need it
-  if ((jb & op.lmask) != op.lmask) return;
-  bool bit = (jb & op.dl) != 0;
-  if ((op.gmask | op.dg) != 0) {
-    const uint64_t g = *sg;
-    if ((g & op.gmask) != op.gmask) return;
-    bit = bit || (g & op.dg) != 0;
-  }
   (void)bit;
-  switch (op.variant) {
+  const uint32_t arg = d.arg;
+  const uint32_t idx = (hdr >> kOpIndexShift) & 0xffu;
 #include "qt_variants.inc"
-    default:
-      break;
-  }
 }
 
-// R = 4 (the default): 16 amplitudes per thread in registers, 256 threads
-// per 2^12-amplitude tile, <= 128 registers so two CTAs (64 KiB smem each)
-// stay resident per SM -- one streams its tile while the other computes.
+// R = 3: 8 amplitudes per thread in registers, 256 threads per 2^11 tile;
+// R = 4: 16 amplitudes per thread, 256 threads per 2^12 tile (<= 128 regs,
+// 2 CTAs per SM). The kernel is latency-bound at low occupancy, so the R = 3
+// minimum-blocks bound trades registers for resident warps.
+#ifndef QT_R3_MINB
+#define QT_R3_MINB 4
+#endif
 template <int R>
-constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? 2 : 4);
+constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? QT_R3_MINB : 4);
 template <int R>
-constexpr int kMaxThreads = R >= 4 ? 256 : 512;
+constexpr int kMaxThreads = R >= 3 ? 256 : 512;
 
 template <int R, typename P>
 __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
@@ -210,11 +322,12 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
       mk &= mk - 1;
     }
   }
-#define QT_SLOT_OFF(s)                                   \
-  ([&] {                                                 \
-    uint64_t o_ = 0;                                     \
-    _Pragma("unroll") for (int i_ = 0; i_ < R; ++i_) if ((s) & (1 << i_)) o_ |= 1ull << hpos[i_]; \
-    return o_;                                           \
+#define QT_SLOT_OFF(s)                                                                \
+  ([&] {                                                                              \
+    uint64_t o_ = 0;                                                                  \
+    _Pragma("unroll") for (int i_ = 0; i_ < R; ++i_) if ((s) & (1 << i_)) o_ |= 1ull \
+        << hpos[i_];                                                                  \
+    return o_;                                                                        \
   }())
 
   // per-tile uniform values live in smem while the register rounds run
@@ -278,7 +391,7 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
         v[s] = sm[a];
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
-      for (uint32_t o = rd.op_first; o < o1; ++o) apply_op<R>(v, p.ops[o], jb, &s_tile[1]);
+      for (uint32_t o = rd.op_first; o < o1; ++o) apply_op<R>(v, p, p.ops[o], jb, &s_tile[1]);
       // opaque copy: forces the 2^R store addresses to be regenerated here
       // instead of being kept live (2^R registers) across the op loop
       uint32_t sjb2 = sjb;

@@ -11,7 +11,8 @@ import json
 
 import numpy as np
 
-D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1 = range(8)
+(D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1,
+ D_MULTI, D_MULTIR, D_DTAB, D_STAB) = range(12)
 
 
 def _bit(idx, pos):
@@ -34,13 +35,54 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
         tile = ps["tile"]
         for rd in ps["round_detail"]:
             reg = rd["reg"]
+            # slot index of every amplitude in this round
+            slot = np.zeros(len(psi), dtype=np.int64)
+            for i, tb in enumerate(reg):
+                slot |= (_bit(idx, tile[tb]).astype(np.int64) << i)
             for op in rd["ops"]:
-                # [type, a, cs, ds, lmask, gmask, dl, dg, m0..m7]: a = target
-                # register slot, cs / ds = control / diagonal-target slot (-1:
-                # not a register bit; SWAP2 keeps its second slot in ds)
+                # [type, a, cs, ds, lmask, gmask, dl, dg, [data]]: a = target
+                # register slot (MULTI: slot mask), cs / ds = control /
+                # diagonal-target slot (-1: not a register bit; SWAP2 keeps
+                # its second slot in ds); data = the op's pool slice
                 typ, a, cs, ds, lmask, gmask, dl, dg = (int(x) for x in op[:8])
+                data = op[8]
                 b = ds
-                m = np.array(op[8:16], dtype=np.float64)
+                if typ in (D_MULTI, D_MULTIR):
+                    k = 0
+                    for sl in range(len(reg)):
+                        if not (a >> sl) & 1:
+                            continue
+                        if typ == D_MULTI:
+                            mm = np.array(data[8 * k:8 * k + 8])
+                            mm = mm[0::2] + 1j * mm[1::2]
+                        else:
+                            mm = np.array(data[4 * k:4 * k + 4], dtype=np.complex128)
+                        t = tile[reg[sl]]
+                        lo = idx[_bit(idx, t) == 0]
+                        hi = lo | np.uint64(1 << t)
+                        x, y = psi[lo].copy(), psi[hi].copy()
+                        psi[lo] = mm[0] * x + mm[1] * y
+                        psi[hi] = mm[2] * x + mm[3] * y
+                        k += 1
+                    continue
+                if typ == D_DTAB:
+                    tab = np.array(data[0::2]) + 1j * np.array(data[1::2])
+                    psi = psi * tab[slot]
+                    continue
+                if typ == D_STAB:
+                    neg = np.zeros(len(psi), dtype=bool)
+                    for slots, lcond, gcond in data:
+                        on = np.ones(len(psi), dtype=bool)
+                        for tb in range(len(tile)):
+                            if (lcond >> tb) & 1:
+                                on &= _bit(idx, tile[tb]) == 1
+                        for pb in range(64):
+                            if (gcond >> pb) & 1:
+                                on &= _bit(idx, pb) == 1
+                        neg ^= on & (((slots >> slot) & 1) == 1)
+                    psi = np.where(neg, -psi, psi)
+                    continue
+                m = np.array(data[0:8], dtype=np.float64)
                 m = m[0::2] + 1j * m[1::2]
                 # control predicate over physical bits
                 ok = np.ones(len(psi), dtype=bool)
@@ -49,9 +91,9 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
                 for tb in range(len(tile)):
                     if (lmask >> tb) & 1:
                         ok &= _bit(idx, tile[tb]) == 1
-                for p in range(64):
-                    if (gmask >> p) & 1:
-                        ok &= _bit(idx, p) == 1
+                for pb in range(64):
+                    if (gmask >> pb) & 1:
+                        ok &= _bit(idx, pb) == 1
                 if typ in (D_DENSE, D_REAL, D_XPERM, D_ANTI):
                     t = tile[reg[a]]
                     lo = idx[(_bit(idx, t) == 0) & ok]

@@ -1,7 +1,5 @@
 set -x
+export QTB_REG_BITS=${QTB_REG_BITS:-4} QTB_TILE_BITS=${QTB_TILE_BITS:-11}
 python tools/prof_pass.py --reps 2 > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:tile_pass -s 22 -c 2 -o gpurun_out/prof_c3 -f python tools/prof_pass.py --reps 2 > gpurun_out/ncu_c3.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:tile_pass -s 31 -c 1 -o gpurun_out/prof_c3_v6 -f python tools/prof_pass.py --reps 2 > gpurun_out/ncu_c3.log 2>&1
 echo ncu rc=$?
-tail -5 gpurun_out/ncu_c3.log
-cat gpurun_out/prof_plain.log
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15
