@@ -19,12 +19,18 @@ def _bit(idx, pos):
     return (idx >> np.uint64(pos)) & np.uint64(1)
 
 
-def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
+def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) -> np.ndarray:
+    """Replays the plan on `state`. For one shard of a sharded state, `base`
+    is the shard's global index offset (rank << nlocal: predicates see global
+    indices) and `exchange(psi, pairs)` performs the exchange passes."""
     plan = json.loads(plan_json) if isinstance(plan_json, str) else plan_json
     psi = state.copy()
-    n = int(len(psi)).bit_length() - 1
-    idx = np.arange(1 << n, dtype=np.uint64)
+    nl = int(len(psi)).bit_length() - 1
+    idx = np.uint64(base) + np.arange(1 << nl, dtype=np.uint64)  # global indices
     for ps in plan["passes"]:
+        if ps["kind"] == "exchange" and exchange is not None:
+            psi = exchange(psi, ps["swap"])
+            continue
         if ps["kind"] == "exchange":
             for g, v in ps["swap"]:
                 sel = (_bit(idx, g) == 1) & (_bit(idx, v) == 0)
@@ -58,8 +64,8 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
                         else:
                             mm = np.array(data[4 * k:4 * k + 4], dtype=np.complex128)
                         t = tile[reg[sl]]
-                        lo = idx[_bit(idx, t) == 0]
-                        hi = lo | np.uint64(1 << t)
+                        lo = np.nonzero(_bit(idx, t) == 0)[0]
+                        hi = lo | (1 << t)
                         x, y = psi[lo].copy(), psi[hi].copy()
                         psi[lo] = mm[0] * x + mm[1] * y
                         psi[hi] = mm[2] * x + mm[3] * y
@@ -96,8 +102,8 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
                         ok &= _bit(idx, pb) == 1
                 if typ in (D_DENSE, D_REAL, D_XPERM, D_ANTI):
                     t = tile[reg[a]]
-                    lo = idx[(_bit(idx, t) == 0) & ok]
-                    hi = lo | np.uint64(1 << t)
+                    lo = np.nonzero((_bit(idx, t) == 0) & ok)[0]
+                    hi = lo | (1 << t)
                     x, y = psi[lo].copy(), psi[hi].copy()
                     if typ in (D_DENSE, D_REAL):
                         if typ == D_REAL:
@@ -127,8 +133,8 @@ def apply_plan(state: np.ndarray, plan_json: str) -> np.ndarray:
                 elif typ == D_SWAP2:
                     ta, tb2 = tile[reg[a]], tile[reg[b]]
                     sel = (_bit(idx, ta) == 1) & (_bit(idx, tb2) == 0)
-                    p0 = idx[sel]
-                    p1 = p0 ^ np.uint64((1 << ta) | (1 << tb2))
+                    p0 = np.nonzero(sel)[0]
+                    p1 = p0 ^ ((1 << ta) | (1 << tb2))
                     psi[p0], psi[p1] = psi[p1].copy(), psi[p0].copy()
                 else:
                     raise ValueError(f"unknown op type {typ}")
