@@ -293,3 +293,17 @@ def test_config5_shape_incremental(gpu):
             got = sim.amplitudes(0, (1 << 14) - 1)
             assert np.abs(got - want).max() <= 1e-10
             assert abs(sim.norm_squared() - 1) <= 1e-12
+
+
+def test_cpp_dropin_program(gpu):
+    """C++ callers compile unchanged against include/qtask/engine.hpp: the
+    restated reference engine tests and acceptance criteria 1, 2, 6, 7."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", os.path.join(root, "tests", "cpp"), "-s"], check=True)
+    out = subprocess.run([os.path.join(root, "tests", "cpp", "test_dropin")],
+                         capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "[FAIL]" not in out.stdout
