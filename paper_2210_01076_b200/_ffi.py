@@ -15,6 +15,8 @@ from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libqtask_b200.so")
+if os.environ.get("QTB_LIB"):  # tuning builds only (tools/); product = in-tree .so
+    LIB_PATH = os.path.join(HERE, os.environ["QTB_LIB"])
 
 # qt_gate (40 bytes): int32 kind, target, control, reserved; f64 theta, phi, lambda
 GATE_DTYPE = np.dtype(

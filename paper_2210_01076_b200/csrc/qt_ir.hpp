@@ -110,10 +110,11 @@ struct SignTerm {
 constexpr int kMaxTileBits = 13;  // 2^13 x 16 B = 128 KiB of smem
 constexpr int kMaxRegBits = 4;
 // Defaults (overridable per state; QTB_TILE_BITS / QTB_REG_BITS for sweeps):
-// 2^11-amplitude tiles (32 KiB smem), 4 register bits -> 128 threads of 16
-// amplitudes, <= 128 registers (measured best on C3, B200).
-constexpr int kDefaultTileBits = 11;
-constexpr int kDefaultRegBits = 4;
+// 2^10-amplitude tiles (16 KiB smem), 3 register bits -> 128 threads of 8
+// amplitudes, <= 64 registers, 8 CTAs (32 warps) per SM -- measured best on
+// C3 on B200 (the pass is latency-bound, so resident warps win over R = 4).
+constexpr int kDefaultTileBits = 10;
+constexpr int kDefaultRegBits = 3;
 
 struct DRound {
   uint16_t op_first;  // into the pass's op array

@@ -267,13 +267,24 @@ void emit_table(const std::vector<cplx>& t, EncRound& out) {
   out.ops.push_back(d);
 }
 
+// Sign terms: unconditional ones (slot patterns only) collapse into one base
+// mask carried in the op itself (dl field); only thread/tile-conditional
+// terms go to the pool.
 void emit_signs(const std::vector<SignTerm>& terms, EncRound& out) {
   if (terms.empty()) return;
+  uint32_t base = 0;
+  std::vector<SignTerm> cond;
+  for (const SignTerm& t : terms) {
+    if (t.lcond == 0 && t.gcond == 0) base ^= t.slots;
+    else cond.push_back(t);
+  }
+  if (base == 0 && cond.empty()) return;
   DOp d{};
   d.hdr = vid(D_STAB, 0, -1, -1);
+  d.dl = base;
   const uint32_t off = static_cast<uint32_t>(out.pool.size());
-  d.arg = off | (static_cast<uint32_t>(terms.size()) << 16);
-  for (const SignTerm& t : terms) {
+  d.arg = off | (static_cast<uint32_t>(cond.size()) << 16);
+  for (const SignTerm& t : cond) {
     const uint64_t w0 = static_cast<uint64_t>(t.slots) | (static_cast<uint64_t>(t.lcond) << 32);
     double dw0, dw1;
     std::memcpy(&dw0, &w0, 8);
@@ -282,6 +293,22 @@ void emit_signs(const std::vector<SignTerm>& terms, EncRound& out) {
     out.pool.push_back(dw1);
   }
   out.ops.push_back(d);
+}
+
+// A table that is emitted anyway absorbs the unconditional sign terms
+// (multiplying entries by -1 is free); conditional terms stay sign ops.
+void fold_signs(std::vector<cplx>& table, std::vector<SignTerm>& terms) {
+  if (table_trivial(table)) return;
+  std::vector<SignTerm> rest;
+  for (const SignTerm& t : terms) {
+    if (t.lcond == 0 && t.gcond == 0) {
+      for (size_t s = 0; s < table.size(); ++s)
+        if ((t.slots >> s) & 1u) table[s] = cplx{-table[s].re, -table[s].im};
+    } else {
+      rest.push_back(t);
+    }
+  }
+  terms.swap(rest);
 }
 
 void emit_multi(LayerState& L, EncRound& out) {
@@ -305,6 +332,7 @@ void emit_multi(LayerState& L, EncRound& out) {
 // Emits the pre part and the layer's MULTI; the post part becomes the next
 // layer's pre part.
 void close_layer(LayerState& L, EncRound& out) {
+  fold_signs(L.pre, L.pre_signs);
   emit_table(L.pre, out);
   emit_signs(L.pre_signs, out);
   emit_multi(L, out);
@@ -317,6 +345,7 @@ void close_layer(LayerState& L, EncRound& out) {
 
 void flush_all(LayerState& L, EncRound& out) {
   close_layer(L, out);
+  fold_signs(L.pre, L.pre_signs);
   emit_table(L.pre, out);
   emit_signs(L.pre_signs, out);
   for (auto& c : L.pre) c = cplx{1.0, 0.0};
@@ -759,11 +788,12 @@ std::string plan_to_json(const Plan& p, bool detail) {
           size_t off = d.arg & 0xffff, len = 8;
           if (type == D_STAB) {
             const uint32_t nt = d.arg >> 16;
+            os << "[" << d.dl << ",0,0]";  // base mask: unconditional terms
             for (uint32_t t = 0; t < nt; ++t) {
               uint64_t w0, w1;
               std::memcpy(&w0, &pr.enc.pool[off + 2 * t], 8);
               std::memcpy(&w1, &pr.enc.pool[off + 2 * t + 1], 8);
-              os << (t ? "," : "") << "[" << (w0 & 0xffffffffull) << "," << (w0 >> 32) << ","
+              os << ",[" << (w0 & 0xffffffffull) << "," << (w0 >> 32) << ","
                  << w1 << "]";
             }
             os << "]]";

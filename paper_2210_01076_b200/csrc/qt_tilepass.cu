@@ -84,13 +84,13 @@ __device__ __forceinline__ void pair_real(double2 (&v)[1 << R], double m0, doubl
 }
 
 template <int R, int A, int CS, typename P>
-__device__ __forceinline__ void k_dense(double2 (&v)[1 << R], const P& p, uint32_t o) {
+__device__ __forceinline__ void k_dense(double2 (&v)[1 << R], const P& p, int o) {
   pair_dense<R, A, CS>(v, p.pool[o], p.pool[o + 1], p.pool[o + 2], p.pool[o + 3],
                        p.pool[o + 4], p.pool[o + 5], p.pool[o + 6], p.pool[o + 7]);
 }
 
 template <int R, int A, int CS, typename P>
-__device__ __forceinline__ void k_real(double2 (&v)[1 << R], const P& p, uint32_t o) {
+__device__ __forceinline__ void k_real(double2 (&v)[1 << R], const P& p, int o) {
   pair_real<R, A, CS>(v, p.pool[o], p.pool[o + 2], p.pool[o + 4], p.pool[o + 6]);
 }
 
@@ -135,7 +135,7 @@ __device__ __forceinline__ void cscale(double2& x, double br, double bi) {
 }
 
 template <int R, int A, int CS, typename P>
-__device__ __forceinline__ void k_anti(double2 (&v)[1 << R], const P& p, uint32_t o) {
+__device__ __forceinline__ void k_anti(double2 (&v)[1 << R], const P& p, int o) {
   const double m1r = p.pool[o + 2], m1i = p.pool[o + 3];
   const double m2r = p.pool[o + 4], m2i = p.pool[o + 5];
 #pragma unroll
@@ -152,7 +152,7 @@ __device__ __forceinline__ void k_anti(double2 (&v)[1 << R], const P& p, uint32_
 // diag(d0, d1) on a bit: DS >= 0 -> register slot bit DS (compile-time
 // choice per slot); DS < 0 -> the thread-uniform bit `bit`.
 template <int R, int CS, int DS, typename P>
-__device__ __forceinline__ void k_diag(double2 (&v)[1 << R], const P& p, uint32_t o,
+__device__ __forceinline__ void k_diag(double2 (&v)[1 << R], const P& p, int o,
                                        bool bit) {
   const double d0r = p.pool[o], d0i = p.pool[o + 1];
   const double d1r = p.pool[o + 6], d1i = p.pool[o + 7];
@@ -171,7 +171,7 @@ __device__ __forceinline__ void k_diag(double2 (&v)[1 << R], const P& p, uint32_
 
 // diag(1, d1): only amplitudes whose bit is set are touched
 template <int R, int CS, int DS, typename P>
-__device__ __forceinline__ void k_phase1(double2 (&v)[1 << R], const P& p, uint32_t o,
+__device__ __forceinline__ void k_phase1(double2 (&v)[1 << R], const P& p, int o,
                                          bool bit) {
   const double d1r = p.pool[o + 6], d1i = p.pool[o + 7];
   if (DS < 0 && !bit) return;
@@ -206,7 +206,7 @@ __device__ __forceinline__ void k_swap2(double2 (&v)[1 << R]) {
 // One 2x2 per register slot in MASK, ascending slots (they commute exactly,
 // so one fixed order); complex: 8 pool doubles per slot, real: 4.
 template <int R, int MASK, typename P>
-__device__ __forceinline__ void k_multi(double2 (&v)[1 << R], const P& p, uint32_t o) {
+__device__ __forceinline__ void k_multi(double2 (&v)[1 << R], const P& p, int o) {
 #pragma unroll
   for (int a = 0; a < R; ++a) {
     if (!(MASK & (1 << a))) continue;
@@ -219,7 +219,7 @@ __device__ __forceinline__ void k_multi(double2 (&v)[1 << R], const P& p, uint32
 }
 
 template <int R, int MASK, typename P>
-__device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, uint32_t o) {
+__device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, int o) {
 #pragma unroll
   for (int a = 0; a < R; ++a) {
     if (!(MASK & (1 << a))) continue;
@@ -234,7 +234,7 @@ __device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, uint3
 
 // per-slot complex factor table (all merged diagonal gates of a layer)
 template <int R, typename P>
-__device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, uint32_t o) {
+__device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, int o) {
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) cscale(v[s], p.pool[o + 2 * s], p.pool[o + 2 * s + 1]);
 }
@@ -243,10 +243,11 @@ __device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, uint32_
 // integer XOR per negated component
 template <int R, typename P>
 __device__ __forceinline__ void k_stab(double2 (&v)[1 << R], const P& p, uint32_t arg,
-                                       uint32_t jb, const uint64_t* sg) {
-  const uint32_t o = arg & 0xffffu, nt = arg >> 16;
-  uint32_t mask = 0;
-  for (uint32_t t = 0; t < nt; ++t) {
+                                       uint32_t base, uint32_t jb, const uint64_t* sg) {
+  const int o = static_cast<int>(arg & 0xffffu);
+  const uint32_t nt = arg >> 16;
+  uint32_t mask = base;  // unconditional terms, folded on the host
+  for (int t = 0; t < static_cast<int>(nt); ++t) {
     const uint64_t w0 = static_cast<uint64_t>(__double_as_longlong(p.pool[o + 2 * t]));
     const uint64_t gc = static_cast<uint64_t>(__double_as_longlong(p.pool[o + 2 * t + 1]));
     const uint32_t lc = static_cast<uint32_t>(w0 >> 32);

@@ -77,7 +77,7 @@ def test_every_op_scheduled_once_and_tiles_bounded():
         assert ps["kind"] == "tile"
         assert len(ps["tile"]) == 10 and ps["tile"][:4] == [0, 1, 2, 3]
         for rd in ps["round_detail"]:
-            assert len(rd["reg"]) == 4  # kDefaultRegBits
+            assert len(rd["reg"]) == 3  # kDefaultRegBits
         seen.extend(ps["gates"])
     # every op lands in exactly one pass (an op is listed under the first
     # gate of its fused run: odd layers leave q0 / q19 without a CZ, so their

@@ -1,5 +1,4 @@
-set -x
-export QTB_REG_BITS=${QTB_REG_BITS:-4} QTB_TILE_BITS=${QTB_TILE_BITS:-11}
-python tools/prof_pass.py --reps 2 > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:tile_pass -s 31 -c 1 -o gpurun_out/prof_c3_v6 -f python tools/prof_pass.py --reps 2 > gpurun_out/ncu_c3.log 2>&1
+export QTB_REG_BITS=3 QTB_TILE_BITS=10
+python tools/microbench.py > gpurun_out/mb_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:tile_pass -s 2 -c 1 -o gpurun_out/prof_mb -f python tools/microbench.py > gpurun_out/ncu_mb.log 2>&1
 echo ncu rc=$?
