@@ -66,6 +66,8 @@ enum DType : uint32_t {
   D_MULTIR = 9,  // real 2x2 (4 doubles) on every reg slot in mask a
   D_DTAB = 10,   // per-slot complex factor table (2^R entries)
   D_STAB = 11,   // sign terms: slot masks negated under thread/tile conditions
+  D_LAYER = 12,  // one dispatch for a whole real layer: [diag table if kOpTable]
+                 // [sign base mask dl] [real 2x2 on every reg slot in mask a]
 };
 
 // Variant id of a device op: the kernel dispatches on it to a fully
@@ -86,6 +88,7 @@ constexpr uint32_t kOpDg = 1u << 19;    // dg != 0
 constexpr uint32_t kOpFlagMask = kOpLctl | kOpGctl | kOpDl | kOpDg;
 // dense dispatch index of the variant (tools/gen_variants.py) in bits 20..27
 constexpr uint32_t kOpIndexShift = 20;
+constexpr uint32_t kOpTable = 1u << 28;  // D_LAYER: a 2^R-entry table leads the pool data
 
 // 32 bytes; lives in the kernel-parameter constant bank (read uniformly).
 // Matrices / tables / sign terms are in the pass's double pool at `arg`.

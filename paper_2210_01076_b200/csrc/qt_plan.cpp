@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <sstream>
@@ -231,7 +232,15 @@ void encode_single(const LOp& op, const std::vector<int>& tile_phys,
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr double kZyzMin = 0.05;  // min(|u00|, |u10|) for the factorisation
+// min(|u00|, |u10|) for the factorisation (QTB_ZYZ overrides, for sweeps;
+// > 1 disables it)
+double zyz_min() {
+  static const double v = [] {
+    const char* e = std::getenv("QTB_ZYZ");
+    return e ? std::atof(e) : 0.05;
+  }();
+  return v;
+}
 
 struct LayerState {
   int R, NS;
@@ -333,9 +342,42 @@ void emit_multi(LayerState& L, EncRound& out) {
 // layer's pre part.
 void close_layer(LayerState& L, EncRound& out) {
   fold_signs(L.pre, L.pre_signs);
-  emit_table(L.pre, out);
-  emit_signs(L.pre_signs, out);
-  emit_multi(L, out);
+  // D_LAYER (one dispatch per real layer) measured slower than separate
+  // DTAB / STAB / MULTIR ops on B200 (C3: 630 vs 526 ms); kept behind
+  // QTB_LAYER=1 for further tuning
+  static const bool use_layer = std::getenv("QTB_LAYER") != nullptr;
+  if (use_layer && L.mmask && L.mreal) {
+    // one D_LAYER dispatch: conditional sign terms first (they commute with
+    // the table and the unconditional signs), then table + signs + rotations
+    uint32_t base = 0;
+    std::vector<SignTerm> cond;
+    for (const SignTerm& t : L.pre_signs) {
+      if (t.lcond == 0 && t.gcond == 0) base ^= t.slots;
+      else cond.push_back(t);
+    }
+    emit_signs(cond, out);
+    DOp d{};
+    const bool tab = !table_trivial(L.pre);
+    d.hdr = vid(D_LAYER, static_cast<int>(L.mmask), -1, -1) | (tab ? kOpTable : 0u);
+    d.dl = base;
+    d.arg = static_cast<uint32_t>(out.pool.size());
+    if (tab) {
+      for (const cplx& c : L.pre) {
+        out.pool.push_back(c.re);
+        out.pool.push_back(c.im);
+      }
+    }
+    for (int i = 0; i < L.R; ++i)
+      if (L.mmask & (1u << i))
+        for (int k = 0; k < 4; ++k) out.pool.push_back(L.M[i][k].re);
+    out.ops.push_back(d);
+    L.mmask = 0;
+    L.mreal = true;
+  } else {
+    emit_table(L.pre, out);
+    emit_signs(L.pre_signs, out);
+    emit_multi(L, out);
+  }
   L.pre.swap(L.post);
   L.pre_signs.swap(L.post_signs);
   for (auto& c : L.post) c = cplx{1.0, 0.0};
@@ -426,7 +468,7 @@ EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse) 
       if (!real) {
         const double c = std::hypot(op.m[0].re, op.m[0].im);
         const double sn = std::hypot(op.m[2].re, op.m[2].im);
-        if (c > kZyzMin && sn > kZyzMin) {
+        if (c > zyz_min() && sn > zyz_min()) {
           // U = diag(p0, p1) . [[c, -s], [s, c]] . diag(1, q1)
           p0 = cplx{op.m[0].re / c, op.m[0].im / c};
           p1 = cplx{op.m[2].re / sn, op.m[2].im / sn};
@@ -746,6 +788,9 @@ std::string plan_to_json(const Plan& p, bool detail) {
           case D_DIAG: case D_PHASE1: case D_DTAB: fp += 4.0; break;
           case D_MULTI: fp += 8.0 * __builtin_popcount(a); break;
           case D_MULTIR: fp += 4.0 * __builtin_popcount(a); break;
+          case D_LAYER:
+            fp += 4.0 * __builtin_popcount(a) + ((d.hdr & kOpTable) ? 4.0 : 0.0);
+            break;
           default: break;
         }
       }
@@ -799,14 +844,16 @@ std::string plan_to_json(const Plan& p, bool detail) {
             os << "]]";
             continue;
           }
+          const bool tab = (d.hdr & kOpTable) != 0;
           if (type == D_MULTI) len = 8 * __builtin_popcount(a);
           else if (type == D_MULTIR) len = 4 * __builtin_popcount(a);
           else if (type == D_DTAB) len = 2 * NS;
+          else if (type == D_LAYER) len = (tab ? 2 * NS : 0) + 4 * __builtin_popcount(a);
           for (size_t k = 0; k < len; ++k) {
             std::snprintf(num, sizeof(num), "%s%.17g", k ? "," : "", pr.enc.pool[off + k]);
             os << num;
           }
-          os << "]]";
+          os << "]," << (tab ? 1 : 0) << "]";
         }
         os << "]}";
       }

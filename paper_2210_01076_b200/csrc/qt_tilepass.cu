@@ -232,6 +232,32 @@ __device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, int o
   }
 }
 
+// A whole real layer in one dispatch: optional per-slot diagonal table,
+// unconditional sign mask, then one real rotation per register slot in MASK.
+template <int R, int MASK, typename P>
+__device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, int o,
+                                        uint32_t signs, bool table) {
+  if (table) {
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+      const double tr = p.pool[o + 2 * s], ti = p.pool[o + 2 * s + 1];
+      const double q0 = -ti * v[s].y, q1 = ti * v[s].x;
+      v[s].x = fma(tr, v[s].x, q0);
+      v[s].y = fma(tr, v[s].y, q1);
+    }
+    o += 2 << R;
+  }
+  if (signs) {
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+      const uint32_t sb = ((signs >> s) & 1u) << 31;
+      v[s] = make_double2(__hiloint2double(__double2hiint(v[s].x) ^ sb, __double2loint(v[s].x)),
+                          __hiloint2double(__double2hiint(v[s].y) ^ sb, __double2loint(v[s].y)));
+    }
+  }
+  k_multir<R, MASK>(v, p, o);
+}
+
 // per-slot complex factor table (all merged diagonal gates of a layer)
 template <int R, typename P>
 __device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, int o) {

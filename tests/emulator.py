@@ -12,7 +12,7 @@ import json
 import numpy as np
 
 (D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1,
- D_MULTI, D_MULTIR, D_DTAB, D_STAB) = range(12)
+ D_MULTI, D_MULTIR, D_DTAB, D_STAB, D_LAYER) = range(13)
 
 
 def _bit(idx, pos):
@@ -74,6 +74,29 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                 if typ == D_DTAB:
                     tab = np.array(data[0::2]) + 1j * np.array(data[1::2])
                     psi = psi * tab[slot]
+                    continue
+                if typ == D_LAYER:
+                    has_tab = int(op[9])
+                    k0 = 0
+                    if has_tab:
+                        ns = 1 << len(reg)
+                        tab = np.array(data[0:2 * ns:2]) + 1j * np.array(data[1:2 * ns:2])
+                        psi = psi * tab[slot]
+                        k0 = 2 * ns
+                    if dl:  # unconditional sign mask
+                        psi = np.where(((dl >> slot) & 1) == 1, -psi, psi)
+                    k = 0
+                    for sl in range(len(reg)):
+                        if not (a >> sl) & 1:
+                            continue
+                        mm = np.array(data[k0 + 4 * k:k0 + 4 * k + 4], dtype=np.complex128)
+                        t = tile[reg[sl]]
+                        lo = np.nonzero(_bit(idx, t) == 0)[0]
+                        hi = lo | (1 << t)
+                        x, y = psi[lo].copy(), psi[hi].copy()
+                        psi[lo] = mm[0] * x + mm[1] * y
+                        psi[hi] = mm[2] * x + mm[3] * y
+                        k += 1
                     continue
                 if typ == D_STAB:
                     neg = np.zeros(len(psi), dtype=bool)
