@@ -163,6 +163,69 @@ def run_reference(args):
     return 0
 
 
+def latency_stats(xs):
+    if not xs:
+        return None
+    s = sorted(xs)
+    return {"mean_ms": statistics.mean(s), "median_ms": statistics.median(s),
+            "p90_ms": s[min(len(s) - 1, int(0.9 * len(s)))], "count": len(s)}
+
+
+def measure_incremental(make_sim, w, nmods, reference=False, tail_split=True):
+    """Per-modifier latency through the Simulator API: host
+    wall time from the start of the modifier calls to the return of
+    update_state (device synchronised, numeric flag checked). Position class:
+    config 5 alternates uniform / last-10% positions every two modifiers."""
+    from paper_2210_01076_b200 import workloads as W
+    sim = make_sim(w.n)
+    drv = W.NetDriver(sim, reference_gates=reference)
+    t0 = time.perf_counter()
+    drv.build(w.gates)
+    build_ms = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    sim.update_state()
+    full_ms = (time.perf_counter() - t0) * 1e3
+    lat = {"uniform": [], "tail": []}
+    for m, mod in enumerate(w.modifiers[:nmods]):
+        cls = "tail" if (tail_split and (m // 2) % 2 == 1) else "uniform"
+        t0 = time.perf_counter()
+        drv.modify(mod)
+        sim.update_state()
+        lat[cls].append((time.perf_counter() - t0) * 1e3)
+    nrm = sim.norm_squared()
+    close = getattr(sim, "close", None)
+    if close:
+        close()
+    return {"build_ms": build_ms, "full_update_ms": full_ms,
+            "uniform": latency_stats(lat["uniform"]), "tail": latency_stats(lat["tail"]),
+            "norm_error": abs(nrm - 1.0)}
+
+
+def incremental_section(nmods_c5):
+    """Config 5 (28 qubits, 5000 gates, alternating insert/remove) on the GPU
+    engine, and config 1 (16 qubits, 400 gates + 20 modifiers) on the GPU
+    engine and on the reference engine (qtask::Simulator, all host threads)."""
+    import oracle
+    from paper_2210_01076_b200 import Config, Simulator
+    from paper_2210_01076_b200 import workloads as W
+    out = {}
+    w5 = W.config5()
+    out["c5_gpu"] = dict(measure_incremental(lambda n: Simulator(n, Config()), w5, nmods_c5),
+                         workload=w5.name, modifiers=nmods_c5)
+    w1 = W.config1()
+    out["c1_gpu"] = dict(measure_incremental(lambda n: Simulator(n, Config()), w1, 20,
+                                             tail_split=False), workload=w1.name)
+    if oracle.ref_available():
+        threads = os.cpu_count() or 1
+        out["c1_reference_cpu"] = dict(
+            measure_incremental(lambda n: oracle.RefSimulator(n, 256, 0), w1, 20,
+                                reference=True, tail_split=False),
+            workload=w1.name, cores=threads, block_size=256,
+            note="reference qtask::Simulator (engine.cpp) compiled from its sources, "
+                 "threads = hardware_concurrency; CZ as H,CX,H nets")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -172,6 +235,8 @@ def main():
     ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--tile-qubits", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--incremental-mods", type=int, default=24,
+                    help="config-5 modifiers measured after the headline (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -293,7 +358,7 @@ def main():
                    "passes_per_step": len(tiles), "note": w.note},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
                      "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": None,
-                     "kernel": "tile_pass_kernel<3>", "peak_kind": peak_kind,
+                     "kernel": "tile_pass_kernel (qt_tilepass.cu)", "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms},
         "roofline_fp64": {"achieved_dfma_per_s": fp64_achieved, "peak_dfma_per_s": fp64_peak,
                           "frac": fp64_achieved / fp64_peak if fp64_peak else None,
@@ -307,6 +372,12 @@ def main():
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(w)
+    if world == 1 and args.incremental_mods > 0:
+        st.close()  # free the 16 GiB state for the incremental engine's checkpoints
+        try:
+            line["incremental"] = incremental_section(args.incremental_mods)
+        except Exception as e:  # reported, never fatal for the headline line
+            line["incremental"] = {"error": f"{type(e).__name__}: {e}"}
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

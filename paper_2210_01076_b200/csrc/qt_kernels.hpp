@@ -37,13 +37,15 @@ using KPassSmall = KPass<kSmallOps, kSmallRounds, kSmallPool>;
 using KPassLarge = KPass<kLargeOps, kLargeRounds, kLargePool>;
 static_assert(sizeof(KPassLarge) <= 32764, "kernel parameter limit");
 
-// Fused tile pass over a state of 2^nlocal amplitudes.
-cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid,
+// Fused tile pass over a state of 2^nlocal amplitudes. generic = false
+// selects the lean instantiation that only handles the fused layer ops
+// (MULTI, MULTIR, DTAB, STAB).
+cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool generic,
                              cudaStream_t s);
-cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid,
+cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
                              cudaStream_t s);
 // Max resident CTAs per SM of the tile-pass kernel for (k, R).
-int tile_pass_occupancy(int k, int R, bool large);
+int tile_pass_occupancy(int k, int R, bool large, bool generic);
 
 // Sets every amplitude to 0 and amplitude `index` to 1.
 cudaError_t launch_set_basis(double2* psi, uint64_t n, uint64_t index,

@@ -336,25 +336,28 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     h.ntiles = 1ull << (buf_bits_ - k);
     h.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
     size_t nops = 0, npool = 0;
+    bool generic = false;  // any single-gate op -> the full-dispatch kernel
     for (const PlanRound& pr : ps.rounds) {
       nops += pr.enc.ops.size();
       npool += pr.enc.pool.size();
+      for (const DOp& d : pr.enc.ops)
+        generic = generic || ((d.hdr & kOpVariantMask) >> 10) < D_MULTI;
     }
     const bool large = nops > static_cast<size_t>(kSmallOps) ||
                        npool > static_cast<size_t>(kSmallPool) ||
                        ps.rounds.size() > static_cast<size_t>(kSmallRounds);
-    const int occ = std::max(1, tile_pass_occupancy(k, R, large));
+    const int occ = std::max(1, tile_pass_occupancy(k, R, large, generic));
     const uint64_t cap = static_cast<uint64_t>(occ) * sms_;
     const int grid = static_cast<int>(std::min<uint64_t>(h.ntiles, cap));
     tstart(0);
     if (large) {
       kp_large_->h = h;
       fill_pass(*kp_large_, ps);
-      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, stream_), "tile pass launch");
+      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, generic, stream_), "tile pass launch");
     } else {
       kp_small_->h = h;
       fill_pass(*kp_small_, ps);
-      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, stream_), "tile pass launch");
+      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, generic, stream_), "tile pass launch");
     }
     tstop();
     stats.passes += 1;

@@ -294,7 +294,7 @@ __device__ __forceinline__ void k_stab(double2 (&v)[1 << R], const P& p, uint32_
 // register bits cleared; `sg` = the tile's global base index (smem).
 // Controls / diagonal bits outside the register slots are only evaluated for
 // ops whose header flags say they have them.
-template <int R, typename P>
+template <int R, bool GENERIC, typename P>
 __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const DOp& d,
                                          uint32_t jb, const uint64_t* sg) {
   const uint32_t hdr = d.hdr;
@@ -326,7 +326,11 @@ constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? QT_R3_MINB : 4);
 template <int R>
 constexpr int kMaxThreads = R >= 3 ? 256 : 512;
 
-template <int R, typename P>
+// GENERIC = false: the lean instantiation that only knows the fused layer
+// ops (MULTI / MULTIR / DTAB / STAB); every extra variant body costs
+// registers and instruction cache in the hot loop, so passes made only of
+// layer ops (e.g. every pass of config 3) run this one.
+template <int R, bool GENERIC, typename P>
 __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
     tile_pass_kernel(double2* psi, const __grid_constant__ P p) {
   extern __shared__ double2 sm[];
@@ -418,7 +422,7 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
         v[s] = sm[a];
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
-      for (uint32_t o = rd.op_first; o < o1; ++o) apply_op<R>(v, p, p.ops[o], jb, &s_tile[1]);
+      for (uint32_t o = rd.op_first; o < o1; ++o) apply_op<R, GENERIC>(v, p, p.ops[o], jb, &s_tile[1]);
       // opaque copy: forces the 2^R store addresses to be regenerated here
       // instead of being kept live (2^R registers) across the op loop
       uint32_t sjb2 = sjb;
@@ -451,32 +455,32 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
   if (__syncthreads_or(bad) && t == 0) atomicOr(h.flag, 1);
 }
 
-template <typename P>
+template <typename P, bool G>
 void* kernel_ptr(int R) {
   switch (R) {
-    case 1: return reinterpret_cast<void*>(&tile_pass_kernel<1, P>);
-    case 2: return reinterpret_cast<void*>(&tile_pass_kernel<2, P>);
-    case 3: return reinterpret_cast<void*>(&tile_pass_kernel<3, P>);
-    default: return reinterpret_cast<void*>(&tile_pass_kernel<4, P>);
+    case 1: return reinterpret_cast<void*>(&tile_pass_kernel<1, G, P>);
+    case 2: return reinterpret_cast<void*>(&tile_pass_kernel<2, G, P>);
+    case 3: return reinterpret_cast<void*>(&tile_pass_kernel<3, G, P>);
+    default: return reinterpret_cast<void*>(&tile_pass_kernel<4, G, P>);
   }
 }
 
-template <typename P>
+template <typename P, bool G>
 cudaError_t launch(double2* psi, const P& p, int grid, cudaStream_t s) {
   const size_t smem = sizeof(double2) << p.h.k;
   const int threads = 1 << (p.h.k - p.h.reg_bits);
   switch (p.h.reg_bits) {
     case 1:
-      tile_pass_kernel<1, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<1, G, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     case 2:
-      tile_pass_kernel<2, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<2, G, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     case 3:
-      tile_pass_kernel<3, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<3, G, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     default:
-      tile_pass_kernel<4, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<4, G, P><<<grid, threads, smem, s>>>(psi, p);
       break;
   }
   return cudaGetLastError();
@@ -484,10 +488,10 @@ cudaError_t launch(double2* psi, const P& p, int grid, cudaStream_t s) {
 
 }  // namespace
 
-int tile_pass_occupancy(int k, int R, bool large) {
-  // per-device cache: (large, k, R) -> resident CTAs per SM
+int tile_pass_occupancy(int k, int R, bool large, bool generic) {
+  // per-device cache: (generic, large, k, R) -> resident CTAs per SM
   static thread_local int cache_dev = -1;
-  static thread_local int cache[2][kMaxTileBits + 1][kMaxRegBits + 1];
+  static thread_local int cache[4][kMaxTileBits + 1][kMaxRegBits + 1];
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev != cache_dev) {
@@ -496,11 +500,12 @@ int tile_pass_occupancy(int k, int R, bool large) {
         for (int& v : row) v = -1;
     cache_dev = dev;
   }
-  int& slot = cache[large ? 1 : 0][k][R];
+  int& slot = cache[(large ? 1 : 0) + (generic ? 2 : 0)][k][R];
   if (slot >= 0) return slot;
   const size_t smem = sizeof(double2) << k;
   const int threads = 1 << (k - R);
-  void* fn = large ? kernel_ptr<KPassLarge>(R) : kernel_ptr<KPassSmall>(R);
+  void* fn = large ? (generic ? kernel_ptr<KPassLarge, true>(R) : kernel_ptr<KPassLarge, false>(R))
+                   : (generic ? kernel_ptr<KPassSmall, true>(R) : kernel_ptr<KPassSmall, false>(R));
   int occ = 0;
   // the attribute is per function: always allow the largest tile (2^13)
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -515,14 +520,16 @@ int tile_pass_occupancy(int k, int R, bool large) {
   return occ;
 }
 
-cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid,
+cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool generic,
                              cudaStream_t s) {
-  return launch(psi, p, grid, s);
+  return generic ? launch<KPassSmall, true>(psi, p, grid, s)
+                 : launch<KPassSmall, false>(psi, p, grid, s);
 }
 
-cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid,
+cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
                              cudaStream_t s) {
-  return launch(psi, p, grid, s);
+  return generic ? launch<KPassLarge, true>(psi, p, grid, s)
+                 : launch<KPassLarge, false>(psi, p, grid, s);
 }
 
 }  // namespace qtb
