@@ -62,12 +62,12 @@ enum DType : uint32_t {
   D_SWAP2 = 6,   // swap qubits on reg slots a and b
   D_PHASE1 = 7,  // multiply by d1 where bit set (S, T, phase) (4 DFMA/amp)
   // fused layer ops built by the round compiler (qt_plan.cpp)
-  D_MULTI = 8,   // complex 2x2 on every reg slot in mask a, ascending slots
-  D_MULTIR = 9,  // real 2x2 (4 doubles) on every reg slot in mask a
+  D_MULTI = 8,   // a LAYER: [diag table if kOpTable][sign terms: base mask dl,
+                 // arg >> 16 conditional terms] then a complex 2x2 on every
+                 // reg slot in mask a, ascending slots
+  D_MULTIR = 9,  // the same with real 2x2s (4 doubles per slot)
   D_DTAB = 10,   // per-slot complex factor table (2^R entries)
   D_STAB = 11,   // sign terms: slot masks negated under thread/tile conditions
-  D_LAYER = 12,  // one dispatch for a whole real layer: [diag table if kOpTable]
-                 // [sign base mask dl] [real 2x2 on every reg slot in mask a]
 };
 
 // Variant id of a device op: the kernel dispatches on it to a fully
@@ -88,13 +88,13 @@ constexpr uint32_t kOpDg = 1u << 19;    // dg != 0
 constexpr uint32_t kOpFlagMask = kOpLctl | kOpGctl | kOpDl | kOpDg;
 // dense dispatch index of the variant (tools/gen_variants.py) in bits 20..27
 constexpr uint32_t kOpIndexShift = 20;
-constexpr uint32_t kOpTable = 1u << 28;  // D_LAYER: a 2^R-entry table leads the pool data
+constexpr uint32_t kOpTable = 1u << 28;  // MULTI/MULTIR: a 2^R-entry table leads the pool data
 
 // 32 bytes; lives in the kernel-parameter constant bank (read uniformly).
 // Matrices / tables / sign terms are in the pass's double pool at `arg`.
 struct alignas(8) DOp {
   uint32_t hdr;      // vid(type, a, cs, ds) | flags
-  uint32_t arg;      // pool offset (doubles); STAB: offset | nterms << 16
+  uint32_t arg;      // pool offset (doubles); STAB / MULTI*: offset | nterms << 16
   uint32_t lmask;    // control bits among the round's NON-register tile bits
   uint32_t dl;       // diag target among non-register tile bits (mask) or 0
   uint64_t gmask;    // control bits outside the tile (global index bits)
@@ -122,9 +122,16 @@ constexpr int kDefaultRegBits = 3;
 struct DRound {
   uint16_t op_first;  // into the pass's op array
   uint16_t op_count;
-  uint8_t reg[kMaxRegBits];  // tile-bit indices of the register bits
+  uint8_t reg[kMaxRegBits];   // tile-bit indices of the register bits (slot order)
+  uint8_t sreg[kMaxRegBits];  // the same bits ascending (thread-index deposit)
+  uint32_t sbit[kMaxRegBits]; // swz(1 << reg[i]) * 16: smem byte-offset term of slot bit i
 };
-static_assert(sizeof(DRound) == 8, "DRound layout");
+static_assert(sizeof(DRound) == 28, "DRound layout");
+
+// Host copy of the device smem swizzle (qt_device.cuh swz): GF(2)-linear.
+constexpr uint32_t swz_host(uint32_t j) {
+  return j ^ ((j >> 3) & 7u) ^ ((j >> 6) & 7u) ^ ((j >> 9) & 7u) ^ ((j >> 12) & 7u);
+}
 
 // Per-launch capacity of the kernel-parameter block (<= 32764 bytes): a
 // pass with more ops / rounds / pool is split by the planner.

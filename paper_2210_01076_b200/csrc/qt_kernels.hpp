@@ -22,6 +22,13 @@ struct KPassHead {
   uint64_t outer_mask; // buffer bits outside the tile
   const double2* src;  // tiles are read from src and written to psi (may alias)
   int* flag;           // set to 1 if any written amplitude is non-finite
+  // 1: check the written amplitudes for inf/nan. Only the last tile pass of a
+  // launch sequence checks: a non-finite amplitude never becomes finite again
+  // under the (finite, linear) gate ops, so the final state shows it.
+  uint32_t check;
+  uint32_t pad_;
+  uint64_t slot_gb[1 << kMaxRegBits];  // byte offset of load slot s (s deposited into hi_mask)
+  uint32_t slot_sb[1 << kMaxRegBits];  // swz(s << (k - R)) * 16: smem byte term of slot s
 };
 
 // Kernel parameters (passed by value as a __grid_constant__: the rounds and

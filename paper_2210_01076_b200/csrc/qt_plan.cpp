@@ -320,11 +320,36 @@ void fold_signs(std::vector<cplx>& table, std::vector<SignTerm>& terms) {
   terms.swap(rest);
 }
 
-void emit_multi(LayerState& L, EncRound& out) {
-  if (!L.mmask) return;
+// Emits a layer as ONE device op (kernel k_layer): the layer's pre table,
+// its pre sign terms (unconditional ones as the base mask in dl, conditional
+// ones in the pool) and one 2x2 per register slot in L.mmask.
+void emit_layer(LayerState& L, EncRound& out) {
   DOp d{};
-  d.hdr = vid(L.mreal ? D_MULTIR : D_MULTI, static_cast<int>(L.mmask), -1, -1);
-  d.arg = static_cast<uint32_t>(out.pool.size());
+  const bool tab = !table_trivial(L.pre);
+  uint32_t base = 0;
+  std::vector<SignTerm> cond;
+  for (const SignTerm& t : L.pre_signs) {
+    if (t.lcond == 0 && t.gcond == 0) base ^= t.slots;
+    else cond.push_back(t);
+  }
+  d.hdr = vid(L.mreal ? D_MULTIR : D_MULTI, static_cast<int>(L.mmask), -1, -1) |
+          (tab ? kOpTable : 0u);
+  d.dl = base;
+  d.arg = static_cast<uint32_t>(out.pool.size()) | (static_cast<uint32_t>(cond.size()) << 16);
+  if (tab) {
+    for (const cplx& c : L.pre) {
+      out.pool.push_back(c.re);
+      out.pool.push_back(c.im);
+    }
+  }
+  for (const SignTerm& t : cond) {
+    const uint64_t w0 = static_cast<uint64_t>(t.slots) | (static_cast<uint64_t>(t.lcond) << 32);
+    double dw0, dw1;
+    std::memcpy(&dw0, &w0, 8);
+    std::memcpy(&dw1, &t.gcond, 8);
+    out.pool.push_back(dw0);
+    out.pool.push_back(dw1);
+  }
   for (int i = 0; i < L.R; ++i) {
     if (!(L.mmask & (1u << i))) continue;
     if (L.mreal) {
@@ -338,45 +363,24 @@ void emit_multi(LayerState& L, EncRound& out) {
   L.mreal = true;
 }
 
-// Emits the pre part and the layer's MULTI; the post part becomes the next
-// layer's pre part.
+// Emits the layer (pre part + 2x2s); the post part becomes the next
+// layer's pre part. QTB_NOLAYER=1 keeps table / signs / 2x2s as separate
+// dispatches (A/B measurements only).
 void close_layer(LayerState& L, EncRound& out) {
   fold_signs(L.pre, L.pre_signs);
-  // D_LAYER (one dispatch per real layer) measured slower than separate
-  // DTAB / STAB / MULTIR ops on B200 (C3: 630 vs 526 ms); kept behind
-  // QTB_LAYER=1 for further tuning
-  static const bool use_layer = std::getenv("QTB_LAYER") != nullptr;
-  if (use_layer && L.mmask && L.mreal) {
-    // one D_LAYER dispatch: conditional sign terms first (they commute with
-    // the table and the unconditional signs), then table + signs + rotations
-    uint32_t base = 0;
-    std::vector<SignTerm> cond;
-    for (const SignTerm& t : L.pre_signs) {
-      if (t.lcond == 0 && t.gcond == 0) base ^= t.slots;
-      else cond.push_back(t);
-    }
-    emit_signs(cond, out);
-    DOp d{};
-    const bool tab = !table_trivial(L.pre);
-    d.hdr = vid(D_LAYER, static_cast<int>(L.mmask), -1, -1) | (tab ? kOpTable : 0u);
-    d.dl = base;
-    d.arg = static_cast<uint32_t>(out.pool.size());
-    if (tab) {
-      for (const cplx& c : L.pre) {
-        out.pool.push_back(c.re);
-        out.pool.push_back(c.im);
-      }
-    }
-    for (int i = 0; i < L.R; ++i)
-      if (L.mmask & (1u << i))
-        for (int k = 0; k < 4; ++k) out.pool.push_back(L.M[i][k].re);
-    out.ops.push_back(d);
-    L.mmask = 0;
-    L.mreal = true;
+  static const bool separate = std::getenv("QTB_NOLAYER") != nullptr;
+  if (L.mmask && !separate) {
+    emit_layer(L, out);
   } else {
     emit_table(L.pre, out);
     emit_signs(L.pre_signs, out);
-    emit_multi(L, out);
+    if (L.mmask) {
+      std::vector<cplx> one(L.NS, cplx{1.0, 0.0});
+      L.pre.swap(one);
+      L.pre_signs.clear();
+      emit_layer(L, out);
+      L.pre.swap(one);
+    }
   }
   L.pre.swap(L.post);
   L.pre_signs.swap(L.post_signs);
@@ -786,9 +790,10 @@ std::string plan_to_json(const Plan& p, bool detail) {
           case D_DENSE: fp += ctl ? 4.0 : 8.0; break;
           case D_REAL: case D_ANTI: fp += ctl ? 2.0 : 4.0; break;
           case D_DIAG: case D_PHASE1: case D_DTAB: fp += 4.0; break;
-          case D_MULTI: fp += 8.0 * __builtin_popcount(a); break;
-          case D_MULTIR: fp += 4.0 * __builtin_popcount(a); break;
-          case D_LAYER:
+          case D_MULTI:
+            fp += 8.0 * __builtin_popcount(a) + ((d.hdr & kOpTable) ? 4.0 : 0.0);
+            break;
+          case D_MULTIR:
             fp += 4.0 * __builtin_popcount(a) + ((d.hdr & kOpTable) ? 4.0 : 0.0);
             break;
           default: break;
@@ -845,14 +850,31 @@ std::string plan_to_json(const Plan& p, bool detail) {
             continue;
           }
           const bool tab = (d.hdr & kOpTable) != 0;
-          if (type == D_MULTI) len = 8 * __builtin_popcount(a);
-          else if (type == D_MULTIR) len = 4 * __builtin_popcount(a);
-          else if (type == D_DTAB) len = 2 * NS;
-          else if (type == D_LAYER) len = (tab ? 2 * NS : 0) + 4 * __builtin_popcount(a);
-          for (size_t k = 0; k < len; ++k) {
-            std::snprintf(num, sizeof(num), "%s%.17g", k ? "," : "", pr.enc.pool[off + k]);
-            os << num;
+          auto put = [&](size_t from, size_t n) {
+            for (size_t k = 0; k < n; ++k) {
+              std::snprintf(num, sizeof(num), "%s%.17g", k ? "," : "", pr.enc.pool[from + k]);
+              os << num;
+            }
+          };
+          if (type == D_MULTI || type == D_MULTIR) {
+            // layer: [..., [2x2 data], tabflag, [table], [[base,0,0], terms...]]
+            const uint32_t nt = d.arg >> 16;
+            const size_t toff = off, soff = off + (tab ? 2 * NS : 0), moff = soff + 2 * nt;
+            put(moff, (type == D_MULTI ? 8 : 4) * __builtin_popcount(a));
+            os << "]," << (tab ? 1 : 0) << ",[";
+            if (tab) put(toff, 2 * NS);
+            os << "],[[" << d.dl << ",0,0]";
+            for (uint32_t t = 0; t < nt; ++t) {
+              uint64_t w0, w1;
+              std::memcpy(&w0, &pr.enc.pool[soff + 2 * t], 8);
+              std::memcpy(&w1, &pr.enc.pool[soff + 2 * t + 1], 8);
+              os << ",[" << (w0 & 0xffffffffull) << "," << (w0 >> 32) << "," << w1 << "]";
+            }
+            os << "]]";
+            continue;
           }
+          if (type == D_DTAB) len = 2 * NS;
+          put(off, len);
           os << "]," << (tab ? 1 : 0) << "]";
         }
         os << "]}";

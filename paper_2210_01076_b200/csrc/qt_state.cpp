@@ -260,12 +260,19 @@ void fill_pass(P& kp, const PlanPass& ps) {
     dr = DRound{};
     dr.op_first = static_cast<uint16_t>(nops);
     dr.op_count = static_cast<uint16_t>(pr.enc.ops.size());
-    for (size_t i = 0; i < pr.reg.size() && i < static_cast<size_t>(kMaxRegBits); ++i)
+    const size_t nreg = std::min(pr.reg.size(), static_cast<size_t>(kMaxRegBits));
+    std::vector<int> sorted(pr.reg.begin(), pr.reg.begin() + nreg);
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 0; i < nreg; ++i) {
       dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
+      dr.sreg[i] = static_cast<uint8_t>(sorted[i]);
+      dr.sbit[i] = swz_host(1u << pr.reg[i]) << 4;
+    }
     for (DOp d : pr.enc.ops) {
       // pool offsets are round-relative: rebase onto the launch's pool
       const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
-      if (type == D_STAB) d.arg = ((d.arg & 0xffff) + npool) | (d.arg & 0xffff0000u);
+      if (type == D_STAB || type == D_MULTI || type == D_MULTIR)
+        d.arg = ((d.arg & 0xffff) + npool) | (d.arg & 0xffff0000u);  // offset | nterms << 16
       else d.arg += npool;
       kp.ops[nops++] = d;
     }
@@ -307,6 +314,9 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
   }
   if (!kp_small_) kp_small_.reset(new KPassSmall);
   if (!kp_large_) kp_large_.reset(new KPassLarge);
+  size_t last_tile = plan.passes.size();
+  for (size_t pi = 0; pi < plan.passes.size(); ++pi)
+    if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
   for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
     const PlanPass& ps = plan.passes[pi];
     if (ps.kind == PlanPass::Exchange) {
@@ -333,6 +343,14 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       else h.hi_mask |= b;
     }
     h.outer_mask = buf_mask & ~tile_mask;
+    h.check = pi == last_tile ? 1u : 0u;
+    for (uint32_t s = 0; s < (1u << R); ++s) {
+      uint64_t off = 0;
+      for (int i = 0; i < R; ++i)
+        if ((s >> i) & 1u) off |= 1ull << ps.tile_phys[k - R + i];
+      h.slot_gb[s] = off * sizeof(double2);
+      h.slot_sb[s] = swz_host(s << (k - R)) << 4;
+    }
     h.ntiles = 1ull << (buf_bits_ - k);
     h.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
     size_t nops = 0, npool = 0;
@@ -341,7 +359,8 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       nops += pr.enc.ops.size();
       npool += pr.enc.pool.size();
       for (const DOp& d : pr.enc.ops)
-        generic = generic || ((d.hdr & kOpVariantMask) >> 10) < D_MULTI;
+        generic = generic || ((d.hdr & kOpVariantMask) >> 10) < D_MULTI ||
+                  (d.hdr & kOpFlagMask) != 0;
     }
     const bool large = nops > static_cast<size_t>(kSmallOps) ||
                        npool > static_cast<size_t>(kSmallPool) ||

@@ -232,32 +232,6 @@ __device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, int o
   }
 }
 
-// A whole real layer in one dispatch: optional per-slot diagonal table,
-// unconditional sign mask, then one real rotation per register slot in MASK.
-template <int R, int MASK, typename P>
-__device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, int o,
-                                        uint32_t signs, bool table) {
-  if (table) {
-#pragma unroll
-    for (int s = 0; s < (1 << R); ++s) {
-      const double tr = p.pool[o + 2 * s], ti = p.pool[o + 2 * s + 1];
-      const double q0 = -ti * v[s].y, q1 = ti * v[s].x;
-      v[s].x = fma(tr, v[s].x, q0);
-      v[s].y = fma(tr, v[s].y, q1);
-    }
-    o += 2 << R;
-  }
-  if (signs) {
-#pragma unroll
-    for (int s = 0; s < (1 << R); ++s) {
-      const uint32_t sb = ((signs >> s) & 1u) << 31;
-      v[s] = make_double2(__hiloint2double(__double2hiint(v[s].x) ^ sb, __double2loint(v[s].x)),
-                          __hiloint2double(__double2hiint(v[s].y) ^ sb, __double2loint(v[s].y)));
-    }
-  }
-  k_multir<R, MASK>(v, p, o);
-}
-
 // per-slot complex factor table (all merged diagonal gates of a layer)
 template <int R, typename P>
 __device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, int o) {
@@ -265,29 +239,56 @@ __device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, int o) 
   for (int s = 0; s < (1 << R); ++s) cscale(v[s], p.pool[o + 2 * s], p.pool[o + 2 * s + 1]);
 }
 
-// sign terms: mask of negated slots from thread/tile conditions, then one
-// integer XOR per negated component
+// Sign terms: `base` = the unconditional terms (folded on the host) and nt
+// thread/tile-conditional terms at pool[o]; then one integer XOR per
+// component (branch-free: the mask differs between threads).
 template <int R, typename P>
-__device__ __forceinline__ void k_stab(double2 (&v)[1 << R], const P& p, uint32_t arg,
-                                       uint32_t base, uint32_t jb, const uint64_t* sg) {
-  const int o = static_cast<int>(arg & 0xffffu);
-  const uint32_t nt = arg >> 16;
-  uint32_t mask = base;  // unconditional terms, folded on the host
+__device__ __forceinline__ void apply_signs(double2 (&v)[1 << R], const P& p, int o,
+                                            uint32_t nt, uint32_t base, uint32_t jb,
+                                            const uint64_t* sg) {
+  uint32_t mask = base;
   for (int t = 0; t < static_cast<int>(nt); ++t) {
     const uint64_t w0 = static_cast<uint64_t>(__double_as_longlong(p.pool[o + 2 * t]));
     const uint64_t gc = static_cast<uint64_t>(__double_as_longlong(p.pool[o + 2 * t + 1]));
     const uint32_t lc = static_cast<uint32_t>(w0 >> 32);
     bool on = (jb & lc) == lc;
     if (gc) on = on && (*sg & gc) == gc;
-    if (on) mask ^= static_cast<uint32_t>(w0);
+    mask ^= on ? static_cast<uint32_t>(w0) : 0u;
   }
-  if (!mask) return;
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
     const uint32_t sb = ((mask >> s) & 1u) << 31;
     v[s] = make_double2(__hiloint2double(__double2hiint(v[s].x) ^ sb, __double2loint(v[s].x)),
                         __hiloint2double(__double2hiint(v[s].y) ^ sb, __double2loint(v[s].y)));
   }
+}
+
+template <int R, typename P>
+__device__ __forceinline__ void k_stab(double2 (&v)[1 << R], const P& p, uint32_t arg,
+                                       uint32_t base, uint32_t jb, const uint64_t* sg) {
+  apply_signs<R>(v, p, static_cast<int>(arg & 0xffffu), arg >> 16, base, jb, sg);
+}
+
+// A fused layer in one dispatch (the round compiler's unit): the layer's
+// diagonal table (kOpTable), its sign terms (base mask in dl, conditional
+// terms counted in arg >> 16), then one 2x2 per register slot in MASK
+// (real rotations after the ZYZ split, or complex). Pool data in that order.
+template <int R, int MASK, bool REAL, typename P>
+__device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32_t arg,
+                                        uint32_t hdr, uint32_t base, uint32_t jb,
+                                        const uint64_t* sg) {
+  int o = static_cast<int>(arg & 0xffffu);
+  const uint32_t nt = arg >> 16;
+  if (hdr & kOpTable) {
+    k_dtab<R>(v, p, o);
+    o += 2 << R;
+  }
+  if (nt | base) {
+    apply_signs<R>(v, p, o, nt, base, jb, sg);
+    o += 2 * static_cast<int>(nt);
+  }
+  if constexpr (REAL) k_multir<R, MASK>(v, p, o);
+  else k_multi<R, MASK>(v, p, o);
 }
 
 // Applies one device op. `jb` = the thread's tile-local index with the
@@ -299,13 +300,16 @@ __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const
                                          uint32_t jb, const uint64_t* sg) {
   const uint32_t hdr = d.hdr;
   bool bit = false;
-  if (hdr & kOpFlagMask) {
-    if ((hdr & kOpLctl) && (jb & d.lmask) != d.lmask) return;
-    if (hdr & kOpDl) bit = (jb & d.dl) != 0;
-    if (hdr & (kOpGctl | kOpDg)) {
-      const uint64_t g = *sg;
-      if ((g & d.gmask) != d.gmask) return;
-      bit = bit || (g & d.dg) != 0;
+  // the fused layer ops (the only ones of the lean kernel) carry no flags
+  if constexpr (GENERIC) {
+    if (hdr & kOpFlagMask) {
+      if ((hdr & kOpLctl) && (jb & d.lmask) != d.lmask) return;
+      if (hdr & kOpDl) bit = (jb & d.dl) != 0;
+      if (hdr & (kOpGctl | kOpDg)) {
+        const uint64_t g = *sg;
+        if ((g & d.gmask) != d.gmask) return;
+        bit = bit || (g & d.dg) != 0;
+      }
     }
   }
   (void)bit;
@@ -336,30 +340,17 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
   extern __shared__ double2 sm[];
   constexpr int NS = 1 << R;
   const KPassHead& h = p.h;
-  const uint32_t lo_bits = h.k - R;
   const uint32_t t = threadIdx.x;
+  char* const smb = reinterpret_cast<char*>(sm);
 
-  // global offsets of this thread's load slots: tile bits [0, k-R) from the
+  // global offset of this thread's load slots: tile bits [0, k-R) from the
   // thread index (coalesced: low tile bits are the low physical bits), tile
-  // bits [k-R, k) from the slot index
+  // bits [k-R, k) from the slot index (host-precomputed byte offsets
+  // h.slot_gb, CTA-uniform)
   const uint64_t off_t = pdep64(t, h.lo_mask);
-  // the R physical bits of the slot index (CTA-uniform)
-  uint32_t hpos[R];
-  {
-    uint64_t mk = h.hi_mask;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {
-      hpos[i] = static_cast<uint32_t>(__ffsll(static_cast<long long>(mk)) - 1);
-      mk &= mk - 1;
-    }
-  }
-#define QT_SLOT_OFF(s)                                                                \
-  ([&] {                                                                              \
-    uint64_t o_ = 0;                                                                  \
-    _Pragma("unroll") for (int i_ = 0; i_ < R; ++i_) if ((s) & (1 << i_)) o_ |= 1ull \
-        << hpos[i_];                                                                  \
-    return o_;                                                                        \
-  }())
+  // smem byte offset of the thread's slots: swz is GF(2)-linear, so
+  // swz(t | s << (k-R)) * 16 = st4 ^ h.slot_sb[s]
+  const uint32_t st4 = swz(t) << 4;
 
   // per-tile uniform values live in smem while the register rounds run
   __shared__ uint64_t s_tile[2];  // [0] tile base, [1] global base (+ rank bits)
@@ -377,81 +368,73 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
       s_tile[1] = h.gbase_hi | base;
     }
     {
-      const double2* src = h.src + base + off_t;
+      const char* src = reinterpret_cast<const char*>(h.src + base + off_t);
       double2 ld[NS];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) ld[s] = __ldcs(src + QT_SLOT_OFF(s));
+      for (int s = 0; s < NS; ++s)
+        ld[s] = __ldcs(reinterpret_cast<const double2*>(src + h.slot_gb[s]));
 #pragma unroll
-      for (int s = 0; s < NS; ++s) sm[swz(t | (uint32_t(s) << lo_bits))] = ld[s];
+      for (int s = 0; s < NS; ++s)
+        *reinterpret_cast<double2*>(smb + (st4 ^ h.slot_sb[s])) = ld[s];
     }
     __syncthreads();
 
     for (uint32_t r = 0; r < h.nrounds; ++r) {
-      const DRound rd = p.rounds[r];
-      uint32_t rb[R];
-#pragma unroll
-      for (int i = 0; i < R; ++i) rb[i] = rd.reg[i];
+      const DRound& rd = p.rounds[r];
       // deposit t into the non-register tile bits (insert zeros ascending)
-      uint32_t sr[R];
-#pragma unroll
-      for (int i = 0; i < R; ++i) sr[i] = rb[i];
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int j2 = i + 1; j2 < R; ++j2)
-          if (sr[j2] < sr[i]) {
-            const uint32_t tmp = sr[i];
-            sr[i] = sr[j2];
-            sr[j2] = tmp;
-          }
       uint32_t jb = t;
 #pragma unroll
-      for (int i = 0; i < R; ++i) jb = insert_zero(jb, sr[i]);
-      // swz is GF(2)-linear: swz(jb | bits) = swz(jb) ^ swz(bits)
-      const uint32_t sjb = swz(jb);
-      uint32_t srb[R];
-#pragma unroll
-      for (int i = 0; i < R; ++i) srb[i] = swz(1u << rb[i]);
+      for (int i = 0; i < R; ++i) jb = insert_zero(jb, rd.sreg[i]);
+      // swz is GF(2)-linear: swz(jb | bits) * 16 = sj4 ^ (XOR of rd.sbit)
+      const uint32_t sj4 = swz(jb) << 4;
       double2 v[NS];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        uint32_t a = sjb;
+        uint32_t a = sj4;
 #pragma unroll
         for (int i = 0; i < R; ++i)
-          if (s & (1 << i)) a ^= srb[i];
-        v[s] = sm[a];
+          if (s & (1 << i)) a ^= rd.sbit[i];
+        v[s] = *reinterpret_cast<const double2*>(smb + a);
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
       for (uint32_t o = rd.op_first; o < o1; ++o) apply_op<R, GENERIC>(v, p, p.ops[o], jb, &s_tile[1]);
       // opaque copy: forces the 2^R store addresses to be regenerated here
       // instead of being kept live (2^R registers) across the op loop
-      uint32_t sjb2 = sjb;
-      asm volatile("" : "+r"(sjb2));
+      // (and the slot terms re-read from the constant bank)
+      uint32_t sj4b = sj4, rr = r;
+      asm volatile("" : "+r"(sj4b), "+r"(rr));
+      const DRound& rd2 = p.rounds[rr];
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        uint32_t a = sjb2;
+        uint32_t a = sj4b;
 #pragma unroll
         for (int i = 0; i < R; ++i)
-          if (s & (1 << i)) a ^= srb[i];
-        sm[a] = v[s];
+          if (s & (1 << i)) a ^= rd2.sbit[i];
+        *reinterpret_cast<double2*>(smb + a) = v[s];
       }
       __syncthreads();
     }
 
     base = s_tile[0];
     {
-      double2* dst = psi + base + off_t;
+      char* dst = reinterpret_cast<char*>(psi + base + off_t);
+      if (h.check) {
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const double2 x = sm[swz(t | (uint32_t(s) << lo_bits))];
-        bad = bad || !finite2(x);
-        __stcs(dst + QT_SLOT_OFF(s), x);
+        for (int s = 0; s < NS; ++s) {
+          const double2 x = *reinterpret_cast<const double2*>(smb + (st4 ^ h.slot_sb[s]));
+          bad = bad || !finite2(x);
+          __stcs(reinterpret_cast<double2*>(dst + h.slot_gb[s]), x);
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+          __stcs(reinterpret_cast<double2*>(dst + h.slot_gb[s]),
+                 *reinterpret_cast<const double2*>(smb + (st4 ^ h.slot_sb[s])));
       }
     }
     base = ((base | ~h.outer_mask) + 1) & h.outer_mask;
     __syncthreads();  // smem reuse by the next tile
   }
-#undef QT_SLOT_OFF
   if (__syncthreads_or(bad) && t == 0) atomicOr(h.flag, 1);
 }
 

@@ -12,11 +12,27 @@ import json
 import numpy as np
 
 (D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1,
- D_MULTI, D_MULTIR, D_DTAB, D_STAB, D_LAYER) = range(13)
+ D_MULTI, D_MULTIR, D_DTAB, D_STAB) = range(12)
 
 
 def _bit(idx, pos):
     return (idx >> np.uint64(pos)) & np.uint64(1)
+
+
+def _signs(psi, terms, slot, idx, tile):
+    """Sign terms [slots, lcond, gcond]: negate where the slot is in `slots`
+    and the tile bits `lcond` / global bits `gcond` are all 1."""
+    neg = np.zeros(len(psi), dtype=bool)
+    for slots, lcond, gcond in terms:
+        on = np.ones(len(psi), dtype=bool)
+        for tb in range(len(tile)):
+            if (lcond >> tb) & 1:
+                on &= _bit(idx, tile[tb]) == 1
+        for pb in range(64):
+            if (gcond >> pb) & 1:
+                on &= _bit(idx, pb) == 1
+        neg ^= on & (((slots >> slot) & 1) == 1)
+    return np.where(neg, -psi, psi)
 
 
 def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) -> np.ndarray:
@@ -54,6 +70,12 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                 data = op[8]
                 b = ds
                 if typ in (D_MULTI, D_MULTIR):
+                    # a layer: [table][sign terms] then one 2x2 per slot in a
+                    # (op[9] table flag, op[10] table, op[11] sign terms)
+                    if int(op[9]):
+                        tab = np.array(op[10][0::2]) + 1j * np.array(op[10][1::2])
+                        psi = psi * tab[slot]
+                    psi = _signs(psi, op[11], slot, idx, tile)
                     k = 0
                     for sl in range(len(reg)):
                         if not (a >> sl) & 1:
@@ -75,41 +97,8 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                     tab = np.array(data[0::2]) + 1j * np.array(data[1::2])
                     psi = psi * tab[slot]
                     continue
-                if typ == D_LAYER:
-                    has_tab = int(op[9])
-                    k0 = 0
-                    if has_tab:
-                        ns = 1 << len(reg)
-                        tab = np.array(data[0:2 * ns:2]) + 1j * np.array(data[1:2 * ns:2])
-                        psi = psi * tab[slot]
-                        k0 = 2 * ns
-                    if dl:  # unconditional sign mask
-                        psi = np.where(((dl >> slot) & 1) == 1, -psi, psi)
-                    k = 0
-                    for sl in range(len(reg)):
-                        if not (a >> sl) & 1:
-                            continue
-                        mm = np.array(data[k0 + 4 * k:k0 + 4 * k + 4], dtype=np.complex128)
-                        t = tile[reg[sl]]
-                        lo = np.nonzero(_bit(idx, t) == 0)[0]
-                        hi = lo | (1 << t)
-                        x, y = psi[lo].copy(), psi[hi].copy()
-                        psi[lo] = mm[0] * x + mm[1] * y
-                        psi[hi] = mm[2] * x + mm[3] * y
-                        k += 1
-                    continue
                 if typ == D_STAB:
-                    neg = np.zeros(len(psi), dtype=bool)
-                    for slots, lcond, gcond in data:
-                        on = np.ones(len(psi), dtype=bool)
-                        for tb in range(len(tile)):
-                            if (lcond >> tb) & 1:
-                                on &= _bit(idx, tile[tb]) == 1
-                        for pb in range(64):
-                            if (gcond >> pb) & 1:
-                                on &= _bit(idx, pb) == 1
-                        neg ^= on & (((slots >> slot) & 1) == 1)
-                    psi = np.where(neg, -psi, psi)
+                    psi = _signs(psi, data, slot, idx, tile)
                     continue
                 m = np.array(data[0:8], dtype=np.float64)
                 m = m[0::2] + 1j * m[1::2]
