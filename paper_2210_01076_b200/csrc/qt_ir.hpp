@@ -65,9 +65,10 @@ enum DType : uint32_t {
   D_MULTI = 8,   // a LAYER: [diag table if kOpTable][sign terms: base mask dl,
                  // arg >> 16 conditional terms] then a complex 2x2 on every
                  // reg slot in mask a, ascending slots
-  D_MULTIR = 9,  // the same with real 2x2s (4 doubles per slot)
-  D_DTAB = 10,   // per-slot complex factor table (2^R entries)
-  D_STAB = 11,   // sign terms: slot masks negated under thread/tile conditions
+  D_MULTIR = 9,  // the same with real rotations [[c,-s],[s,c]] (2 doubles per slot)
+  // (a lone diagonal table or sign op is a MULTIR layer with an empty mask)
+  D_DTAB = 10,   // retired: was a separate table op
+  D_STAB = 11,   // retired: was a separate sign-term op
 };
 
 // Variant id of a device op: the kernel dispatches on it to a fully

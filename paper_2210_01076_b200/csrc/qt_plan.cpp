@@ -267,7 +267,7 @@ bool table_trivial(const std::vector<cplx>& t) {
 void emit_table(const std::vector<cplx>& t, EncRound& out) {
   if (table_trivial(t)) return;
   DOp d{};
-  d.hdr = vid(D_DTAB, 0, -1, -1);
+  d.hdr = vid(D_MULTIR, 0, -1, -1) | kOpTable;  // a layer with no 2x2s
   d.arg = static_cast<uint32_t>(out.pool.size());
   for (const cplx& c : t) {
     out.pool.push_back(c.re);
@@ -289,7 +289,7 @@ void emit_signs(const std::vector<SignTerm>& terms, EncRound& out) {
   }
   if (base == 0 && cond.empty()) return;
   DOp d{};
-  d.hdr = vid(D_STAB, 0, -1, -1);
+  d.hdr = vid(D_MULTIR, 0, -1, -1);  // a layer with no table and no 2x2s
   d.dl = base;
   const uint32_t off = static_cast<uint32_t>(out.pool.size());
   d.arg = off | (static_cast<uint32_t>(cond.size()) << 16);
@@ -353,7 +353,9 @@ void emit_layer(LayerState& L, EncRound& out) {
   for (int i = 0; i < L.R; ++i) {
     if (!(L.mmask & (1u << i))) continue;
     if (L.mreal) {
-      for (int k = 0; k < 4; ++k) out.pool.push_back(L.M[i][k].re);
+      // rotation form (to_rotations): [[c, -s], [s, c]] stored as (c, s)
+      out.pool.push_back(L.M[i][0].re);
+      out.pool.push_back(L.M[i][2].re);
     } else {
       push_matrix(out.pool, L.M[i]);
     }
@@ -366,7 +368,32 @@ void emit_layer(LayerState& L, EncRound& out) {
 // Emits the layer (pre part + 2x2s); the post part becomes the next
 // layer's pre part. QTB_NOLAYER=1 keeps table / signs / 2x2s as separate
 // dispatches (A/B measurements only).
+// Real layers are stored as rotations (2 doubles per slot, half the constant
+// loads): a real orthogonal 2x2 is a rotation [[c,-s],[s,c]] or a reflection
+// [[c,s],[s,-c]] = rotation . Z, whose Z joins the layer's (earlier-applied)
+// sign terms. Anything else makes the layer complex.
+void to_rotations(LayerState& L) {
+  if (!L.mmask || !L.mreal) return;
+  for (int i = 0; i < L.R; ++i) {
+    if (!(L.mmask & (1u << i))) continue;
+    const double m0 = L.M[i][0].re, m1 = L.M[i][1].re, m2 = L.M[i][2].re, m3 = L.M[i][3].re;
+    if (m0 == m3 && m1 == -m2) continue;
+    if (m0 == -m3 && m1 == m2) {
+      SignTerm z{};
+      for (int s = 0; s < L.NS; ++s)
+        if ((s >> i) & 1) z.slots |= 1u << s;
+      L.pre_signs.push_back(z);
+      L.M[i][1] = cplx{-m2, 0.0};
+      L.M[i][3] = cplx{m0, 0.0};
+      continue;
+    }
+    L.mreal = false;
+    return;
+  }
+}
+
 void close_layer(LayerState& L, EncRound& out) {
+  to_rotations(L);
   fold_signs(L.pre, L.pre_signs);
   static const bool separate = std::getenv("QTB_NOLAYER") != nullptr;
   if (L.mmask && !separate) {
@@ -405,6 +432,8 @@ inline bool bit_of(int s, int slot) { return slot >= 0 && ((s >> slot) & 1); }
 // Stores each op's dense dispatch index (the kernel's switch key).
 void set_dispatch_index(EncRound& out, int R) {
   for (DOp& d : out.ops) {
+    const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
+    if (type == D_MULTI || type == D_MULTIR) continue;  // layers: kernel k_layer
     const uint16_t idx = variant_index(R, d.hdr & kOpVariantMask);
     if (idx == 0xffff) throw std::logic_error("device op without a kernel variant");
     d.hdr = (d.hdr & ~(0xffu << kOpIndexShift)) | (static_cast<uint32_t>(idx) << kOpIndexShift);
@@ -860,7 +889,7 @@ std::string plan_to_json(const Plan& p, bool detail) {
             // layer: [..., [2x2 data], tabflag, [table], [[base,0,0], terms...]]
             const uint32_t nt = d.arg >> 16;
             const size_t toff = off, soff = off + (tab ? 2 * NS : 0), moff = soff + 2 * nt;
-            put(moff, (type == D_MULTI ? 8 : 4) * __builtin_popcount(a));
+            put(moff, (type == D_MULTI ? 8 : 2) * __builtin_popcount(a));
             os << "]," << (tab ? 1 : 0) << ",[";
             if (tab) put(toff, 2 * NS);
             os << "],[[" << d.dl << ",0,0]";

@@ -203,35 +203,6 @@ __device__ __forceinline__ void k_swap2(double2 (&v)[1 << R]) {
   }
 }
 
-// One 2x2 per register slot in MASK, ascending slots (they commute exactly,
-// so one fixed order); complex: 8 pool doubles per slot, real: 4.
-template <int R, int MASK, typename P>
-__device__ __forceinline__ void k_multi(double2 (&v)[1 << R], const P& p, int o) {
-#pragma unroll
-  for (int a = 0; a < R; ++a) {
-    if (!(MASK & (1 << a))) continue;
-    if (a == 0) k_dense<R, 0, -1>(v, p, o);
-    if (a == 1) k_dense<R, (R > 1 ? 1 : 0), -1>(v, p, o);
-    if (a == 2) k_dense<R, (R > 2 ? 2 : 0), -1>(v, p, o);
-    if (a == 3) k_dense<R, (R > 3 ? 3 : 0), -1>(v, p, o);
-    o += 8;
-  }
-}
-
-template <int R, int MASK, typename P>
-__device__ __forceinline__ void k_multir(double2 (&v)[1 << R], const P& p, int o) {
-#pragma unroll
-  for (int a = 0; a < R; ++a) {
-    if (!(MASK & (1 << a))) continue;
-    const double m0 = p.pool[o], m1 = p.pool[o + 1], m2 = p.pool[o + 2], m3 = p.pool[o + 3];
-    if (a == 0) pair_real<R, 0, -1>(v, m0, m1, m2, m3);
-    if (a == 1) pair_real<R, (R > 1 ? 1 : 0), -1>(v, m0, m1, m2, m3);
-    if (a == 2) pair_real<R, (R > 2 ? 2 : 0), -1>(v, m0, m1, m2, m3);
-    if (a == 3) pair_real<R, (R > 3 ? 3 : 0), -1>(v, m0, m1, m2, m3);
-    o += 4;
-  }
-}
-
 // per-slot complex factor table (all merged diagonal gates of a layer)
 template <int R, typename P>
 __device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, int o) {
@@ -263,19 +234,44 @@ __device__ __forceinline__ void apply_signs(double2 (&v)[1 << R], const P& p, in
   }
 }
 
-template <int R, typename P>
-__device__ __forceinline__ void k_stab(double2 (&v)[1 << R], const P& p, uint32_t arg,
-                                       uint32_t base, uint32_t jb, const uint64_t* sg) {
-  apply_signs<R>(v, p, static_cast<int>(arg & 0xffffu), arg >> 16, base, jb, sg);
+// slot bodies of a layer, slots A..R-1 (compile-time slot index, runtime mask)
+template <int R, int A, typename P>
+__device__ __forceinline__ void layer_rot(double2 (&v)[1 << R], const P& p, uint32_t mask,
+                                          int o) {
+  if constexpr (A < R) {
+    if (mask & (1u << A)) {
+      // rotation [[c, -s], [s, c]] stored as (c, s)
+      const double c = p.pool[o], sn = p.pool[o + 1];
+      pair_real<R, A, -1>(v, c, -sn, sn, c);
+      o += 2;
+    }
+    layer_rot<R, A + 1>(v, p, mask, o);
+  }
 }
 
-// A fused layer in one dispatch (the round compiler's unit): the layer's
-// diagonal table (kOpTable), its sign terms (base mask in dl, conditional
-// terms counted in arg >> 16), then one 2x2 per register slot in MASK
-// (real rotations after the ZYZ split, or complex). Pool data in that order.
-template <int R, int MASK, bool REAL, typename P>
-__device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32_t arg,
-                                        uint32_t hdr, uint32_t base, uint32_t jb,
+template <int R, int A, typename P>
+__device__ __forceinline__ void layer_dense(double2 (&v)[1 << R], const P& p, uint32_t mask,
+                                            int o) {
+  if constexpr (A < R) {
+    if (mask & (1u << A)) {
+      k_dense<R, A, -1>(v, p, o);
+      o += 8;
+    }
+    layer_dense<R, A + 1>(v, p, mask, o);
+  }
+}
+
+// A fused LAYER in one dispatch (the round compiler's unit, types MULTI /
+// MULTIR): the layer's diagonal table (kOpTable), its sign terms (base mask
+// in dl, conditional terms counted in arg >> 16), then one 2x2 per register
+// slot in the slot mask, ascending slots (they commute exactly, so one fixed
+// order): real rotations (c, s) after the ZYZ split, or complex 2x2s. Pool
+// data in that order. A lone table / sign op is a layer with an empty mask.
+// The slot loop is a runtime (CTA-uniform) mask over R compiled slot bodies:
+// one copy of each body keeps the hot loop inside the instruction cache.
+template <int R, typename P>
+__device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32_t hdr,
+                                        uint32_t arg, uint32_t base, uint32_t jb,
                                         const uint64_t* sg) {
   int o = static_cast<int>(arg & 0xffffu);
   const uint32_t nt = arg >> 16;
@@ -287,8 +283,9 @@ __device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32
     apply_signs<R>(v, p, o, nt, base, jb, sg);
     o += 2 * static_cast<int>(nt);
   }
-  if constexpr (REAL) k_multir<R, MASK>(v, p, o);
-  else k_multi<R, MASK>(v, p, o);
+  const uint32_t mask = (hdr >> 6) & 15u;
+  if (((hdr & kOpVariantMask) >> 10) == D_MULTIR) layer_rot<R, 0>(v, p, mask, o);
+  else layer_dense<R, 0>(v, p, mask, o);
 }
 
 // Applies one device op. `jb` = the thread's tile-local index with the
@@ -299,20 +296,22 @@ template <int R, bool GENERIC, typename P>
 __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const DOp& d,
                                          uint32_t jb, const uint64_t* sg) {
   const uint32_t hdr = d.hdr;
+  const uint32_t type = (hdr & kOpVariantMask) >> 10;
+  if (!GENERIC || type == D_MULTI || type == D_MULTIR) {
+    // the fused layer ops (the only ones of the lean kernel) carry no flags
+    k_layer<R>(v, p, hdr, d.arg, d.dl, jb, sg);
+    return;
+  }
   bool bit = false;
-  // the fused layer ops (the only ones of the lean kernel) carry no flags
-  if constexpr (GENERIC) {
-    if (hdr & kOpFlagMask) {
-      if ((hdr & kOpLctl) && (jb & d.lmask) != d.lmask) return;
-      if (hdr & kOpDl) bit = (jb & d.dl) != 0;
-      if (hdr & (kOpGctl | kOpDg)) {
-        const uint64_t g = *sg;
-        if ((g & d.gmask) != d.gmask) return;
-        bit = bit || (g & d.dg) != 0;
-      }
+  if (hdr & kOpFlagMask) {
+    if ((hdr & kOpLctl) && (jb & d.lmask) != d.lmask) return;
+    if (hdr & kOpDl) bit = (jb & d.dl) != 0;
+    if (hdr & (kOpGctl | kOpDg)) {
+      const uint64_t g = *sg;
+      if ((g & d.gmask) != d.gmask) return;
+      bit = bit || (g & d.dg) != 0;
     }
   }
-  (void)bit;
   const uint32_t arg = d.arg;
   const uint32_t idx = (hdr >> kOpIndexShift) & 0xffu;
 #include "qt_variants.inc"

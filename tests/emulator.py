@@ -83,8 +83,9 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                         if typ == D_MULTI:
                             mm = np.array(data[8 * k:8 * k + 8])
                             mm = mm[0::2] + 1j * mm[1::2]
-                        else:
-                            mm = np.array(data[4 * k:4 * k + 4], dtype=np.complex128)
+                        else:  # rotation (c, s): [[c, -s], [s, c]]
+                            c, sn = data[2 * k], data[2 * k + 1]
+                            mm = np.array([c, -sn, sn, c], dtype=np.complex128)
                         t = tile[reg[sl]]
                         lo = np.nonzero(_bit(idx, t) == 0)[0]
                         hi = lo | (1 << t)
