@@ -62,10 +62,11 @@ enum DType : uint32_t {
   D_SWAP2 = 6,   // swap qubits on reg slots a and b
   D_PHASE1 = 7,  // multiply by d1 where bit set (S, T, phase) (4 DFMA/amp)
   // fused layer ops built by the round compiler (qt_plan.cpp)
-  D_MULTI = 8,   // a LAYER: [diag table if kOpTable][sign terms: base mask dl,
-                 // arg >> 16 conditional terms] then a complex 2x2 on every
-                 // reg slot in mask a, ascending slots
-  D_MULTIR = 9,  // the same with real rotations [[c,-s],[s,c]] (2 doubles per slot)
+  D_MULTI = 8,   // retired: complex layers are MULTIR layers with an lmask
+  D_MULTIR = 9,  // a LAYER: [diag table if kOpTable][sign terms: base mask dl,
+                 // arg >> 16 conditional terms][a real rotation [[c,-s],[s,c]]
+                 // (2 doubles) on every reg slot in mask a][a complex 2x2
+                 // (8 doubles) on every reg slot in lmask], ascending slots
   // (a lone diagonal table or sign op is a MULTIR layer with an empty mask)
   D_DTAB = 10,   // retired: was a separate table op
   D_STAB = 11,   // retired: was a separate sign-term op

@@ -250,7 +250,7 @@ struct LayerState {
   uint32_t post_slots = 0;  // register slots the post factors depend on
   cplx M[kMaxRegBits][4];
   uint32_t mmask = 0;
-  bool mreal = true;
+  uint32_t cmask = 0;  // slots of mmask holding complex 2x2s (the rest: real)
 
   explicit LayerState(int r) : R(r), NS(1 << r), pre(1 << r), post(1 << r) {
     for (auto& c : pre) c = cplx{1.0, 0.0};
@@ -322,7 +322,9 @@ void fold_signs(std::vector<cplx>& table, std::vector<SignTerm>& terms) {
 
 // Emits a layer as ONE device op (kernel k_layer): the layer's pre table,
 // its pre sign terms (unconditional ones as the base mask in dl, conditional
-// ones in the pool) and one 2x2 per register slot in L.mmask.
+// ones in the pool) and one 2x2 per register slot in L.mmask: rotations on
+// the real slots (mask in the variant's a field), then complex 2x2s on the
+// others (mask in lmask).
 void emit_layer(LayerState& L, EncRound& out) {
   DOp d{};
   const bool tab = !table_trivial(L.pre);
@@ -332,7 +334,8 @@ void emit_layer(LayerState& L, EncRound& out) {
     if (t.lcond == 0 && t.gcond == 0) base ^= t.slots;
     else cond.push_back(t);
   }
-  d.hdr = vid(L.mreal ? D_MULTIR : D_MULTI, static_cast<int>(L.mmask), -1, -1) |
+  const uint32_t rmask = L.mmask & ~L.cmask;
+  d.hdr = vid(D_MULTIR, static_cast<int>(rmask), -1, -1) |
           (tab ? kOpTable : 0u);
   d.dl = base;
   d.arg = static_cast<uint32_t>(out.pool.size()) | (static_cast<uint32_t>(cond.size()) << 16);
@@ -352,30 +355,28 @@ void emit_layer(LayerState& L, EncRound& out) {
   }
   for (int i = 0; i < L.R; ++i) {
     if (!(L.mmask & (1u << i))) continue;
-    if (L.mreal) {
-      // rotation form (to_rotations): [[c, -s], [s, c]] stored as (c, s)
+    // rotation form (to_rotations): [[c, -s], [s, c]] stored as (c, s)
+    if (rmask & (1u << i)) {
       out.pool.push_back(L.M[i][0].re);
       out.pool.push_back(L.M[i][2].re);
-    } else {
-      push_matrix(out.pool, L.M[i]);
     }
   }
+  for (int i = 0; i < L.R; ++i)
+    if (L.cmask & (1u << i)) push_matrix(out.pool, L.M[i]);
+  d.lmask = L.cmask;  // layers: the complex-slot mask (no control bits)
   out.ops.push_back(d);
   L.mmask = 0;
-  L.mreal = true;
+  L.cmask = 0;
 }
 
-// Emits the layer (pre part + 2x2s); the post part becomes the next
-// layer's pre part. QTB_NOLAYER=1 keeps table / signs / 2x2s as separate
-// dispatches (A/B measurements only).
-// Real layers are stored as rotations (2 doubles per slot, half the constant
+// Real slots are stored as rotations (2 doubles per slot, half the constant
 // loads): a real orthogonal 2x2 is a rotation [[c,-s],[s,c]] or a reflection
 // [[c,s],[s,-c]] = rotation . Z, whose Z joins the layer's (earlier-applied)
-// sign terms. Anything else makes the layer complex.
+// sign terms. Anything else makes that slot complex.
 void to_rotations(LayerState& L) {
-  if (!L.mmask || !L.mreal) return;
+  if (!L.mmask) return;
   for (int i = 0; i < L.R; ++i) {
-    if (!(L.mmask & (1u << i))) continue;
+    if (!(L.mmask & (1u << i)) || (L.cmask & (1u << i))) continue;
     const double m0 = L.M[i][0].re, m1 = L.M[i][1].re, m2 = L.M[i][2].re, m3 = L.M[i][3].re;
     if (m0 == m3 && m1 == -m2) continue;
     if (m0 == -m3 && m1 == m2) {
@@ -387,11 +388,15 @@ void to_rotations(LayerState& L) {
       L.M[i][3] = cplx{m0, 0.0};
       continue;
     }
-    L.mreal = false;
-    return;
+    L.cmask |= 1u << i;
   }
+  static const bool nomix = std::getenv("QTB_NOMIX") != nullptr;  // A/B only
+  if (nomix && L.cmask) L.cmask = L.mmask;
 }
 
+// Emits the layer (pre part + 2x2s); the post part becomes the next
+// layer's pre part. QTB_NOLAYER=1 keeps table / signs / 2x2s as separate
+// dispatches (A/B measurements only).
 void close_layer(LayerState& L, EncRound& out) {
   to_rotations(L);
   fold_signs(L.pre, L.pre_signs);
@@ -527,7 +532,8 @@ EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse) 
       }
       for (int k = 0; k < 4; ++k) L.M[a][k] = R2[k];
       L.mmask |= 1u << a;
-      L.mreal = L.mreal && real;
+      if (real) L.cmask &= ~(1u << a);
+      else L.cmask |= 1u << a;
       continue;
     }
     // ---- anything else: flush, then a single op --------------------------------
@@ -819,11 +825,9 @@ std::string plan_to_json(const Plan& p, bool detail) {
           case D_DENSE: fp += ctl ? 4.0 : 8.0; break;
           case D_REAL: case D_ANTI: fp += ctl ? 2.0 : 4.0; break;
           case D_DIAG: case D_PHASE1: case D_DTAB: fp += 4.0; break;
-          case D_MULTI:
-            fp += 8.0 * __builtin_popcount(a) + ((d.hdr & kOpTable) ? 4.0 : 0.0);
-            break;
-          case D_MULTIR:
-            fp += 4.0 * __builtin_popcount(a) + ((d.hdr & kOpTable) ? 4.0 : 0.0);
+          case D_MULTIR:  // a layer: rotations (a), complex 2x2s (lmask), table
+            fp += 4.0 * __builtin_popcount(a) + 8.0 * __builtin_popcount(d.lmask) +
+                  ((d.hdr & kOpTable) ? 4.0 : 0.0);
             break;
           default: break;
         }
@@ -889,7 +893,7 @@ std::string plan_to_json(const Plan& p, bool detail) {
             // layer: [..., [2x2 data], tabflag, [table], [[base,0,0], terms...]]
             const uint32_t nt = d.arg >> 16;
             const size_t toff = off, soff = off + (tab ? 2 * NS : 0), moff = soff + 2 * nt;
-            put(moff, (type == D_MULTI ? 8 : 2) * __builtin_popcount(a));
+            put(moff, 2 * __builtin_popcount(a) + 8 * __builtin_popcount(d.lmask));
             os << "]," << (tab ? 1 : 0) << ",[";
             if (tab) put(toff, 2 * NS);
             os << "],[[" << d.dl << ",0,0]";

@@ -237,7 +237,7 @@ __device__ __forceinline__ void apply_signs(double2 (&v)[1 << R], const P& p, in
 // slot bodies of a layer, slots A..R-1 (compile-time slot index, runtime mask)
 template <int R, int A, typename P>
 __device__ __forceinline__ void layer_rot(double2 (&v)[1 << R], const P& p, uint32_t mask,
-                                          int o) {
+                                          int& o) {
   if constexpr (A < R) {
     if (mask & (1u << A)) {
       // rotation [[c, -s], [s, c]] stored as (c, s)
@@ -251,7 +251,7 @@ __device__ __forceinline__ void layer_rot(double2 (&v)[1 << R], const P& p, uint
 
 template <int R, int A, typename P>
 __device__ __forceinline__ void layer_dense(double2 (&v)[1 << R], const P& p, uint32_t mask,
-                                            int o) {
+                                            int& o) {
   if constexpr (A < R) {
     if (mask & (1u << A)) {
       k_dense<R, A, -1>(v, p, o);
@@ -271,8 +271,8 @@ __device__ __forceinline__ void layer_dense(double2 (&v)[1 << R], const P& p, ui
 // one copy of each body keeps the hot loop inside the instruction cache.
 template <int R, typename P>
 __device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32_t hdr,
-                                        uint32_t arg, uint32_t base, uint32_t jb,
-                                        const uint64_t* sg) {
+                                        uint32_t arg, uint32_t base, uint32_t cmask,
+                                        uint32_t jb, const uint64_t* sg) {
   int o = static_cast<int>(arg & 0xffffu);
   const uint32_t nt = arg >> 16;
   if (hdr & kOpTable) {
@@ -283,9 +283,11 @@ __device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32
     apply_signs<R>(v, p, o, nt, base, jb, sg);
     o += 2 * static_cast<int>(nt);
   }
-  const uint32_t mask = (hdr >> 6) & 15u;
-  if (((hdr & kOpVariantMask) >> 10) == D_MULTIR) layer_rot<R, 0>(v, p, mask, o);
-  else layer_dense<R, 0>(v, p, mask, o);
+  const uint32_t rmask = (hdr >> 6) & 15u;
+  // (offsets advance slot by slot: no popcount, which would leave the
+  // uniform datapath and turn every constant load into a per-thread LDC)
+  if (rmask) layer_rot<R, 0>(v, p, rmask, o);
+  if (cmask) layer_dense<R, 0>(v, p, cmask, o);
 }
 
 // Applies one device op. `jb` = the thread's tile-local index with the
@@ -299,7 +301,7 @@ __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const
   const uint32_t type = (hdr & kOpVariantMask) >> 10;
   if (!GENERIC || type == D_MULTI || type == D_MULTIR) {
     // the fused layer ops (the only ones of the lean kernel) carry no flags
-    k_layer<R>(v, p, hdr, d.arg, d.dl, jb, sg);
+    k_layer<R>(v, p, hdr, d.arg, d.dl, d.lmask, jb, sg);
     return;
   }
   bool bit = false;

@@ -76,23 +76,27 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                         tab = np.array(op[10][0::2]) + 1j * np.array(op[10][1::2])
                         psi = psi * tab[slot]
                     psi = _signs(psi, op[11], slot, idx, tile)
+                    # rotations (c, s) on the slots in a, then complex 2x2s
+                    # on the slots in lmask (op[4])
+                    mats = []
                     k = 0
                     for sl in range(len(reg)):
-                        if not (a >> sl) & 1:
-                            continue
-                        if typ == D_MULTI:
-                            mm = np.array(data[8 * k:8 * k + 8])
-                            mm = mm[0::2] + 1j * mm[1::2]
-                        else:  # rotation (c, s): [[c, -s], [s, c]]
-                            c, sn = data[2 * k], data[2 * k + 1]
-                            mm = np.array([c, -sn, sn, c], dtype=np.complex128)
+                        if (a >> sl) & 1:
+                            c, sn = data[k], data[k + 1]
+                            mats.append((sl, np.array([c, -sn, sn, c], dtype=np.complex128)))
+                            k += 2
+                    for sl in range(len(reg)):
+                        if (lmask >> sl) & 1:
+                            mm = np.array(data[k:k + 8])
+                            mats.append((sl, mm[0::2] + 1j * mm[1::2]))
+                            k += 8
+                    for sl, mm in mats:
                         t = tile[reg[sl]]
                         lo = np.nonzero(_bit(idx, t) == 0)[0]
                         hi = lo | (1 << t)
                         x, y = psi[lo].copy(), psi[hi].copy()
                         psi[lo] = mm[0] * x + mm[1] * y
                         psi[hi] = mm[2] * x + mm[3] * y
-                        k += 1
                     continue
                 if typ == D_DTAB:
                     tab = np.array(data[0::2]) + 1j * np.array(data[1::2])
