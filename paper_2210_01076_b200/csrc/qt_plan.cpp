@@ -107,6 +107,113 @@ double op_fp64_per_amp(const LOp& op) {
   }
 }
 
+namespace {
+
+// min(|u00|, |u10|) for the diag . rotation . diag factorisation (QTB_ZYZ
+// overrides, for sweeps; > 1 disables it). Below it the phases would be
+// amplified by 1/s^2 (reconstruction error ~1e-16 / s^2).
+double zyz_min() {
+  static const double v = [] {
+    const char* e = std::getenv("QTB_ZYZ");
+    return e ? std::atof(e) : 0.05;
+  }();
+  return v;
+}
+
+inline cplx conjc(cplx a) { return cplx{a.re, -a.im}; }
+
+// Phase pushing (after fusion): single-qubit diagonal factors are carried
+// forward on their qubit -- they commute with everything that acts on it
+// diagonally (controls, CZ, other diagonals) -- and merged into the next
+// single-qubit X-role op there:
+//  * a dense U absorbs them (U' = U . D) and is split U' = diag(p0, p1) . V
+//    with V = [[c, u01'/p0], [s, u11'/p1]], c = |u00'|, s = |u10'| real >= 0
+//    (so the round compiler's ZYZ of V leaves no output phases); diag(p0, p1)
+//    is carried on;
+//  * an anti-diagonal op becomes a pure swap: [[0, a], [b, 0]] . D =
+//    diag(a d1, b d0) . X;
+//  * any other X-role use (a CX / controlled-U target, SWAP) and the end of
+//    the list flush the carried factor as one diagonal op.
+// So a layered circuit pays one diagonal table per rotation layer (the
+// rotations' input phases) instead of an extra one at every round end.
+void push_phases(std::vector<LOp>& ops, int nqubits) {
+  if (std::getenv("QTB_NOPUSH")) return;  // A/B measurements only
+  std::vector<LOp> out;
+  out.reserve(ops.size() + static_cast<size_t>(nqubits));
+  std::vector<cplx> d0(nqubits, cplx{1.0, 0.0}), d1(nqubits, cplx{1.0, 0.0});
+  std::vector<char> has(nqubits, 0);
+  auto flush = [&](int q, uint32_t gate) {
+    if (!has[q]) return;
+    has[q] = 0;
+    if (is_one(d0[q]) && is_one(d1[q])) return;
+    LOp f;
+    f.kind = LKind::Diag;
+    f.target = q;
+    f.m[0] = d0[q];
+    f.m[1] = cplx{0.0, 0.0};
+    f.m[2] = cplx{0.0, 0.0};
+    f.m[3] = d1[q];
+    f.gate = gate;
+    out.push_back(f);
+    d0[q] = d1[q] = cplx{1.0, 0.0};
+  };
+  const double th = zyz_min();
+  for (const LOp& op : ops) {
+    const int t = op.target;
+    if (op.control < 0 && op.kind == LKind::Diag) {
+      d0[t] = cmul(op.m[0], d0[t]);
+      d1[t] = cmul(op.m[3], d1[t]);
+      has[t] = 1;
+      continue;
+    }
+    if (op.control < 0 && op.kind == LKind::Anti) {
+      LOp x = op;
+      const cplx a = cmul(op.m[1], d1[t]), b = cmul(op.m[2], d0[t]);
+      x.m[1] = x.m[2] = cplx{1.0, 0.0};
+      out.push_back(x);
+      d0[t] = a;
+      d1[t] = b;
+      has[t] = 1;
+      continue;
+    }
+    if (op.control < 0 && op.kind == LKind::Dense) {
+      LOp u = op;
+      u.m[0] = cmul(op.m[0], d0[t]);
+      u.m[1] = cmul(op.m[1], d1[t]);
+      u.m[2] = cmul(op.m[2], d0[t]);
+      u.m[3] = cmul(op.m[3], d1[t]);
+      const double c = std::hypot(u.m[0].re, u.m[0].im);
+      const double sn = std::hypot(u.m[2].re, u.m[2].im);
+      if (c > th && sn > th) {
+        const cplx p0{u.m[0].re / c, u.m[0].im / c}, p1{u.m[2].re / sn, u.m[2].im / sn};
+        u.m[0] = cplx{c, 0.0};
+        u.m[1] = cmul(u.m[1], conjc(p0));
+        u.m[2] = cplx{sn, 0.0};
+        u.m[3] = cmul(u.m[3], conjc(p1));
+        d0[t] = p0;
+        d1[t] = p1;
+        has[t] = 1;
+      } else {
+        d0[t] = d1[t] = cplx{1.0, 0.0};
+        has[t] = 0;
+      }
+      reclassify(u);
+      out.push_back(u);
+      continue;
+    }
+    QR rl[3];
+    const int nr = roles(op, rl);
+    for (int k = 0; k < nr; ++k)
+      if (rl[k].r == XRole) flush(rl[k].q, op.gate);
+    out.push_back(op);
+  }
+  const uint32_t last = ops.empty() ? 0u : ops.back().gate;
+  for (int q = 0; q < nqubits; ++q) flush(q, last);
+  ops.swap(out);
+}
+
+}  // namespace
+
 void fuse_ops(std::vector<LOp>& ops, int nqubits) {
   std::vector<LOp> out;
   out.reserve(ops.size());
@@ -148,6 +255,7 @@ void fuse_ops(std::vector<LOp>& ops, int nqubits) {
     kept.push_back(op);
   }
   ops.swap(kept);
+  push_phases(ops, nqubits);
 }
 
 namespace {
@@ -231,16 +339,6 @@ void encode_single(const LOp& op, const std::vector<int>& tile_phys,
 // multiply or one integer sign flip.
 // ---------------------------------------------------------------------------
 namespace {
-
-// min(|u00|, |u10|) for the factorisation (QTB_ZYZ overrides, for sweeps;
-// > 1 disables it)
-double zyz_min() {
-  static const double v = [] {
-    const char* e = std::getenv("QTB_ZYZ");
-    return e ? std::atof(e) : 0.05;
-  }();
-  return v;
-}
 
 struct LayerState {
   int R, NS;

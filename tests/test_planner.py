@@ -81,16 +81,23 @@ def test_every_op_scheduled_once_and_tiles_bounded():
         seen.extend(ps["gates"])
     # every op lands in exactly one pass (an op is listed under the first
     # gate of its fused run: odd layers leave q0 / q19 without a CZ, so their
-    # consecutive U3s fuse)
-    assert len(seen) == len(set(seen)) == plan["ops"]
-    assert plan["ops"] == len(w.gates) - 2 * 2
+    # consecutive U3s fuse); the output phases carried forward by phase
+    # pushing are flushed once per qubit at the end as diagonal ops listed
+    # under the last gate
+    fused = len(w.gates) - 2 * 2
+    assert len(set(seen)) == fused
+    assert sum(ps["ops"] for ps in plan["passes"]) == plan["ops"]
+    assert fused < plan["ops"] <= fused + 20
 
 
 def test_fusion_merges_single_qubit_runs():
     g = gate_array([gate(K.Rz, 0, theta=0.3), gate(K.Ry, 0, theta=0.2),
                     gate(K.Rz, 0, theta=0.1), gate(K.H, 1)])
     plan = json.loads(plan_probe(4, g))
-    assert plan["ops"] == 2  # the three rotations on q0 are one 2x2
+    # the three rotations on q0 are one 2x2, whose output phase is carried
+    # forward (phase pushing) and flushed as one diagonal at the end; H's
+    # factorisation has no output phase
+    assert plan["ops"] == 3
 
 
 def test_deep_fusion_of_layered_circuit():
