@@ -110,17 +110,44 @@ double op_fp64_per_amp(const LOp& op) {
 namespace {
 
 // min(|u00|, |u10|) for the diag . rotation . diag factorisation (QTB_ZYZ
-// overrides, for sweeps; > 1 disables it). Below it the phases would be
-// amplified by 1/s^2 (reconstruction error ~1e-16 / s^2).
+// overrides, for sweeps; > 1 disables it). zyz_split is accurate for any
+// c, s > 0, the threshold only keeps clear of zero / subnormal divisions.
 double zyz_min() {
   static const double v = [] {
     const char* e = std::getenv("QTB_ZYZ");
-    return e ? std::atof(e) : 0.05;
+    return e ? std::atof(e) : 1e-100;
   }();
   return v;
 }
 
 inline cplx conjc(cplx a) { return cplx{a.re, -a.im}; }
+
+}  // namespace
+
+// U = diag(p0, p1) . [[c, -s], [s, c]] . diag(1, q1) with c = |u00|,
+// s = |u10| (u00 = p0 c, u01 = -p0 s q1, u10 = p1 s, u11 = p1 c q1).
+// p0, p1 are the normalised first column; q1 is taken from the LARGER of
+// u11 (c >= s: q1 = u11 conj(p1) / c) and u01 (c < s: q1 = -u01 conj(p0) / s),
+// so every reconstructed entry is within O(eps) of U for a unitary U (the
+// phase of a small column entry is ill-determined, but it only ever
+// multiplies that small magnitude). False when c or s is below zyz_min().
+bool zyz_split(const cplx* u, cplx& p0, cplx& p1, double& c, double& s, cplx& q1) {
+  c = std::hypot(u[0].re, u[0].im);
+  s = std::hypot(u[2].re, u[2].im);
+  if (!(c > zyz_min() && s > zyz_min())) return false;
+  p0 = cplx{u[0].re / c, u[0].im / c};
+  p1 = cplx{u[2].re / s, u[2].im / s};
+  if (c >= s) {
+    const cplx t = cmul(u[3], conjc(p1));
+    q1 = cplx{t.re / c, t.im / c};
+  } else {
+    const cplx t = cmul(u[1], conjc(p0));
+    q1 = cplx{-t.re / s, -t.im / s};
+  }
+  return true;
+}
+
+namespace {
 
 // Phase pushing (after fusion): single-qubit diagonal factors are carried
 // forward on their qubit -- they commute with everything that acts on it
@@ -157,7 +184,6 @@ void push_phases(std::vector<LOp>& ops, int nqubits) {
     out.push_back(f);
     d0[q] = d1[q] = cplx{1.0, 0.0};
   };
-  const double th = zyz_min();
   for (const LOp& op : ops) {
     const int t = op.target;
     if (op.control < 0 && op.kind == LKind::Diag) {
@@ -182,14 +208,14 @@ void push_phases(std::vector<LOp>& ops, int nqubits) {
       u.m[1] = cmul(op.m[1], d1[t]);
       u.m[2] = cmul(op.m[2], d0[t]);
       u.m[3] = cmul(op.m[3], d1[t]);
-      const double c = std::hypot(u.m[0].re, u.m[0].im);
-      const double sn = std::hypot(u.m[2].re, u.m[2].im);
-      if (c > th && sn > th) {
-        const cplx p0{u.m[0].re / c, u.m[0].im / c}, p1{u.m[2].re / sn, u.m[2].im / sn};
+      cplx p0, p1, q1;
+      double c, sn;
+      if (zyz_split(u.m, p0, p1, c, sn, q1)) {
+        // V = diag(p0, p1)^-1 U' = [[c, -s q1], [s, c q1]]
         u.m[0] = cplx{c, 0.0};
-        u.m[1] = cmul(u.m[1], conjc(p0));
+        u.m[1] = cplx{-sn * q1.re, -sn * q1.im};
         u.m[2] = cplx{sn, 0.0};
-        u.m[3] = cmul(u.m[3], conjc(p1));
+        u.m[3] = cplx{c * q1.re, c * q1.im};
         d0[t] = p0;
         d1[t] = p1;
         has[t] = 1;
@@ -602,17 +628,9 @@ EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse) 
       bool factored = false;
       bool real = type == D_REAL;
       if (!real) {
-        const double c = std::hypot(op.m[0].re, op.m[0].im);
-        const double sn = std::hypot(op.m[2].re, op.m[2].im);
-        if (c > zyz_min() && sn > zyz_min()) {
+        double c, sn;
+        if (zyz_split(op.m, p0, p1, c, sn, d1)) {
           // U = diag(p0, p1) . [[c, -s], [s, c]] . diag(1, q1)
-          p0 = cplx{op.m[0].re / c, op.m[0].im / c};
-          p1 = cplx{op.m[2].re / sn, op.m[2].im / sn};
-          // q1 = -u01 / (p0 s) = -u01 conj(p0) / s   (|p0| = 1)
-          const cplx u01 = op.m[1];
-          const cplx pc = {p0.re, -p0.im};
-          const cplx t = cmul(u01, pc);
-          d1 = cplx{-t.re / sn, -t.im / sn};
           R2[0] = {c, 0.0};
           R2[1] = {-sn, 0.0};
           R2[2] = {sn, 0.0};

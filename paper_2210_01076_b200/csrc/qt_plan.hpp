@@ -19,8 +19,13 @@ struct PlanOptions {
 
 // Merges runs of uncontrolled single-qubit ops on the same qubit into one
 // 2x2 (matrix product) and drops exact identities. Order-preserving:
-// an op merges into the latest op touching its qubit only.
+// an op merges into the latest op touching its qubit only. Then pushes
+// single-qubit diagonal factors forward into the next single-qubit op on
+// their qubit (qt_plan.cpp push_phases).
 void fuse_ops(std::vector<LOp>& ops, int nqubits);
+// U = diag(p0, p1) . [[c, -s], [s, c]] . diag(1, q1) (qt_plan.cpp); false when
+// c or s is ~0 (U diagonal or anti-diagonal).
+bool zyz_split(const cplx* u, cplx& p0, cplx& p1, double& c, double& s, cplx& q1);
 
 // Plans `ops` (logical qubits) for a state of nqubits bits of which the top
 // nqubits - nlocal are sharded (global). perm maps logical -> physical and

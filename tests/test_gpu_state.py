@@ -184,3 +184,24 @@ def test_deterministic_bits(gpu):
     a, _ = run_gpu(18, g)
     b, _ = run_gpu(18, g)
     assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-9])
+def test_near_diagonal_u3_layers(gpu, eps):
+    """Near-diagonal / near-anti-diagonal U3 layers (the ZYZ split's hard
+    cases) at 12 qubits on the GPU vs the oracle."""
+    rng = np.random.default_rng(11)
+    n = 12
+    rows = []
+    for layer in range(10):
+        for q in range(n):
+            th = eps if (q + layer) % 2 else math.pi - eps
+            rows.append(gate(K.U3, q, -1, th, *rng.uniform(0, 2 * math.pi, 2)))
+        for a in range(layer % 2, n - 1, 2):
+            rows.append(gate(K.Cz, a + 1, a))
+    g = gate_array(rows)
+    psi0 = random_state(rng, n)
+    want = oracle.simulate(n, lower_to_reference(g), state=psi0.copy())
+    got, nrm = run_gpu(n, g, psi0)
+    assert np.abs(got - want).max() < TOL
+    assert abs(nrm - 1.0) < NORM_TOL

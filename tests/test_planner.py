@@ -4,6 +4,7 @@ The detailed plan (qt_plan_probe_ex) is replayed by tests/emulator.py, an
 independent numpy interpretation of every encoded op, and compared with the
 dense oracle (oracle/, the restatement of oracle.cpp:15-50)."""
 import json
+import math
 
 import numpy as np
 import pytest
@@ -11,7 +12,7 @@ import pytest
 import oracle
 from paper_2210_01076_b200 import plan_probe, workloads as W
 from paper_2210_01076_b200.gates import GateKind as K
-from paper_2210_01076_b200.gates import gate, gate_array
+from paper_2210_01076_b200.gates import gate, gate_array, lower_to_reference
 from tests.emulator import apply_plan, logical_view
 
 ALL = list(K)
@@ -108,3 +109,27 @@ def test_deep_fusion_of_layered_circuit():
     tiles = [p for p in plan["passes"] if p["kind"] == "tile"]
     assert len(tiles) < len(w.gates) / 20
     assert sum(p["ops"] for p in tiles) == plan["ops"]
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-7, 1e-12])
+def test_near_diagonal_and_antidiagonal_factorisation(eps):
+    """U3s within eps of diagonal / anti-diagonal (|u10| or |u00| ~ eps) go
+    through the diag . rotation . diag split and phase pushing; the split
+    takes q1 from the larger column entry, so the replay stays at rounding
+    level for any eps (qt_plan.cpp zyz_split)."""
+    rng = np.random.default_rng(7)
+    n = 6
+    rows = []
+    for layer in range(8):
+        for q in range(n):
+            th = eps if (q + layer) % 2 else math.pi - eps
+            rows.append(gate(K.U3, q, -1, th, *rng.uniform(0, 2 * math.pi, 2)))
+        for a in range(layer % 2, n - 1, 2):
+            rows.append(gate(K.Cz, a + 1, a))
+    g = gate_array(rows)
+    psi0 = random_state(rng, n)
+    want = oracle.simulate(n, lower_to_reference(g), state=psi0.copy())
+    for tq in (0, 4):
+        plan = json.loads(plan_probe(n, g, tile_qubits=tq, detail=True))
+        got = apply_plan(psi0, plan)
+        assert np.abs(got - want).max() < 1e-13
