@@ -603,20 +603,28 @@ EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse) 
         else if (pl.tile(op.control) >= 0) t.lcond |= 1u << pl.tile(op.control);
         else t.gcond |= 1ull << op.control;
       }
-      L.post_signs.push_back(t);
-      L.post_slots |= deps;
+      // a term on slots without a 2x2 in the open layer commutes with that
+      // layer's 2x2s: it joins the layer's pre part, so the layer stays open
+      // for later 2x2s on those slots
+      if (deps & L.mmask) {
+        L.post_signs.push_back(t);
+        L.post_slots |= deps;
+      } else {
+        L.pre_signs.push_back(t);
+      }
       continue;
     }
     // ---- diagonal ops living on register slots: one table ----------------------
     if (type == D_DIAG || type == D_PHASE1) {
       const int tslot = pl.slot(op.target);
       if (tslot >= 0 && (op.control < 0 || cslot >= 0)) {
+        const uint32_t deps = (1u << tslot) | (cslot >= 0 ? 1u << cslot : 0u);
+        std::vector<cplx>& tab = (deps & L.mmask) ? L.post : L.pre;  // as for signs
         for (int s = 0; s < L.NS; ++s) {
           if (op.control >= 0 && !bit_of(s, cslot)) continue;
-          L.post[s] = cmul(L.post[s], bit_of(s, tslot) ? op.m[3] : op.m[0]);
+          tab[s] = cmul(tab[s], bit_of(s, tslot) ? op.m[3] : op.m[0]);
         }
-        L.post_slots |= 1u << tslot;
-        if (cslot >= 0) L.post_slots |= 1u << cslot;
+        if (deps & L.mmask) L.post_slots |= deps;
         continue;
       }
     }
@@ -663,69 +671,125 @@ EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse) 
 
 namespace {
 
+// One greedy register round over `remaining` (application order, with
+// hoisting): an op joins when it commutes with every skipped op on its
+// qubits and its X-role qubits are (or, without `preset`, can still become)
+// register bits. Returns the number of X-role ops scheduled.
+int greedy_round(const PlanPass& pass, const std::vector<int>& remaining, int R,
+                 const std::vector<int>& tix, const std::vector<int>* preset,
+                 const PlanOptions& opt, PlanRound& round, std::vector<int>& rest) {
+  const int k = static_cast<int>(pass.tile_phys.size());
+  const int nphys = static_cast<int>(tix.size());
+  std::vector<char> blockAll(nphys, 0), blockX(nphys, 0), inReg(k, 0);
+  round = PlanRound{};
+  rest.clear();
+  if (preset) {
+    round.reg = *preset;
+    for (int ti : *preset) inReg[ti] = 1;
+  }
+  int xops = 0;
+  QR rl[3];
+  for (int idx : remaining) {
+    const LOp& op = pass.ops[idx];
+    const int nr = roles(op, rl);
+    bool can = static_cast<int>(round.ops.size()) < opt.max_round_ops;
+    for (int t = 0; t < nr && can; ++t) {
+      if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
+    }
+    bool isx = false;
+    if (can) {
+      int need[2], nn = 0;
+      for (int t = 0; t < nr; ++t) {
+        if (rl[t].r != XRole) continue;
+        isx = true;
+        const int ti = tix[rl[t].q];
+        if (!inReg[ti]) {
+          bool dup = false;
+          for (int u = 0; u < nn; ++u) dup = dup || need[u] == ti;
+          if (!dup) need[nn++] = ti;
+        }
+      }
+      if (nn == 0 || (!preset && static_cast<int>(round.reg.size()) + nn <= R)) {
+        for (int u = 0; u < nn; ++u) {
+          inReg[need[u]] = 1;
+          round.reg.push_back(need[u]);
+        }
+        round.ops.push_back(idx);
+        xops += isx ? 1 : 0;
+      } else {
+        can = false;
+      }
+    }
+    if (!can) {
+      rest.push_back(idx);
+      for (int t = 0; t < nr; ++t) {
+        if (rl[t].r == XRole) blockAll[rl[t].q] = 1;
+        else blockX[rl[t].q] = 1;
+      }
+    }
+  }
+  // pad the register set with the highest unused tile bits
+  for (int ti = k - 1; static_cast<int>(round.reg.size()) < R && ti >= 0; --ti) {
+    if (!inReg[ti]) {
+      inReg[ti] = 1;
+      round.reg.push_back(ti);
+    }
+  }
+  return xops;
+}
+
 // Splits the ops of one pass (physical qubits, application order) into
-// register rounds of R tile bits, then device-encodes every round.
+// register rounds of R tile bits, then device-encodes every round. Each
+// round's register set is chosen among the first few tile bits that still
+// have X-role ops: every R-subset is tried and the one that schedules the
+// most X-role ops wins (ties: the plain first-need greedy), so rounds hold
+// full layers instead of whatever the op order reaches first.
 void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt) {
   const int k = static_cast<int>(pass.tile_phys.size());
   std::vector<int> tix(nphys, -1);
   for (int i = 0; i < k; ++i) tix[pass.tile_phys[i]] = i;
   std::vector<int> remaining(pass.ops.size());
   for (size_t i = 0; i < remaining.size(); ++i) remaining[i] = static_cast<int>(i);
-  std::vector<char> blockAll(nphys), blockX(nphys);
-  std::vector<char> inReg(k);
+  static const int kCand = [] {
+    const char* e = std::getenv("QTB_ROUND_CAND");  // tuning only; <= R: plain greedy
+    return e ? std::atoi(e) : 8;
+  }();
+  PlanRound best, trial;
+  std::vector<int> best_rest, trial_rest;
+  QR rl[3];
   while (!remaining.empty()) {
-    std::fill(blockAll.begin(), blockAll.end(), 0);
-    std::fill(blockX.begin(), blockX.end(), 0);
-    std::fill(inReg.begin(), inReg.end(), 0);
-    PlanRound round;
-    std::vector<int> rest;
-    QR rl[3];
+    int best_x = greedy_round(pass, remaining, R, tix, nullptr, opt, best, best_rest);
+    // candidate register bits: tile bits with X-role ops, in first-need order
+    std::vector<int> cand;
     for (int idx : remaining) {
-      const LOp& op = pass.ops[idx];
-      const int nr = roles(op, rl);
-      bool can = static_cast<int>(round.ops.size()) < opt.max_round_ops;
-      for (int t = 0; t < nr && can; ++t) {
-        if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
+      const int nr = roles(pass.ops[idx], rl);
+      for (int t = 0; t < nr; ++t) {
+        if (rl[t].r != XRole) continue;
+        const int ti = tix[rl[t].q];
+        if (std::find(cand.begin(), cand.end(), ti) == cand.end()) cand.push_back(ti);
       }
-      if (can) {
-        int need[2], nn = 0;
-        for (int t = 0; t < nr; ++t) {
-          if (rl[t].r != XRole) continue;
-          const int ti = tix[rl[t].q];
-          if (!inReg[ti]) {
-            bool dup = false;
-            for (int u = 0; u < nn; ++u) dup = dup || need[u] == ti;
-            if (!dup) need[nn++] = ti;
-          }
-        }
-        if (static_cast<int>(round.reg.size()) + nn <= R) {
-          for (int u = 0; u < nn; ++u) {
-            inReg[need[u]] = 1;
-            round.reg.push_back(need[u]);
-          }
-          round.ops.push_back(idx);
-        } else {
-          can = false;
-        }
-      }
-      if (!can) {
-        rest.push_back(idx);
-        for (int t = 0; t < nr; ++t) {
-          if (rl[t].r == XRole) blockAll[rl[t].q] = 1;
-          else blockX[rl[t].q] = 1;
+      if (static_cast<int>(cand.size()) >= kCand) break;
+    }
+    const int m = static_cast<int>(cand.size());
+    if (m > R && R <= 4) {
+      std::vector<int> pick(R);
+      // all R-subsets of cand (m <= 8: at most 70)
+      for (uint32_t bits = 0; bits < (1u << m); ++bits) {
+        if (__builtin_popcount(bits) != R) continue;
+        int j = 0;
+        for (int i = 0; i < m; ++i)
+          if ((bits >> i) & 1u) pick[j++] = cand[i];
+        const int x = greedy_round(pass, remaining, R, tix, &pick, opt, trial, trial_rest);
+        if (x > best_x) {
+          best_x = x;
+          std::swap(best, trial);
+          std::swap(best_rest, trial_rest);
         }
       }
     }
-    // pad the register set with the highest unused tile bits
-    for (int ti = k - 1; static_cast<int>(round.reg.size()) < R && ti >= 0; --ti) {
-      if (!inReg[ti]) {
-        inReg[ti] = 1;
-        round.reg.push_back(ti);
-      }
-    }
-    round.enc = compile_round(pass, round, opt.fuse_layers);
-    pass.rounds.push_back(std::move(round));
-    remaining.swap(rest);
+    best.enc = compile_round(pass, best, opt.fuse_layers);
+    pass.rounds.push_back(std::move(best));
+    remaining.swap(best_rest);
   }
 }
 
