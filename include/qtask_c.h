@@ -43,6 +43,8 @@ extern "C" {
 #define QT_ERR_STALE_STATE (-7)      /* qtask::StaleStateError            */
 #define QT_ERR_NUMERIC (-8)          /* qtask::NumericError               */
 #define QT_ERR_SUPERPOSITION (-9)    /* qtask::SuperpositionGateError     */
+#define QT_ERR_QASM_PARSE (-10)      /* qtask::qasm::ParseError           */
+#define QT_ERR_QASM_UNSUPPORTED (-11) /* qtask::qasm::UnsupportedGateError */
 #define QT_ERR_CUDA (-20)            /* CUDA runtime failure              */
 #define QT_ERR_OOM (-21)             /* device allocation failed          */
 #define QT_ERR_NCCL (-22)            /* NCCL failure                      */
@@ -214,6 +216,33 @@ int qt_sim_gate_info(const qt_sim* sim, uint32_t gate, qt_gate* out,
                      uint32_t* net);
 int qt_sim_export_gates(const qt_sim* sim, qt_gate* out, size_t cap,
                         size_t* count);
+
+/* ---- OpenQASM 2.0 front end (reference qasm.hpp:11-66, qasm.cpp:34-426) --
+ * Same accepted subset, errors (line / column of the offending token) and
+ * ASAP levelling as the reference; implementation: include/qtask/qasm.hpp. */
+typedef struct qt_qasm_stmt {
+  int32_t kind;      /* 0 gate, 1 barrier */
+  int32_t gate;      /* qt_gate_kind (gates only) */
+  double theta;      /* rx / ry / rz angle */
+  int32_t has_theta;
+  int32_t nqubits;   /* operands: cx = control, target; swap = target, control */
+  int32_t qubits[2];
+  int32_t line, column;
+  int32_t level;     /* ASAP level (levelize), -1 for barriers */
+  int32_t reserved;
+} qt_qasm_stmt;
+
+/* Parses `len` bytes of QASM text. On success *count statements (up to cap
+ * are written; call with cap 0 to size), *num_qubits the qreg size. On
+ * QT_ERR_QASM_PARSE / QT_ERR_QASM_UNSUPPORTED, *err_line / *err_col locate
+ * the offending token. */
+int qt_qasm_parse(const char* text, size_t len, qt_qasm_stmt* out, size_t cap,
+                  size_t* count, uint32_t* num_qubits, int* err_line,
+                  int* err_col);
+/* build_circuit (qasm.cpp:407-426): parses `text` and appends one net per ASAP
+ * level to `sim` (qt_sim_create'd with at least the qreg size). */
+int qt_qasm_build(qt_sim* sim, const char* text, size_t len, int* err_line,
+                  int* err_col);
 
 #ifdef __cplusplus
 }

@@ -99,8 +99,38 @@ def ref_lib():
         lib.ref_sim_norm.argtypes = [ctypes.c_void_p]
         lib.ref_sim_norm.restype = ctypes.c_double
         lib.ref_sim_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.ref_qasm_parse.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p,
+                                       ctypes.c_void_p, ctypes.c_size_t,
+                                       ctypes.POINTER(ctypes.c_uint32),
+                                       ctypes.POINTER(ctypes.c_int),
+                                       ctypes.POINTER(ctypes.c_int)]
+        lib.ref_qasm_parse.restype = ctypes.c_int64
+        lib.ref_qasm_build.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]
+        lib.ref_qasm_build.restype = ctypes.c_int
         _ref = lib
     return _ref
+
+
+def ref_qasm_parse(text: str):
+    """The reference parser (qasm.cpp:34-405) on ``text``: ("ok", num_qubits,
+    rows, levels) with rows = [kind, gate, theta, has_theta, q0, q1, line,
+    column] per statement, or ("parse" | "unsupported", line, column)."""
+    lib = ref_lib()
+    data = text.encode("utf-8")
+    cap = max(1, data.count(b";") + 1)
+    rows = np.zeros((cap, 8), dtype=np.float64)
+    levels = np.zeros(cap, dtype=np.int32)
+    nq = ctypes.c_uint32(0)
+    line, col = ctypes.c_int(0), ctypes.c_int(0)
+    n = lib.ref_qasm_parse(data, len(data), rows.ctypes.data, levels.ctypes.data, cap,
+                           ctypes.byref(nq), ctypes.byref(line), ctypes.byref(col))
+    if n == -1:
+        return ("parse", line.value, col.value)
+    if n == -2:
+        return ("unsupported", line.value, col.value)
+    if n < 0:
+        raise ValueError("reference qasm parser failed")
+    return ("ok", nq.value, rows[:n], levels[:n])
 
 
 def _gates_arg(gates: np.ndarray):
@@ -214,6 +244,11 @@ class RefSimulator:
 
     def norm_squared(self):
         return self.lib.ref_sim_norm(self.h)
+
+    def qasm_build(self, text: str):
+        """qtask::qasm::build_circuit(parse(text)) on this handle."""
+        data = text.encode("utf-8")
+        self._chk(self.lib.ref_qasm_build(self.h, data, len(data)))
 
     def stats(self):
         out = np.zeros(4, dtype=np.uint64)

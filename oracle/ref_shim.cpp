@@ -9,6 +9,9 @@
 //   * ref_sim_*           -> qtask::Simulator (engine.hpp:46-100): the
 //                            reference's incremental engine, driven through
 //                            its public modifier / update / readout API
+//   * ref_qasm_parse      -> qtask::qasm::parse + levelize (qasm.cpp:34-405)
+//   * ref_qasm_build      -> qtask::qasm::build_circuit (qasm.cpp:407-426)
+//                            into a ref_sim handle
 // so tests can pin oracle/qt_oracle.c against the reference and bench.py's
 // reference arm can time the reference's own CPU implementation.
 //
@@ -22,6 +25,7 @@
 
 #include "qtask/engine.hpp"
 #include "qtask/oracle.hpp"
+#include "qtask/qasm.hpp"
 
 namespace {
 
@@ -223,6 +227,59 @@ void ref_sim_stats(void* s, uint64_t* out4) {
   out4[1] = st.executed_partitions;
   out4[2] = st.materialized_blocks;
   out4[3] = st.rewritten_amplitudes;
+}
+
+// ---- the reference OpenQASM front end -------------------------------------
+
+// Flattened statements, 8 doubles each: [kind (0 gate, 1 barrier), gate,
+// theta, has_theta, q0, q1 (-1 if absent), line, column] plus, in `levels`,
+// each statement's ASAP level (-1 for barriers). Returns the statement count,
+// or -1 (ParseError) / -2 (UnsupportedGateError) with *line / *col set, or
+// -3 for any other failure. *nq = qreg size.
+int64_t ref_qasm_parse(const char* text, size_t len, double* out, int32_t* levels,
+                       size_t cap, uint32_t* nq, int* line, int* col) {
+  try {
+    const auto p = qtask::qasm::parse(std::string_view(text, len));
+    const auto lv = qtask::qasm::levelize(p);
+    std::vector<int32_t> level(p.statements.size(), -1);
+    for (size_t l = 0; l < lv.size(); ++l)
+      for (size_t i : lv[l]) level[i] = static_cast<int32_t>(l);
+    *nq = static_cast<uint32_t>(p.num_qubits);
+    for (size_t i = 0; i < p.statements.size() && i < cap; ++i) {
+      const auto& st = p.statements[i];
+      double* r = out + 8 * i;
+      r[0] = st.kind == qtask::qasm::Statement::Kind::Barrier ? 1 : 0;
+      r[1] = static_cast<double>(static_cast<int>(st.gate));
+      r[2] = st.theta;
+      r[3] = st.has_theta ? 1 : 0;
+      r[4] = st.qubits.size() > 0 ? st.qubits[0] : -1;
+      r[5] = st.qubits.size() > 1 ? st.qubits[1] : -1;
+      r[6] = st.line;
+      r[7] = st.column;
+      levels[i] = level[i];
+    }
+    return static_cast<int64_t>(p.statements.size());
+  } catch (const qtask::qasm::ParseError& e) {
+    *line = e.line();
+    *col = e.column();
+    return -1;
+  } catch (const qtask::qasm::UnsupportedGateError& e) {
+    *line = e.line();
+    *col = e.column();
+    return -2;
+  } catch (...) {
+    return -3;
+  }
+}
+
+int ref_qasm_build(void* s, const char* text, size_t len) {
+  try {
+    qtask::qasm::build_circuit(*static_cast<qtask::Simulator*>(s),
+                               qtask::qasm::parse(std::string_view(text, len)));
+    return 0;
+  } catch (const std::exception& e) {
+    return error_code(e);
+  }
 }
 
 }  // extern "C"

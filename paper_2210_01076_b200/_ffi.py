@@ -61,7 +61,7 @@ HEADER_SYMBOLS = [
     "qt_sim_remove_gate", "qt_sim_update_state", "qt_sim_pending", "qt_sim_amplitude",
     "qt_sim_amplitudes", "qt_sim_norm_squared", "qt_sim_last_update",
     "qt_sim_num_gates", "qt_sim_num_nets", "qt_sim_net_order", "qt_sim_net_gates",
-    "qt_sim_gate_info", "qt_sim_export_gates",
+    "qt_sim_gate_info", "qt_sim_export_gates", "qt_qasm_parse", "qt_qasm_build",
 ]
 
 _lib = None
@@ -123,6 +123,11 @@ _SIGS = {
                          _c.c_int),
     "qt_sim_gate_info": ([_vp, _c.c_uint32, _vp, _c.POINTER(_c.c_uint32)], _c.c_int),
     "qt_sim_export_gates": ([_vp, _vp, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
+    "qt_qasm_parse": ([_c.c_char_p, _c.c_size_t, _vp, _c.c_size_t, _c.POINTER(_c.c_size_t),
+                       _c.POINTER(_c.c_uint32), _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)],
+                      _c.c_int),
+    "qt_qasm_build": ([_vp, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_int),
+                       _c.POINTER(_c.c_int)], _c.c_int),
 }
 
 

@@ -16,6 +16,7 @@
 #include "qt_sim.hpp"
 #include "qt_state.hpp"
 #include "qtask_c.h"
+#include "qtask/qasm.hpp"
 
 struct qt_state {
   qtb::State* s;
@@ -374,6 +375,99 @@ int qt_sim_export_gates(const qt_sim* sim, qt_gate* outp, size_t cap, size_t* co
     if (count) *count = gs.size();
     for (size_t i = 0; i < gs.size() && i < cap && outp; ++i) outp[i] = gs[i];
   });
+}
+
+}  // extern "C"
+
+// ---- OpenQASM 2.0 front end ---------------------------------------------------
+
+namespace {
+template <typename F>
+int qasm_guard(int* err_line, int* err_col, F&& f) {
+  try {
+    f();
+    return QT_OK;
+  } catch (const qtask::qasm::ParseError& e) {
+    if (err_line) *err_line = e.line();
+    if (err_col) *err_col = e.column();
+    g_err = e.what();
+    return QT_ERR_QASM_PARSE;
+  } catch (const qtask::qasm::UnsupportedGateError& e) {
+    if (err_line) *err_line = e.line();
+    if (err_col) *err_col = e.column();
+    g_err = e.what();
+    return QT_ERR_QASM_UNSUPPORTED;
+  } catch (const qtask::Error& e) {  // the drop-in wrapper's mapped error
+    g_err = e.what();
+    return QT_ERR_ARG;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int qt_qasm_parse(const char* text, size_t len, qt_qasm_stmt* outp, size_t cap,
+                  size_t* count, uint32_t* num_qubits, int* err_line, int* err_col) {
+  if (!text && len) return null_arg();
+  int rc = QT_OK;
+  const int g = guard([&] {
+    rc = qasm_guard(err_line, err_col, [&] {
+      const qtask::qasm::QasmProgram prog =
+          qtask::qasm::parse(std::string_view(text ? text : "", len));
+      std::vector<int> level(prog.statements.size(), -1);
+      const auto levels = qtask::qasm::levelize(prog);
+      for (size_t l = 0; l < levels.size(); ++l)
+        for (size_t i : levels[l]) level[i] = static_cast<int>(l);
+      if (count) *count = prog.statements.size();
+      if (num_qubits) *num_qubits = static_cast<uint32_t>(prog.num_qubits);
+      for (size_t i = 0; i < prog.statements.size() && i < cap && outp; ++i) {
+        const auto& st = prog.statements[i];
+        qt_qasm_stmt r{};
+        r.kind = st.kind == qtask::qasm::Statement::Kind::Barrier ? 1 : 0;
+        r.gate = static_cast<int32_t>(st.gate);
+        r.theta = st.theta;
+        r.has_theta = st.has_theta ? 1 : 0;
+        r.nqubits = static_cast<int32_t>(st.qubits.size());
+        for (size_t k = 0; k < st.qubits.size() && k < 2; ++k) r.qubits[k] = st.qubits[k];
+        r.line = st.line;
+        r.column = st.column;
+        r.level = level[i];
+        outp[i] = r;
+      }
+    });
+  });
+  return g != QT_OK ? g : rc;
+}
+
+int qt_qasm_build(qt_sim* sim, const char* text, size_t len, int* err_line, int* err_col) {
+  if (!sim || (!text && len)) return null_arg();
+  int rc = QT_OK;
+  const int g = guard([&] {
+    rc = qasm_guard(err_line, err_col, [&] {
+      const qtask::qasm::QasmProgram prog =
+          qtask::qasm::parse(std::string_view(text ? text : "", len));
+      // build_circuit (qasm.cpp:407-426) through this handle's modifier calls
+      for (const auto& lv : qtask::qasm::levelize(prog)) {
+        uint32_t net = 0;
+        qtask::detail::check(qt_sim_insert_net_back(sim, &net));
+        for (size_t i : lv) {
+          const auto& st = prog.statements[i];
+          uint32_t gid = 0;
+          const double th[3] = {st.theta, 0.0, 0.0};
+          int t = st.qubits[0], c = -1;
+          if (st.gate == qtask::GateKind::Cnot) {
+            t = st.qubits[1];
+            c = st.qubits[0];
+          } else if (st.gate == qtask::GateKind::Swap) {
+            c = st.qubits[1];
+          }
+          qtask::detail::check(qt_sim_insert_gate(sim, static_cast<int>(st.gate),
+                                                  st.has_theta ? th : nullptr, net, t, c, &gid));
+        }
+      }
+    });
+  });
+  return g != QT_OK ? g : rc;
 }
 
 }  // extern "C"

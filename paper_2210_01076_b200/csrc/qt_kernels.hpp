@@ -51,6 +51,9 @@ cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool g
                              cudaStream_t s);
 cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
                              cudaStream_t s);
+// Max threads per CTA of the tile-pass kernel for R register bits (its
+// launch bounds): a pass's tile has at most R + log2(this) bits.
+constexpr int tile_max_threads(int R) { return R >= 4 ? 256 : 512; }
 // Max resident CTAs per SM of the tile-pass kernel for (k, R).
 int tile_pass_occupancy(int k, int R, bool large, bool generic);
 

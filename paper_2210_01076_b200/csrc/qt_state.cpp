@@ -66,6 +66,12 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   // tuning overrides (benchmark sweeps only)
   if (const char* e = std::getenv("QTB_REG_BITS")) opt_.reg_bits = std::max(1, std::min(kMaxRegBits, std::atoi(e)));
   if (const char* e = std::getenv("QTB_TILE_BITS")) opt_.tile_bits = std::max(2, std::min(kMaxTileBits, std::atoi(e)));
+  // a tile's non-register bits index the CTA's threads (launch bounds)
+  {
+    int tb = 0;
+    while ((2 << tb) <= tile_max_threads(opt_.reg_bits)) ++tb;
+    opt_.tile_bits = std::min(opt_.tile_bits, opt_.reg_bits + tb);
+  }
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
 
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");

@@ -319,17 +319,15 @@ __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const
 #include "qt_variants.inc"
 }
 
-// R = 3: 8 amplitudes per thread in registers, 256 threads per 2^11 tile;
-// R = 4: 16 amplitudes per thread, 256 threads per 2^12 tile (<= 128 regs,
-// 2 CTAs per SM). The kernel is latency-bound at low occupancy, so the R = 3
-// minimum-blocks bound trades registers for resident warps.
-#ifndef QT_R3_MINB
-#define QT_R3_MINB 4
-#endif
+// R = 3: 8 amplitudes per thread in registers, up to 512 threads (2^12
+// tiles) at <= 64 registers (32 warps per SM); R = 4: 16 amplitudes per
+// thread, up to 256 threads (2^12 tiles) at <= 128 registers. The kernel is
+// latency-bound at low occupancy, so the R = 3 bound trades registers for
+// resident warps. kTileMaxThreads (qt_kernels.hpp) must match.
 template <int R>
-constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? QT_R3_MINB : 4);
+constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? 2 : 4);
 template <int R>
-constexpr int kMaxThreads = R >= 3 ? 256 : 512;
+constexpr int kMaxThreads = R >= 4 ? 256 : 512;
 
 // GENERIC = false: the lean instantiation that only knows the fused layer
 // ops (MULTI / MULTIR / DTAB / STAB); every extra variant body costs

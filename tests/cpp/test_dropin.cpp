@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "qtask/engine.hpp"
+#include "qtask/qasm.hpp"
 
 extern "C" int qo_apply(int n, double* state, const void* gates, size_t count, int threads);
 
@@ -247,6 +248,40 @@ int main() {
            std::memcmp(res[0].data(), res[2].data(), bytes) == 0;
     }
     report("criterion 7: amplitudes bit-identical across runs / thread settings", ok);
+  }
+  {
+    // OpenQASM front end (qtask/qasm.hpp): the reference's test_qasm.cpp checks
+    const std::string src =
+        "// GHZ-like\nOPENQASM 2.0;\ninclude \"qelib1.inc\";\nqreg q[3];\ncreg c[3];\n"
+        "h q[0];\ncx q[0],q[1];\nbarrier q;\ncx q[1],q[2];\nrz(-pi/2) q[2];\n";
+    const qasm::QasmProgram p = qasm::parse(src);
+    bool ok = p.num_qubits == 3 && p.statements.size() == 5 &&
+              p.statements[1].qubits == std::vector<int>{0, 1} &&
+              std::abs(p.statements[4].theta + M_PI / 2) < 1e-15;
+    const auto lv = qasm::levelize(p);
+    ok = ok && lv.size() == 4 && lv[0].size() == 1 && lv[3].size() == 1;
+    const qasm::QasmProgram q = qasm::parse(qasm::to_qasm(p));
+    ok = ok && q.statements.size() == p.statements.size() && q.statements[4].theta == p.statements[4].theta;
+    report("qasm: parse / levelize / round trip", ok);
+    int line = 0;
+    try {
+      qasm::parse("OPENQASM 2.0;\nqreg q[2];\nh q[5];\n");
+    } catch (const qasm::ParseError& e) {
+      line = e.line();
+    }
+    report("qasm: errors carry the line",
+           line == 3 && throws<qasm::UnsupportedGateError>([&] {
+             qasm::parse("OPENQASM 2.0;\nqreg q[3];\nccx q[0],q[1],q[2];\n");
+           }) && throws<qasm::ParseError>([&] { qasm::parse("OPENQASM 3.0;\nqreg q[1];\n"); }));
+    Simulator sim(3);
+    qasm::build_circuit(sim, p);
+    sim.update_state();
+    // (|000> + |111>)/sqrt(2) with RZ(-pi/2) on q2: e^{+i pi/4} on |000>, e^{-i pi/4} on |111>
+    const double r = 1 / std::sqrt(2.0);
+    const Complex a0 = std::polar(r, M_PI / 4), a7 = std::polar(r, -M_PI / 4);
+    report("qasm: build_circuit + update_state",
+           sim.circuit().net_order().size() == 4 && std::abs(sim.amplitude(0) - a0) < 1e-12 &&
+               std::abs(sim.amplitude(7) - a7) < 1e-12 && max_dev(sim) <= 1e-12);
   }
   std::printf("%s: %d failure(s)\n", g_fail ? "FAILURES" : "all passed", g_fail);
   return g_fail;
