@@ -14,6 +14,13 @@ outputs are committed as small .npz files; this script is how they were made.
 * golden_traces.npz      -- the reference's Listing-1 / entangle5 edit and an
                             8-qubit interleaved construction/removal sequence,
                             restated as modifier logs, with reference states.
+* golden_fixture_traces.npz -- the reference's own trace fixtures
+                            (proj/tests/data/entangle5.trace, mixed8.trace)
+                            parsed by paper_2210_01076_b200.trace and replayed
+                            on the reference engine: parsed statements (as
+                            arrays) and the amplitudes after every update.
+
+  python tests/golden/make_golden.py [random incremental traces fixture_traces]
 """
 import json
 import math
@@ -199,11 +206,37 @@ def make_traces():
     save_logs("golden_traces.npz", logs)
 
 
+def make_fixture_traces():
+    from paper_2210_01076_b200 import trace
+    from tests.test_trace import ref_insert, trace_to_arrays
+    out = {}
+    for name in ("entangle5", "mixed8"):
+        path = os.path.join("/root/reference/proj/tests/data", name + ".trace")
+        tr = trace.parse(open(path).read())
+        states = []
+        sim = oracle.RefSimulator(tr.num_qubits, 16, 1)
+        trace.replay(sim, tr, verify=lambda s: states.append(s.amplitudes()) or 0.0,
+                     insert_gate=ref_insert)
+        sim.close()
+        rows, ids = trace_to_arrays(tr)
+        out[name] = np.stack(states)
+        out[name + "_stmts"] = rows
+        out[name + "_ids"] = ids
+        out[name + "_n"] = np.array(tr.num_qubits)
+    np.savez_compressed(os.path.join(HERE, "golden_fixture_traces.npz"), **out)
+
+
 if __name__ == "__main__":
     oracle.build()
-    make_random()
-    make_incremental()
-    make_traces()
+    which = sys.argv[1:] or ["random", "incremental", "traces", "fixture_traces"]
+    if "random" in which:
+        make_random()
+    if "incremental" in which:
+        make_incremental()
+    if "traces" in which:
+        make_traces()
+    if "fixture_traces" in which:
+        make_fixture_traces()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)), "bytes")
