@@ -562,7 +562,7 @@ inline bool bit_of(int s, int slot) { return slot >= 0 && ((s >> slot) & 1); }
 void set_dispatch_index(EncRound& out, int R) {
   for (DOp& d : out.ops) {
     const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
-    if (type == D_MULTI || type == D_MULTIR) continue;  // layers: kernel k_layer
+    if (type == D_MULTI || type == D_MULTIR || type == D_XPERM) continue;  // k_layer / k_perm
     const uint16_t idx = variant_index(R, d.hdr & kOpVariantMask);
     if (idx == 0xffff) throw std::logic_error("device op without a kernel variant");
     d.hdr = (d.hdr & ~(0xffu << kOpIndexShift)) | (static_cast<uint32_t>(idx) << kOpIndexShift);

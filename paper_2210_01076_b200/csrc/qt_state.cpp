@@ -365,8 +365,13 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       nops += pr.enc.ops.size();
       npool += pr.enc.pool.size();
       for (const DOp& d : pr.enc.ops)
-        generic = generic || ((d.hdr & kOpVariantMask) >> 10) < D_MULTI ||
-                  (d.hdr & kOpFlagMask) != 0;
+      {
+        const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
+        if (type == D_XPERM)  // lean kernel: k_perm (controls: slot / thread / tile bits)
+          generic = generic || (d.hdr & (kOpDl | kOpDg)) != 0;
+        else
+          generic = generic || type < D_MULTI || (d.hdr & kOpFlagMask) != 0;
+      }
     }
     const bool large = nops > static_cast<size_t>(kSmallOps) ||
                        npool > static_cast<size_t>(kSmallPool) ||

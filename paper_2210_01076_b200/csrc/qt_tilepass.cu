@@ -290,17 +290,70 @@ __device__ __forceinline__ void k_layer(double2 (&v)[1 << R], const P& p, uint32
   if (cmask) layer_dense<R, 0>(v, p, cmask, o);
 }
 
+// X / CX as a register permutation: swap the pairs of slot A (runtime target
+// slot, one compiled body per slot) where the control holds -- a register
+// slot (runtime, CTA-uniform per pair), a thread bit (lmask: per-thread,
+// branch-free masked XOR swaps) and / or a bit outside the tile (gmask:
+// tile-uniform, checked once).
+__device__ __forceinline__ void mswap(double& a, double& b, uint64_t m) {
+  long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  const long long t = (x ^ y) & static_cast<long long>(m);
+  asm volatile("" : "+l"(x), "+l"(y));
+  a = __longlong_as_double(x ^ t);
+  b = __longlong_as_double(y ^ t);
+}
+
+template <int R, int A>
+__device__ __forceinline__ void perm_slot(double2 (&v)[1 << R], int cs, bool masked,
+                                          uint64_t m) {
+#pragma unroll
+  for (int s = 0; s < (1 << R); ++s) {
+    if (s & (1 << A)) continue;
+    if (cs >= 0 && !((s >> cs) & 1)) continue;  // CTA-uniform
+    const int s1 = s | (1 << A);
+    if (masked) {
+      mswap(v[s].x, v[s1].x, m);
+      mswap(v[s].y, v[s1].y, m);
+    } else {
+      xswap2(v[s], v[s1]);
+    }
+  }
+}
+
+template <int R, int A>
+__device__ __forceinline__ void perm_dispatch(double2 (&v)[1 << R], int a, int cs, bool masked,
+                                              uint64_t m) {
+  if constexpr (A < R) {
+    if (a == A) perm_slot<R, A>(v, cs, masked, m);
+    else perm_dispatch<R, A + 1>(v, a, cs, masked, m);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void k_perm(double2 (&v)[1 << R], uint32_t hdr, const DOp& d,
+                                       uint32_t jb, const uint64_t* sg) {
+  if ((hdr & kOpGctl) && (*sg & d.gmask) != d.gmask) return;  // tile-uniform
+  const int a = static_cast<int>((hdr >> 6) & 15u);
+  const int cs = static_cast<int>((hdr >> 3) & 7u) - 1;
+  const bool masked = (hdr & kOpLctl) != 0;
+  const uint64_t m = masked && (jb & d.lmask) == d.lmask ? ~0ull : 0ull;
+  perm_dispatch<R, 0>(v, a, cs, masked, m);
+}
+
 // Applies one device op. `jb` = the thread's tile-local index with the
 // register bits cleared; `sg` = the tile's global base index (smem).
 // Controls / diagonal bits outside the register slots are only evaluated for
 // ops whose header flags say they have them.
 template <int R, bool GENERIC, typename P>
 __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const DOp& d,
-                                         uint32_t jb, const uint64_t* sg) {
-  const uint32_t hdr = d.hdr;
+                                         uint32_t hdr, uint32_t jb, const uint64_t* sg) {
   const uint32_t type = (hdr & kOpVariantMask) >> 10;
+  if (type == D_XPERM) {  // X / CX on a register slot: the lean kernel has it too
+    k_perm<R>(v, hdr, d, jb, sg);
+    return;
+  }
   if (!GENERIC || type == D_MULTI || type == D_MULTIR) {
-    // the fused layer ops (the only ones of the lean kernel) carry no flags
+    // the fused layer ops carry no flags
     k_layer<R>(v, p, hdr, d.arg, d.dl, d.lmask, jb, sg);
     return;
   }
@@ -396,7 +449,15 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
         v[s] = *reinterpret_cast<const double2*>(smb + a);
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
-      for (uint32_t o = rd.op_first; o < o1; ++o) apply_op<R, GENERIC>(v, p, p.ops[o], jb, &s_tile[1]);
+      // the next op's header is loaded while the current op runs (the
+      // dispatch chain of an op starts from it; the op array always has a
+      // readable slot after the last op: pool data follows it)
+      uint32_t hdr = p.ops[rd.op_first].hdr;
+      for (uint32_t o = rd.op_first; o < o1; ++o) {
+        const uint32_t hdr_next = p.ops[o + 1].hdr;
+        apply_op<R, GENERIC>(v, p, p.ops[o], hdr, jb, &s_tile[1]);
+        hdr = hdr_next;
+      }
       // opaque copy: forces the 2^R store addresses to be regenerated here
       // instead of being kept live (2^R registers) across the op loop
       // (and the slot terms re-read from the constant bank)

@@ -95,9 +95,11 @@ _JUNK = list(";[](),qx1 \n/-*.e\"") + ["measure", "ccx", "pi", "//", "qreg", "ba
 
 
 def random_program(rng):
+    """A VALID program (errors only come from `corrupt`)."""
     n = int(rng.integers(1, 9))
+    one_line = rng.random() < 0.2  # then no // comments (they would end the program)
     out = []
-    if rng.random() < 0.3:
+    if rng.random() < 0.3 and not one_line:
         out.append("// generated")
     out.append("OPENQASM 2.0;")
     if rng.random() < 0.5:
@@ -117,10 +119,9 @@ def random_program(rng):
                        f"q[{int(rng.integers(n))}];")
         else:
             out.append(f"{_GATES1[int(rng.integers(len(_GATES1)))]} q[{int(rng.integers(n))}];")
-        if rng.random() < 0.1:
+        if rng.random() < 0.1 and not one_line:
             out[-1] += "  // note"
-    sep = " " if rng.random() < 0.2 else "\n"
-    return sep.join(out) + "\n"
+    return (" " if one_line else "\n").join(out) + "\n"
 
 
 def corrupt(rng, text):
