@@ -217,6 +217,16 @@ int qt_sim_gate_info(const qt_sim* sim, uint32_t gate, qt_gate* out,
 int qt_sim_export_gates(const qt_sim* sim, qt_gate* out, size_t cap,
                         size_t* count);
 
+/* Host-only audit of a sharded exchange (State::exchange): the grouped
+ * send/recv steps `rank` performs to swap the k global rank bits gbit[j]
+ * (0-based above the local bits) with local victim bits vbit[j], for an
+ * exchange buffer of tmp_amps amplitudes. Rows of 4 uint64: step, peer,
+ * send offset (amplitudes into the shard), receive offset (into the buffer);
+ * *piece = amplitudes per row. Call with cap 0 to size. */
+int qt_exchange_schedule(int rank, int nlocal, int k, const int* gbit, const int* vbit,
+                         uint64_t tmp_amps, uint64_t* rows, size_t cap, size_t* count,
+                         uint64_t* piece);
+
 /* ---- OpenQASM 2.0 front end (reference qasm.hpp:11-66, qasm.cpp:34-426) --
  * Same accepted subset, errors (line / column of the offending token) and
  * ASAP levelling as the reference; implementation: include/qtask/qasm.hpp. */

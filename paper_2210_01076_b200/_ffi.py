@@ -62,6 +62,7 @@ HEADER_SYMBOLS = [
     "qt_sim_amplitudes", "qt_sim_norm_squared", "qt_sim_last_update",
     "qt_sim_num_gates", "qt_sim_num_nets", "qt_sim_net_order", "qt_sim_net_gates",
     "qt_sim_gate_info", "qt_sim_export_gates", "qt_qasm_parse", "qt_qasm_build",
+    "qt_exchange_schedule",
 ]
 
 _lib = None
@@ -128,6 +129,9 @@ _SIGS = {
                       _c.c_int),
     "qt_qasm_build": ([_vp, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_int),
                        _c.POINTER(_c.c_int)], _c.c_int),
+    "qt_exchange_schedule": ([_c.c_int, _c.c_int, _c.c_int, _vp, _vp, _c.c_uint64, _vp,
+                              _c.c_size_t, _c.POINTER(_c.c_size_t),
+                              _c.POINTER(_c.c_uint64)], _c.c_int),
 }
 
 
@@ -191,3 +195,21 @@ def plan_probe(n: int, gates, global_qubits: int = 0, tile_qubits: int = 0,
     check(lib().qt_plan_probe_ex(n, global_qubits, tile_qubits, d, g.ctypes.data, len(g),
                                  buf, need.value, ctypes.byref(need)))
     return buf.value.decode()
+
+
+def exchange_schedule(rank: int, nlocal: int, pairs, tmp_amps: int):
+    """The grouped send/recv steps of a sharded exchange on `rank`
+    (qt_exchange_schedule): (rows [step, peer, send_off, recv_off], piece).
+    pairs: (global bit index above the local bits, local victim bit)."""
+    k = len(pairs)
+    g = np.array([p[0] for p in pairs], dtype=np.int32)
+    v = np.array([p[1] for p in pairs], dtype=np.int32)
+    n = ctypes.c_size_t(0)
+    piece = ctypes.c_uint64(0)
+    check(lib().qt_exchange_schedule(rank, nlocal, k, g.ctypes.data, v.ctypes.data, tmp_amps,
+                                     None, 0, ctypes.byref(n), ctypes.byref(piece)))
+    rows = np.zeros((max(1, n.value), 4), dtype=np.uint64)
+    check(lib().qt_exchange_schedule(rank, nlocal, k, g.ctypes.data, v.ctypes.data, tmp_amps,
+                                     rows.ctypes.data, n.value, ctypes.byref(n),
+                                     ctypes.byref(piece)))
+    return rows[:n.value], piece.value

@@ -377,6 +377,30 @@ int qt_sim_export_gates(const qt_sim* sim, qt_gate* outp, size_t cap, size_t* co
   });
 }
 
+int qt_exchange_schedule(int rank, int nlocal, int k, const int* gbit, const int* vbit,
+                         uint64_t tmp_amps, uint64_t* rows, size_t cap, size_t* count,
+                         uint64_t* piece) {
+  if ((k > 0 && (!gbit || !vbit)) || k < 1 || nlocal < k || nlocal > 62) return null_arg();
+  return guard([&] {
+    std::vector<std::pair<int, int>> ex;
+    for (int j = 0; j < k; ++j) ex.emplace_back(nlocal + gbit[j], vbit[j]);
+    const auto steps = qtb::exchange_schedule(rank, nlocal, ex, tmp_amps);
+    size_t n = 0;
+    for (size_t si = 0; si < steps.size(); ++si) {
+      for (size_t i = 0; i < steps[si].peer.size(); ++i, ++n) {
+        if (rows && n < cap) {
+          rows[4 * n] = si;
+          rows[4 * n + 1] = static_cast<uint64_t>(steps[si].peer[i]);
+          rows[4 * n + 2] = steps[si].send_off[i];
+          rows[4 * n + 3] = steps[si].recv_off[i];
+        }
+      }
+      if (piece) *piece = steps[si].piece;
+    }
+    if (count) *count = n;
+  });
+}
+
 }  // extern "C"
 
 // ---- OpenQASM 2.0 front end ---------------------------------------------------

@@ -399,47 +399,39 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
   stats.rewritten_amplitudes = plan.passes.empty() ? 0 : (1ull << n_);
 }
 
-void State::exchange(const PlanPass& pass) {
-  if (mode_ == Mode::Loopback) {
-    for (const auto& gv : pass.exchange)
-      cuda_check(launch_bitswap(psi_, buf_bits_, gv.first, gv.second, stream_),
-                 "bitswap");
-    stats.exchanged_bytes += pass.exchange.size() * (buffer_amps() / 2) * sizeof(double2);
-    return;
-  }
-  if (mode_ != Mode::Nccl) fail(QT_ERR_ARG, "exchange on an unsharded state");
-  const int k = static_cast<int>(pass.exchange.size());
+// The all-to-all of one exchange pass, as grouped send/recv steps. The pass
+// swaps k global (rank) bits G_j with k local victim bits V_j: this rank
+// keeps the part of its shard whose victim bits equal its own global bits
+// (rho) and trades, with each of the 2^k - 1 partners p (rank bits G_j set to
+// c_j), the region whose victim bits equal c -- receiving p's region whose
+// victim bits equal rho, into the same place. Regions are cut into runs of
+// 2^min(V) contiguous amplitudes and the runs into pieces that fit `tmp_amps`
+// (all peers' pieces side by side).
+std::vector<ExchangeStep> exchange_schedule(int rank, int nlocal,
+                                            const std::vector<std::pair<int, int>>& ex,
+                                            uint64_t tmp_amps) {
+  const int k = static_cast<int>(ex.size());
   std::vector<int> gbit(k), vbit(k);
   uint64_t vmask = 0;
-  int minv = nlocal_;
+  int minv = nlocal;
   for (int j = 0; j < k; ++j) {
-    gbit[j] = pass.exchange[j].first - nlocal_;
-    vbit[j] = pass.exchange[j].second;
+    gbit[j] = ex[j].first - nlocal;
+    vbit[j] = ex[j].second;
     vmask |= 1ull << vbit[j];
     minv = std::min(minv, vbit[j]);
   }
   int rho = 0;
-  for (int j = 0; j < k; ++j) rho |= ((rank_ >> gbit[j]) & 1) << j;
+  for (int j = 0; j < k; ++j) rho |= ((rank >> gbit[j]) & 1) << j;
   const uint64_t run_len = 1ull << minv;
-  const uint64_t region = 1ull << (nlocal_ - k);
+  const uint64_t region = 1ull << (nlocal - k);
   const uint64_t runs = region / run_len;
   const int npeer = (1 << k) - 1;
-  // receive buffer: at most 1/8 of the shard, split across the peers
-  uint64_t want = std::max<uint64_t>(1, (1ull << nlocal_) / 8);
-  want = std::min<uint64_t>(want, 1ull << 27);  // 2 GiB
-  if (d_tmp_amps_ < want) {
-    cuda_check(cudaStreamSynchronize(stream_), "sync");
-    cudaFree(d_tmp_);
-    d_tmp_ = nullptr;
-    d_tmp_amps_ = want;
-    cuda_check(cudaMalloc(&d_tmp_, d_tmp_amps_ * sizeof(double2)), "exchange buffer");
-  }
   uint64_t piece = run_len;
-  while (piece * npeer > d_tmp_amps_ && piece > 1) piece >>= 1;
+  while (piece * static_cast<uint64_t>(npeer) > tmp_amps && piece > 1) piece >>= 1;
   const uint64_t per_run = run_len / piece;
   // bits >= minv that are not V bits enumerate the runs of a region
   uint64_t above = 0;
-  for (int b = minv; b < nlocal_; ++b)
+  for (int b = minv; b < nlocal; ++b)
     if (!((vmask >> b) & 1)) above |= 1ull << b;
   auto pdep = [](uint64_t x, uint64_t mask) {
     uint64_t r = 0;
@@ -451,39 +443,78 @@ void State::exchange(const PlanPass& pass) {
     return r;
   };
   std::vector<int> peers;
-  std::vector<int> cval;
+  std::vector<uint64_t> vbase;  // the victim-bit pattern of each partner's region
   for (int c = 0; c < (1 << k); ++c) {
     if (c == rho) continue;
-    int pr = rank_;
+    int pr = rank;
+    uint64_t vb = 0;
     for (int j = 0; j < k; ++j) {
-      pr &= ~(1 << gbit[j]);
-      pr |= ((c >> j) & 1) << gbit[j];
+      pr = (pr & ~(1 << gbit[j])) | (((c >> j) & 1) << gbit[j]);
+      vb |= static_cast<uint64_t>((c >> j) & 1) << vbit[j];
     }
     peers.push_back(pr);
-    cval.push_back(c);
+    vbase.push_back(vb);
   }
-  std::vector<const void*> sends(npeer);
-  std::vector<void*> recvs(npeer);
-  std::string err;
+  std::vector<ExchangeStep> steps;
+  steps.reserve(runs * per_run);
   for (uint64_t r = 0; r < runs; ++r) {
     const uint64_t run_base = pdep(r, above);
     for (uint64_t w = 0; w < per_run; ++w) {
+      ExchangeStep st;
+      st.piece = piece;
       for (int i = 0; i < npeer; ++i) {
-        uint64_t vb = 0;
-        for (int j = 0; j < k; ++j) vb |= static_cast<uint64_t>((cval[i] >> j) & 1) << vbit[j];
-        sends[i] = psi_ + (run_base | vb) + w * piece;
-        recvs[i] = d_tmp_ + static_cast<uint64_t>(i) * piece;
+        st.peer.push_back(peers[i]);
+        st.send_off.push_back((run_base | vbase[i]) + w * piece);
+        st.recv_off.push_back(static_cast<uint64_t>(i) * piece);
       }
-      if (!comm_->sendrecv(npeer, peers.data(), sends.data(), recvs.data(),
-                           piece * sizeof(double2), stream_, &err))
-        fail(QT_ERR_NCCL, err);
-      for (int i = 0; i < npeer; ++i)
-        cuda_check(cudaMemcpyAsync(const_cast<void*>(sends[i]), recvs[i],
-                                   piece * sizeof(double2),
-                                   cudaMemcpyDeviceToDevice, stream_),
-                   "exchange copy");
+      steps.push_back(std::move(st));
     }
   }
+  return steps;
+}
+
+void State::exchange(const PlanPass& pass) {
+  if (mode_ == Mode::Loopback) {
+    for (const auto& gv : pass.exchange)
+      cuda_check(launch_bitswap(psi_, buf_bits_, gv.first, gv.second, stream_),
+                 "bitswap");
+    stats.exchanged_bytes += pass.exchange.size() * (buffer_amps() / 2) * sizeof(double2);
+    return;
+  }
+  if (mode_ != Mode::Nccl) fail(QT_ERR_ARG, "exchange on an unsharded state");
+  const int k = static_cast<int>(pass.exchange.size());
+  // receive buffer: at most 1/8 of the shard, split across the peers
+  uint64_t want = std::max<uint64_t>(1, (1ull << nlocal_) / 8);
+  want = std::min<uint64_t>(want, 1ull << 27);  // 2 GiB
+  if (d_tmp_amps_ < want) {
+    cuda_check(cudaStreamSynchronize(stream_), "sync");
+    cudaFree(d_tmp_);
+    d_tmp_ = nullptr;
+    d_tmp_amps_ = want;
+    cuda_check(cudaMalloc(&d_tmp_, d_tmp_amps_ * sizeof(double2)), "exchange buffer");
+  }
+  const std::vector<ExchangeStep> steps =
+      exchange_schedule(rank_, nlocal_, pass.exchange, d_tmp_amps_);
+  const int npeer = (1 << k) - 1;
+  std::vector<const void*> sends(npeer);
+  std::vector<void*> recvs(npeer);
+  std::vector<int> peers(npeer);
+  std::string err;
+  for (const ExchangeStep& st : steps) {
+    for (int i = 0; i < npeer; ++i) {
+      peers[i] = st.peer[i];
+      sends[i] = psi_ + st.send_off[i];
+      recvs[i] = d_tmp_ + st.recv_off[i];
+    }
+    if (!comm_->sendrecv(npeer, peers.data(), sends.data(), recvs.data(),
+                         st.piece * sizeof(double2), stream_, &err))
+      fail(QT_ERR_NCCL, err);
+    for (int i = 0; i < npeer; ++i)
+      cuda_check(cudaMemcpyAsync(const_cast<void*>(sends[i]), recvs[i],
+                                 st.piece * sizeof(double2), cudaMemcpyDeviceToDevice, stream_),
+                 "exchange copy");
+  }
+  const uint64_t region = 1ull << (nlocal_ - k);
   stats.exchanged_bytes += static_cast<uint64_t>(npeer) * region * sizeof(double2);
 }
 

@@ -33,6 +33,21 @@ struct PassTiming {
   int kind = 0;  // 0 tile, 1 exchange
 };
 
+// One grouped send/recv step of a sharded exchange (State::exchange): with
+// each peer[i], send `piece` amplitudes at shard offset send_off[i] and
+// receive as many into the exchange buffer at recv_off[i], then copy them
+// back over send_off[i].
+struct ExchangeStep {
+  uint64_t piece = 0;
+  std::vector<int> peer;
+  std::vector<uint64_t> send_off, recv_off;
+};
+// The steps of one exchange pass on `rank` (pairs: global physical bit,
+// local victim bit), for an exchange buffer of tmp_amps amplitudes.
+std::vector<ExchangeStep> exchange_schedule(int rank, int nlocal,
+                                            const std::vector<std::pair<int, int>>& ex,
+                                            uint64_t tmp_amps);
+
 class State {
  public:
   State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,

@@ -60,7 +60,32 @@ def exchange_gloo(psi, pairs, rank, nlocal):
     return out
 
 
-def _worker(rank, world, port, n, gates, psi0, want, q):
+def exchange_gloo_lib(psi, pairs, rank, nlocal, tmp_amps):
+    """Runs the library's own exchange schedule (qt_exchange_schedule, the
+    steps State::exchange issues to NCCL) with gloo send/recv: every step
+    sends each peer's piece, receives into a buffer of tmp_amps amplitudes,
+    then copies the received pieces over the sent ones."""
+    from paper_2210_01076_b200._ffi import exchange_schedule
+    rows, piece = exchange_schedule(rank, nlocal, [(g - nlocal, v) for g, v in pairs], tmp_amps)
+    out = psi.copy()
+    tmp = np.zeros(tmp_amps, dtype=np.complex128)
+    for step in np.unique(rows[:, 0]):
+        sel = rows[rows[:, 0] == step]
+        reqs, bufs = [], []
+        for _, peer, soff, roff in sel.tolist():
+            send = torch.from_numpy(out[soff:soff + piece].view(np.float64).copy())
+            recv = torch.empty_like(send)
+            reqs += [dist.isend(send, int(peer)), dist.irecv(recv, int(peer))]
+            bufs.append((soff, roff, recv))
+        for r in reqs:
+            r.wait()
+        for soff, roff, recv in bufs:
+            tmp[roff:roff + piece] = recv.numpy().view(np.complex128)
+            out[soff:soff + piece] = tmp[roff:roff + piece]
+    return out
+
+
+def _worker(rank, world, port, n, gates, psi0, want, q, use_lib=False):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
@@ -69,8 +94,11 @@ def _worker(rank, world, port, n, gates, psi0, want, q):
         plan = json.loads(plan_probe(n, gates, global_qubits=g, tile_qubits=5, detail=True))
         assert any(p["kind"] == "exchange" for p in plan["passes"])
         shard = psi0[rank << nlocal:(rank + 1) << nlocal]
-        out = apply_plan(shard, plan, base=rank << nlocal,
-                         exchange=lambda s, pairs: exchange_gloo(s, pairs, rank, nlocal))
+        if use_lib:  # small buffer: several pieces per run
+            ex = lambda s, pairs: exchange_gloo_lib(s, pairs, rank, nlocal, 1 << (nlocal - 4))
+        else:
+            ex = lambda s, pairs: exchange_gloo(s, pairs, rank, nlocal)
+        out = apply_plan(shard, plan, base=rank << nlocal, exchange=ex)
         t = torch.from_numpy(out.view(np.float64).copy())
         parts = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(parts, t)
@@ -82,8 +110,11 @@ def _worker(rank, world, port, n, gates, psi0, want, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,seed", [(2, 0), (2, 1), (4, 2), (4, 3)])
-def test_sharded_plan_over_gloo(world, seed):
+@pytest.mark.parametrize("world,seed,use_lib", [(2, 0, False), (2, 1, False), (4, 2, False),
+                                                (4, 3, False), (2, 4, True), (4, 5, True)])
+def test_sharded_plan_over_gloo(world, seed, use_lib):
+    """use_lib: the exchanges run the library's NCCL step schedule
+    (qt_exchange_schedule) instead of the restated region semantics."""
     rng = np.random.default_rng(900 + seed)
     n = 10
     gates = random_circuit(rng, n, 120)
@@ -92,7 +123,7 @@ def test_sharded_plan_over_gloo(world, seed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, gates, psi0, want, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, gates, psi0, want, q, use_lib))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -113,3 +144,40 @@ def test_config4_shape_plan_exchanges():
     for p in ex:
         for g, v in p["swap"]:
             assert g >= 13 and v < 13
+
+
+@pytest.mark.parametrize("g,k,tmp_div", [(1, 1, 1), (2, 1, 8), (2, 2, 4), (3, 3, 16), (3, 2, 64)])
+def test_exchange_schedule_all_ranks(g, k, tmp_div):
+    """All ranks' schedules (qt_exchange_schedule) executed together in numpy
+    swap the k chosen global bits with the k victim local bits of the whole
+    vector -- the sharded exchange's index math, for any buffer size."""
+    from paper_2210_01076_b200._ffi import exchange_schedule
+    rng = np.random.default_rng(17 * g + k)
+    nlocal = 9
+    world = 1 << g
+    gsel = sorted(rng.choice(g, k, replace=False).tolist())
+    vsel = sorted(rng.choice(nlocal, k, replace=False).tolist())
+    full = rng.normal(size=world << nlocal) + 1j * rng.normal(size=world << nlocal)
+    shards = [full[r << nlocal:(r + 1) << nlocal].copy() for r in range(world)]
+    tmp = max(1, (1 << nlocal) // tmp_div)
+    scheds = [exchange_schedule(r, nlocal, list(zip(gsel, vsel)), tmp) for r in range(world)]
+    new = [s.copy() for s in shards]
+    for r, (rows, piece) in enumerate(scheds):
+        for _, peer, soff, roff in rows.tolist():
+            # what `peer` sends to r in the matching step: its row addressed to r
+            prow = scheds[peer][0]
+            mine = [x for x in prow.tolist() if x[1] == r]
+            # pieces are matched by order: the i-th piece r sends to peer pairs
+            # with the i-th piece peer sends to r
+            idx = [x for x in rows.tolist() if x[1] == peer].index([_, peer, soff, roff])
+            src = mine[idx][2]
+            new[r][soff:soff + piece] = shards[peer][src:src + piece]
+    got = np.concatenate(new)
+    idx = np.arange(world << nlocal)
+    perm = idx.copy()
+    for gb, vb in zip(gsel, vsel):
+        G = nlocal + gb
+        bg, bv = (perm >> G) & 1, (perm >> vb) & 1
+        perm = perm & ~((1 << G) | (1 << vb)) | (bg << vb) | (bv << G)
+    want = full[perm]
+    assert np.abs(got - want).max() == 0.0
