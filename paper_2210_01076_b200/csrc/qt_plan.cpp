@@ -744,7 +744,7 @@ int greedy_round(const PlanPass& pass, const std::vector<int>& remaining, int R,
 // have X-role ops: every R-subset is tried and the one that schedules the
 // most X-role ops wins (ties: the plain first-need greedy), so rounds hold
 // full layers instead of whatever the op order reaches first.
-void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt) {
+void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt, bool search) {
   const int k = static_cast<int>(pass.tile_phys.size());
   std::vector<int> tix(nphys, -1);
   for (int i = 0; i < k; ++i) tix[pass.tile_phys[i]] = i;
@@ -762,6 +762,7 @@ void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt) {
     // candidate register bits: tile bits with X-role ops, in first-need order
     std::vector<int> cand;
     for (int idx : remaining) {
+      if (!search) break;
       const int nr = roles(pass.ops[idx], rl);
       for (int t = 0; t < nr; ++t) {
         if (rl[t].r != XRole) continue;
@@ -771,7 +772,7 @@ void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt) {
       if (static_cast<int>(cand.size()) >= kCand) break;
     }
     const int m = static_cast<int>(cand.size());
-    if (m > R && R <= 4) {
+    if (search && m > R && R <= 4) {
       std::vector<int> pick(R);
       // all R-subsets of cand (m <= 8: at most 70)
       for (uint32_t bits = 0; bits < (1u << m); ++bits) {
@@ -968,7 +969,7 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
     for (int p = 0; p < nlocal; ++p)
       if (inQ[p]) pass.tile_phys.push_back(p);
     if (pass.ops.empty()) throw std::logic_error("planner made no progress");
-    make_rounds(pass, R, nqubits, opt);
+    make_rounds(pass, R, nqubits, opt, nlocal >= opt.round_search_min_bits);
     split_pass(pass, plan.passes);
   }
   plan.perm_after = cur;

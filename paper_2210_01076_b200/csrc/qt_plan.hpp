@@ -15,6 +15,10 @@ struct PlanOptions {
   int lookahead = 4096;// ops scanned per pass
   bool fuse_layers = true;  // round compiler: MULTI / diagonal-table layers
   int max_round_ops = 48;   // logical ops per register round (param space)
+  // register-set search per round (qt_plan.cpp make_rounds) from this many
+  // local qubits up: it costs host time per round and pays off only where a
+  // pass streams enough amplitudes (small states are launch/host-bound)
+  int round_search_min_bits = 22;
 };
 
 // Merges runs of uncontrolled single-qubit ops on the same qubit into one
