@@ -156,6 +156,20 @@ class Simulator {
     detail::check(qt_sim_norm_squared(s_, &v));
     return v;
   }
+  // Amplitude report (reference tools/qtask_cli.cpp:53-86, additive here):
+  // the k amplitudes of largest std::norm, ties by smaller index, selected
+  // on the device; (index, amplitude) pairs, largest first.
+  std::vector<std::pair<std::uint64_t, Complex>> top_k(std::uint64_t k) const {
+    const std::uint64_t dim = std::uint64_t{1} << num_qubits();
+    if (k > dim) k = dim;
+    std::vector<std::uint64_t> idx(k ? k : 1);
+    std::vector<Complex> amp(k ? k : 1);
+    std::uint64_t n = 0;
+    detail::check(qt_sim_top_k(s_, k, idx.data(), reinterpret_cast<double*>(amp.data()), &n));
+    std::vector<std::pair<std::uint64_t, Complex>> out(n);
+    for (std::uint64_t i = 0; i < n; ++i) out[i] = {idx[i], amp[i]};
+    return out;
+  }
   UpdateStats last_update() const {
     qt_run_stats s{};
     qt_sim_last_update(s_, &s);

@@ -152,6 +152,13 @@ int qt_apply(qt_state* st, const qt_gate* gates, size_t count);
 /* Sum |a|^2 by a deterministic tree reduction (fixed order, bit-stable
  * across runs); sharded: fixed-order combine over ranks. */
 int qt_norm_squared(qt_state* st, double* out);
+/* Top-K readout (the reference's amplitude report, qtask_cli.cpp:53-86):
+ * the min(k, 2^n) amplitudes of largest |a|^2 (std::norm; ties: smaller
+ * index first), sorted, with their logical indices -- selected on the
+ * device, only k records cross PCIe. *count = records written.
+ * Single-device and loopback states. */
+int qt_top_k(qt_state* st, uint64_t k, uint64_t* indices, double* amps_interleaved,
+             uint64_t* count);
 int qt_sync(qt_state* st);
 int qt_last_stats(const qt_state* st, qt_run_stats* out);
 /* Device-resident checkpoint slots (HBM copies of the state). */
@@ -202,6 +209,10 @@ int qt_sim_amplitude(qt_sim* sim, uint64_t index, double* out2);
 int qt_sim_amplitudes(qt_sim* sim, uint64_t first, uint64_t last,
                       double* interleaved);
 int qt_sim_norm_squared(qt_sim* sim, double* out);
+/* qt_top_k on the simulator's committed state (QT_ERR_STALE_STATE while
+ * modifiers pend, like amplitude queries). */
+int qt_sim_top_k(qt_sim* sim, uint64_t k, uint64_t* indices, double* amps_interleaved,
+                 uint64_t* count);
 int qt_sim_last_update(const qt_sim* sim, qt_run_stats* out);
 
 /* Circuit introspection (Circuit, circuit.hpp:32-66): counts and the

@@ -62,7 +62,7 @@ HEADER_SYMBOLS = [
     "qt_sim_amplitudes", "qt_sim_norm_squared", "qt_sim_last_update",
     "qt_sim_num_gates", "qt_sim_num_nets", "qt_sim_net_order", "qt_sim_net_gates",
     "qt_sim_gate_info", "qt_sim_export_gates", "qt_qasm_parse", "qt_qasm_build",
-    "qt_exchange_schedule",
+    "qt_exchange_schedule", "qt_top_k", "qt_sim_top_k",
 ]
 
 _lib = None
@@ -129,6 +129,8 @@ _SIGS = {
                       _c.c_int),
     "qt_qasm_build": ([_vp, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_int),
                        _c.POINTER(_c.c_int)], _c.c_int),
+    "qt_top_k": ([_vp, _c.c_uint64, _vp, _vp, _c.POINTER(_c.c_uint64)], _c.c_int),
+    "qt_sim_top_k": ([_vp, _c.c_uint64, _vp, _vp, _c.POINTER(_c.c_uint64)], _c.c_int),
     "qt_exchange_schedule": ([_c.c_int, _c.c_int, _c.c_int, _vp, _vp, _c.c_uint64, _vp,
                               _c.c_size_t, _c.POINTER(_c.c_size_t),
                               _c.POINTER(_c.c_uint64)], _c.c_int),

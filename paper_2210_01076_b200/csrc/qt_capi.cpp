@@ -333,6 +333,30 @@ int qt_sim_amplitudes(qt_sim* sim, uint64_t first, uint64_t last, double* outp) 
   if (!sim || !outp) return null_arg();
   return guard([&] { sim->s->amplitudes(first, last, outp); });
 }
+namespace {
+void put_topk(const std::vector<qtb::TopkItem>& items, uint64_t* idx, double* amps,
+              uint64_t* count) {
+  for (size_t i = 0; i < items.size(); ++i) {
+    if (idx) idx[i] = items[i].index;
+    if (amps) {
+      amps[2 * i] = items[i].amp.x;
+      amps[2 * i + 1] = items[i].amp.y;
+    }
+  }
+  if (count) *count = items.size();
+}
+}  // namespace
+
+int qt_sim_top_k(qt_sim* sim, uint64_t k, uint64_t* idx, double* amps, uint64_t* count) {
+  if (!sim) return null_arg();
+  return guard([&] { put_topk(sim->s->top_k(k), idx, amps, count); });
+}
+
+int qt_top_k(qt_state* st, uint64_t k, uint64_t* idx, double* amps, uint64_t* count) {
+  if (!st) return null_arg();
+  return guard([&] { put_topk(st->s->top_k(k), idx, amps, count); });
+}
+
 int qt_sim_norm_squared(qt_sim* sim, double* outp) {
   if (!sim || !outp) return null_arg();
   return guard([&] { *outp = sim->s->norm_squared(); });

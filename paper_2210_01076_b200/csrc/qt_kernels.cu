@@ -150,6 +150,111 @@ __global__ void check_finite_kernel(const double2* __restrict__ psi,
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// ---- top-K readout by |a|^2 (the reference's amplitude report,
+// tools/qtask_cli.cpp:53-86: partial_sort by norm descending, index
+// ascending) -- an exact radix select over the 64-bit key below, then one
+// collecting pass; every pass streams the state once. -----------------------
+
+// |a|^2 exactly as std::norm (x*x + y*y, no FMA contraction); the IEEE bits of
+// a non-negative double order like its value.
+__device__ __forceinline__ uint64_t norm_key(double2 a) {
+  const double n = __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+  return static_cast<uint64_t>(__double_as_longlong(n));
+}
+
+__global__ void topk_hist_kernel(const double2* __restrict__ psi, uint64_t count,
+                                 uint64_t prefix, uint64_t pmask, int shift,
+                                 unsigned long long* __restrict__ hist) {
+  __shared__ unsigned int h[kTopkBins];
+  for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const uint64_t k = norm_key(__ldcs(psi + i));
+    if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & (kTopkBins - 1)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], static_cast<unsigned long long>(h[i]));
+}
+
+// Appends every amplitude with key >= lo (at most `cap`; the caller sized it).
+__global__ void topk_collect_kernel(const double2* __restrict__ psi, uint64_t count,
+                                    uint64_t base, uint64_t lo, TopkItem* __restrict__ out,
+                                    unsigned long long* __restrict__ n, uint64_t cap) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const double2 a = __ldcs(psi + i);
+    const uint64_t k = norm_key(a);
+    if (k >= lo) {
+      const unsigned long long at = atomicAdd(n, 1ull);
+      if (at < cap) out[at] = TopkItem{base + i, k, a};
+    }
+  }
+}
+
+// Block b of a fixed partition ([b * per, (b + 1) * per)) counts keys == t.
+__global__ void topk_ties_kernel(const double2* __restrict__ psi, uint64_t count, uint64_t per,
+                                 uint64_t t, unsigned long long* __restrict__ ties) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * per;
+  const uint64_t b1 = b0 + per < count ? b0 + per : count;
+  unsigned int c = 0;
+  for (uint64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) c += norm_key(__ldcs(psi + i)) == t;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ unsigned int w[32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) s += w[i];
+    ties[blockIdx.x] = s;
+  }
+}
+
+// Writes the keys > t (atomic append into out[0, n_gt)) and, in index order,
+// the first `r` keys == t (out[n_gt + rank]); tie_off[b] = ties in blocks < b.
+__global__ void topk_final_kernel(const double2* __restrict__ psi, uint64_t count, uint64_t per,
+                                  uint64_t base, uint64_t t, uint64_t r, uint64_t n_gt,
+                                  const unsigned long long* __restrict__ tie_off,
+                                  TopkItem* __restrict__ out, unsigned long long* __restrict__ n) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * per;
+  const uint64_t b1 = b0 + per < count ? b0 + per : count;
+  __shared__ unsigned int wsum[32];
+  uint64_t rank = tie_off[blockIdx.x];
+  if (rank >= r) r = 0;  // no tie of this block is needed (gt keys still are)
+  for (uint64_t c0 = b0; c0 < b1; c0 += blockDim.x) {
+    const uint64_t i = c0 + threadIdx.x;
+    double2 a = make_double2(0.0, 0.0);
+    uint64_t k = 0;
+    if (i < b1) {
+      a = __ldcs(psi + i);
+      k = norm_key(a);
+    }
+    const bool tie = i < b1 && k == t;
+    if (i < b1 && k > t) {
+      const unsigned long long at = atomicAdd(n, 1ull);
+      if (at < n_gt) out[at] = TopkItem{base + i, k, a};
+    }
+    // in-order rank of this thread's tie within the chunk (block scan)
+    const unsigned int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned int bal = __ballot_sync(0xffffffffu, tie);
+    const unsigned int before = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    unsigned int woff = 0, total = 0;
+    for (unsigned int x = 0; x < (blockDim.x >> 5); ++x) {
+      if (x < warp) woff += wsum[x];
+      total += wsum[x];
+    }
+    if (tie && rank + woff + before < r) {
+      const uint64_t at = rank + woff + before;
+      out[n_gt + at] = TopkItem{base + i, k, a};
+    }
+    rank += total;
+    __syncthreads();
+  }
+}
+
 int grid_for(uint64_t work, int block) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -210,6 +315,34 @@ cudaError_t launch_gather_shard(const double2* psi, double2* out,
 cudaError_t launch_fp64_probe(double* out, int grid, int block, int iters,
                               cudaStream_t s) {
   fp64_probe_kernel<<<grid, block, 0, s>>>(out, iters);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_hist(const double2* psi, uint64_t count, uint64_t prefix,
+                             uint64_t pmask, int shift, unsigned long long* hist,
+                             cudaStream_t s) {
+  topk_hist_kernel<<<grid_for(count, 256), 256, 0, s>>>(psi, count, prefix, pmask, shift, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_collect(const double2* psi, uint64_t count, uint64_t base, uint64_t lo,
+                                TopkItem* out, unsigned long long* n, uint64_t cap,
+                                cudaStream_t s) {
+  topk_collect_kernel<<<grid_for(count, 256), 256, 0, s>>>(psi, count, base, lo, out, n, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_ties(const double2* psi, uint64_t count, uint64_t per, int blocks,
+                             uint64_t t, unsigned long long* ties, cudaStream_t s) {
+  topk_ties_kernel<<<blocks, 256, 0, s>>>(psi, count, per, t, ties);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_final(const double2* psi, uint64_t count, uint64_t per, int blocks,
+                              uint64_t base, uint64_t t, uint64_t r, uint64_t n_gt,
+                              const unsigned long long* tie_off, TopkItem* out,
+                              unsigned long long* n, cudaStream_t s) {
+  topk_final_kernel<<<blocks, 256, 0, s>>>(psi, count, per, base, t, r, n_gt, tie_off, out, n);
   return cudaGetLastError();
 }
 

@@ -82,6 +82,32 @@ cudaError_t launch_gather_shard(const double2* psi, double2* out,
 // FP64 throughput probe: iters x 16 independent FMA chains per thread.
 cudaError_t launch_fp64_probe(double* out, int grid, int block, int iters,
                               cudaStream_t s);
+// ---- top-K by |a|^2 (qt_state.cpp State::top_k drives these) ----
+constexpr int kTopkBits = 11;
+constexpr int kTopkBins = 1 << kTopkBits;
+struct TopkItem {
+  uint64_t index;  // logical index (chunk base + position)
+  uint64_t key;    // bits of |a|^2 (std::norm, no FMA)
+  double2 amp;
+};
+// hist[(key >> shift) & (bins-1)] += 1 for keys with (key & pmask) == prefix
+cudaError_t launch_topk_hist(const double2* psi, uint64_t count, uint64_t prefix,
+                             uint64_t pmask, int shift, unsigned long long* hist,
+                             cudaStream_t s);
+// appends every amplitude with key >= lo (at most cap written)
+cudaError_t launch_topk_collect(const double2* psi, uint64_t count, uint64_t base, uint64_t lo,
+                                TopkItem* out, unsigned long long* n, uint64_t cap,
+                                cudaStream_t s);
+// per-block (fixed partition of `per` amplitudes) counts of key == t
+cudaError_t launch_topk_ties(const double2* psi, uint64_t count, uint64_t per, int blocks,
+                             uint64_t t, unsigned long long* ties, cudaStream_t s);
+// keys > t appended into out[0, n_gt); the first r keys == t in index order
+// into out[n_gt + rank] (tie_off = exclusive prefix of the tie counts)
+cudaError_t launch_topk_final(const double2* psi, uint64_t count, uint64_t per, int blocks,
+                              uint64_t base, uint64_t t, uint64_t r, uint64_t n_gt,
+                              const unsigned long long* tie_off, TopkItem* out,
+                              unsigned long long* n, cudaStream_t s);
+
 // Checks a range for non-finite values (flag |= 1).
 cudaError_t launch_check_finite(const double2* psi, uint64_t n, int* flag,
                                 cudaStream_t s);

@@ -289,6 +289,11 @@ void Sim::amplitudes(uint64_t first, uint64_t last, double* out) {
   st_->read(first, last - first + 1, out);
 }
 
+std::vector<TopkItem> Sim::top_k(uint64_t k) {
+  if (pending_) fail(QT_ERR_STALE_STATE, "modifiers pending; call update_state first");
+  return st_->top_k(k);
+}
+
 double Sim::norm_squared() {
   // engine.cpp:551-564 reads the last committed state without a pending check
   return st_->norm_squared();

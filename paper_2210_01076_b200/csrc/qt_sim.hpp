@@ -32,6 +32,7 @@ class Sim {
 
   void amplitudes(uint64_t first, uint64_t last, double* out);
   double norm_squared();
+  std::vector<TopkItem> top_k(uint64_t k);
   const qt_run_stats& last_update() const { return last_; }
 
   size_t num_gates() const { return gates_.size(); }

@@ -518,6 +518,148 @@ void State::exchange(const PlanPass& pass) {
   stats.exchanged_bytes += static_cast<uint64_t>(npeer) * region * sizeof(double2);
 }
 
+// Top-K readout (the reference's amplitude report, qtask_cli.cpp:53-86:
+// partial_sort by std::norm descending, index ascending) without copying the
+// state to the host: an exact radix select over the 64-bit |a|^2 key, 11 bits
+// per pass (a pass = one HBM sweep + a 16 KiB histogram readback); as soon as
+// the selected bin holds <= 2^16 keys, one collecting pass gathers every key
+// >= the bin's floor and the host sorts those few. Fully tied states (e.g. a
+// uniform superposition) go to the exact threshold and rank its ties in
+// logical index order (two more sweeps). Permuted (loopback) states are
+// streamed in logical-order chunks through the gather kernel.
+std::vector<TopkItem> State::top_k(uint64_t k) {
+  if (mode_ == Mode::Nccl) fail(QT_ERR_ARG, "top_k: sharded (NCCL) states are not supported");
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const uint64_t total = 1ull << n_;
+  k = std::min(k, total);
+  if (k == 0) return {};
+  bool identity = true;
+  for (int q = 0; q < n_; ++q) identity = identity && perm_[q] == q;
+  const uint64_t chunk = 1ull << 22;
+  std::vector<uint8_t> pm(n_);
+  for (int q = 0; q < n_; ++q) pm[q] = static_cast<uint8_t>(perm_[q]);
+  if (!identity && d_tmp_amps_ < std::min(total, chunk)) {
+    cudaFree(d_tmp_);
+    d_tmp_ = nullptr;
+    d_tmp_amps_ = std::min(total, chunk);
+    cuda_check(cudaMalloc(&d_tmp_, d_tmp_amps_ * sizeof(double2)), "gather buffer");
+  }
+  auto for_chunks = [&](const auto& fn) {
+    if (identity) {
+      fn(static_cast<const double2*>(psi_), total, uint64_t{0});
+      return;
+    }
+    for (uint64_t off = 0; off < total; off += chunk) {
+      const uint64_t c = std::min(chunk, total - off);
+      cuda_check(launch_gather(psi_, d_tmp_, off, c, pm.data(), n_, stream_), "gather");
+      fn(static_cast<const double2*>(d_tmp_), c, off);
+    }
+  };
+  const uint64_t cap = 1ull << 16;
+  unsigned long long *d_hist = nullptr, *d_n = nullptr;
+  TopkItem* d_items = nullptr;
+  cuda_check(cudaMalloc(&d_hist, sizeof(unsigned long long) * kTopkBins), "topk hist");
+  cuda_check(cudaMalloc(&d_n, sizeof(unsigned long long)), "topk counter");
+  cuda_check(cudaMalloc(&d_items, sizeof(TopkItem) * (k + cap)), "topk items");
+  struct Free {
+    void* a[3];
+    ~Free() {
+      for (void* p : a) cudaFree(p);
+    }
+  } guard_{{d_hist, d_n, d_items}};
+  std::vector<unsigned long long> h(kTopkBins);
+  std::vector<TopkItem> items;
+  auto finish = [&](uint64_t count) {
+    items.resize(count);
+    cuda_check(cudaMemcpyAsync(items.data(), d_items, sizeof(TopkItem) * count,
+                               cudaMemcpyDeviceToHost, stream_),
+               "topk readback");
+    sync();
+    std::sort(items.begin(), items.end(), [](const TopkItem& a, const TopkItem& b) {
+      return a.key != b.key ? a.key > b.key : a.index < b.index;
+    });
+    if (items.size() > k) items.resize(k);
+  };
+  uint64_t prefix = 0, pmask = 0, c_gt = 0;
+  int shift = 64;
+  while (shift > 0) {
+    const int bits = std::min(kTopkBits, shift);
+    shift -= bits;
+    cuda_check(cudaMemsetAsync(d_hist, 0, sizeof(unsigned long long) * kTopkBins, stream_),
+               "topk hist reset");
+    for_chunks([&](const double2* src, uint64_t c, uint64_t) {
+      cuda_check(launch_topk_hist(src, c, prefix, pmask, shift, d_hist, stream_), "topk hist");
+    });
+    cuda_check(cudaMemcpyAsync(h.data(), d_hist, sizeof(unsigned long long) * kTopkBins,
+                               cudaMemcpyDeviceToHost, stream_),
+               "topk hist readback");
+    sync();
+    uint64_t above = 0;
+    int b = (1 << bits) - 1;
+    for (; b > 0; --b) {
+      if (c_gt + above + h[b] >= k) break;
+      above += h[b];
+    }
+    c_gt += above;
+    prefix |= static_cast<uint64_t>(b) << shift;
+    pmask |= ((1ull << bits) - 1) << shift;
+    if (h[b] <= cap) {
+      // every key >= the bin's floor: c_gt + h[b] <= k + cap of them
+      const uint64_t want = c_gt + h[b];
+      cuda_check(cudaMemsetAsync(d_n, 0, sizeof(unsigned long long), stream_), "topk counter");
+      for_chunks([&](const double2* src, uint64_t c, uint64_t base) {
+        cuda_check(launch_topk_collect(src, c, base, prefix, d_items, d_n, k + cap, stream_),
+                   "topk collect");
+      });
+      finish(want);
+      return items;
+    }
+  }
+  // exact threshold key t = prefix with c_gt keys above it: rank its ties
+  const uint64_t t = prefix, r = k - c_gt;
+  const int blocks_max = 8 * sms_;
+  std::vector<std::vector<unsigned long long>> tie_off;
+  unsigned long long* d_ties = nullptr;
+  cuda_check(cudaMalloc(&d_ties, sizeof(unsigned long long) * blocks_max), "topk ties");
+  struct FreeOne {
+    void* p;
+    ~FreeOne() { cudaFree(p); }
+  } guard2_{d_ties};
+  uint64_t running = 0;
+  for_chunks([&](const double2* src, uint64_t c, uint64_t) {
+    const int blocks = static_cast<int>(std::min<uint64_t>(blocks_max, (c + 255) / 256));
+    const uint64_t per = (c + blocks - 1) / blocks;
+    cuda_check(launch_topk_ties(src, c, per, blocks, t, d_ties, stream_), "topk ties");
+    std::vector<unsigned long long> cnt(blocks);
+    cuda_check(cudaMemcpyAsync(cnt.data(), d_ties, sizeof(unsigned long long) * blocks,
+                               cudaMemcpyDeviceToHost, stream_),
+               "topk ties readback");
+    sync();
+    std::vector<unsigned long long> off(blocks);
+    for (int i = 0; i < blocks; ++i) {
+      off[i] = running;
+      running += cnt[i];
+    }
+    tie_off.push_back(std::move(off));
+  });
+  cuda_check(cudaMemsetAsync(d_n, 0, sizeof(unsigned long long), stream_), "topk counter");
+  size_t ci = 0;
+  for_chunks([&](const double2* src, uint64_t c, uint64_t base) {
+    const std::vector<unsigned long long>& off = tie_off[ci++];
+    const int blocks = static_cast<int>(off.size());
+    const uint64_t per = (c + blocks - 1) / blocks;
+    cuda_check(cudaMemcpyAsync(d_ties, off.data(), sizeof(unsigned long long) * blocks,
+                               cudaMemcpyHostToDevice, stream_),
+               "topk tie offsets");
+    cuda_check(launch_topk_final(src, c, per, blocks, base, t, r, c_gt, d_ties, d_items, d_n,
+                                 stream_),
+               "topk final");
+    sync();  // d_ties is rewritten for the next chunk
+  });
+  finish(k);
+  return items;
+}
+
 double State::norm_squared() {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   double* out = d_scratch_ + kNormBlocks;

@@ -81,6 +81,9 @@ class State {
   void bind(int i, const std::vector<int>& perm);
   void apply(const qt_gate* gates, size_t count);
   double norm_squared();
+  // The k amplitudes of largest |a|^2 (ties: smaller logical index first),
+  // sorted; logical indices. Single / loopback states (State::top_k).
+  std::vector<TopkItem> top_k(uint64_t k);
   void sync();  // also raises QT_ERR_NUMERIC if a pass saw a non-finite value
 
   void checkpoint_save(int slot);

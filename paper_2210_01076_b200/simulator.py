@@ -206,6 +206,18 @@ class Simulator:
         check(lib().qt_sim_amplitudes(self._h, first, last, out.ctypes.data))
         return out
 
+    def top_k(self, k: int):
+        """The reference's amplitude report (qtask_cli.cpp:53-86): indices and
+        amplitudes of the k largest |a|^2 (ties: smaller index first),
+        selected on the device. StaleStateError while modifiers pend."""
+        k = min(int(k), 1 << self.num_qubits())
+        idx = np.empty(max(1, k), dtype=np.uint64)
+        amps = np.empty(max(1, k), dtype=np.complex128)
+        cnt = ctypes.c_uint64(0)
+        check(lib().qt_sim_top_k(self._h, k, idx.ctypes.data, amps.ctypes.data,
+                                 ctypes.byref(cnt)))
+        return idx[:cnt.value], amps[:cnt.value]
+
     def norm_squared(self) -> float:
         v = ctypes.c_double(0.0)
         check(lib().qt_sim_norm_squared(self._h, ctypes.byref(v)))

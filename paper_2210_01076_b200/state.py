@@ -77,6 +77,16 @@ class StateVector:
         check(lib().qt_read(self._h, first, count, out.ctypes.data))
         return out
 
+    def top_k(self, k: int):
+        """(indices, amplitudes) of the k largest |a|^2, largest first, ties by
+        smaller index -- selected on the device (qt_top_k)."""
+        k = min(int(k), 1 << self.n)
+        idx = np.empty(max(1, k), dtype=np.uint64)
+        amps = np.empty(max(1, k), dtype=np.complex128)
+        cnt = ctypes.c_uint64(0)
+        check(lib().qt_top_k(self._h, k, idx.ctypes.data, amps.ctypes.data, ctypes.byref(cnt)))
+        return idx[:cnt.value], amps[:cnt.value]
+
     def norm_squared(self) -> float:
         v = ctypes.c_double(0.0)
         check(lib().qt_norm_squared(self._h, ctypes.byref(v)))

@@ -116,12 +116,35 @@ def c5(nmods):
                 workload=w.name, modifiers=nmods)
 
 
+def topk():
+    """Device top-K readout (qt_top_k) of the C3 final state at 30 qubits vs
+    the full-state D2H copy it replaces."""
+    w = W.config3()
+    st = StateVector(w.n)
+    st.apply(w.gates)
+    st.sync()
+    out = {"qubits": w.n}
+    for k in (16, 4096):
+        st.top_k(k)
+        t0 = time.perf_counter()
+        idx, amps = st.top_k(k)
+        dt = time.perf_counter() - t0
+        out[f"k{k}_seconds"] = dt
+        out[f"k{k}_first"] = [int(idx[0]), abs(complex(amps[0])) ** 2]
+    half = np.empty(1 << (w.n - 1), dtype=np.complex128)
+    t0 = time.perf_counter()
+    st.read(0, 1 << (w.n - 1), out=half)
+    out["d2h_full_state_seconds_est"] = 2 * (time.perf_counter() - t0)
+    st.close()
+    return out
+
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--c5-mods", type=int, default=1000)
 ap.add_argument("--skip", nargs="*", default=[])
 args = ap.parse_args()
 res = {}
-for name, fn in (("c2", c2), ("c4", c4), ("c5", lambda: c5(args.c5_mods))):
+for name, fn in (("c2", c2), ("c4", c4), ("c5", lambda: c5(args.c5_mods)), ("topk", topk)):
     if name in args.skip:
         continue
     try:
