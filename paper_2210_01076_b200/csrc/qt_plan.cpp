@@ -479,10 +479,13 @@ void emit_layer(LayerState& L, EncRound& out) {
   }
   for (int i = 0; i < L.R; ++i) {
     if (!(L.mmask & (1u << i))) continue;
-    // rotation form (to_rotations): [[c, -s], [s, c]] stored as (c, s)
+    // rotation [[c, -s], [s, c]] (c >= 0, to_rotations) as three in-place
+    // shears (kernel pair_shear): x += a y; y += b x; x += a y with
+    // a = -tan(theta/2) = -s / (1 + c) in [-1, 1] and b = sin(theta) = s
     if (rmask & (1u << i)) {
-      out.pool.push_back(L.M[i][0].re);
-      out.pool.push_back(L.M[i][2].re);
+      const double c = L.M[i][0].re, sn = L.M[i][2].re;
+      out.pool.push_back(-sn / (1.0 + c));
+      out.pool.push_back(sn);
     }
   }
   for (int i = 0; i < L.R; ++i)
@@ -502,17 +505,28 @@ void to_rotations(LayerState& L) {
   for (int i = 0; i < L.R; ++i) {
     if (!(L.mmask & (1u << i)) || (L.cmask & (1u << i))) continue;
     const double m0 = L.M[i][0].re, m1 = L.M[i][1].re, m2 = L.M[i][2].re, m3 = L.M[i][3].re;
-    if (m0 == m3 && m1 == -m2) continue;
-    if (m0 == -m3 && m1 == m2) {
+    bool rot = m0 == m3 && m1 == -m2;
+    if (!rot && m0 == -m3 && m1 == m2) {
       SignTerm z{};
       for (int s = 0; s < L.NS; ++s)
         if ((s >> i) & 1) z.slots |= 1u << s;
       L.pre_signs.push_back(z);
       L.M[i][1] = cplx{-m2, 0.0};
       L.M[i][3] = cplx{m0, 0.0};
+      rot = true;
+    }
+    if (!rot) {
+      L.cmask |= 1u << i;
       continue;
     }
-    L.cmask |= 1u << i;
+    if (L.M[i][0].re < 0.0) {
+      // R(theta) = -R(theta - pi): keep |theta| <= pi/2 (shear factors <= 1);
+      // the scalar -1 commutes with everything and joins the layer's signs
+      for (int k = 0; k < 4; ++k) L.M[i][k] = cplx{-L.M[i][k].re, 0.0};
+      SignTerm all{};
+      all.slots = (L.NS >= 32) ? 0xffffffffu : ((1u << L.NS) - 1u);
+      L.pre_signs.push_back(all);
+    }
   }
   static const bool nomix = std::getenv("QTB_NOMIX") != nullptr;  // A/B only
   if (nomix && L.cmask) L.cmask = L.mmask;
@@ -1007,7 +1021,7 @@ std::string plan_to_json(const Plan& p, bool detail) {
           case D_REAL: case D_ANTI: fp += ctl ? 2.0 : 4.0; break;
           case D_DIAG: case D_PHASE1: case D_DTAB: fp += 4.0; break;
           case D_MULTIR:  // a layer: rotations (a), complex 2x2s (lmask), table
-            fp += 4.0 * __builtin_popcount(a) + 8.0 * __builtin_popcount(d.lmask) +
+            fp += 3.0 * __builtin_popcount(a) + 8.0 * __builtin_popcount(d.lmask) +
                   ((d.hdr & kOpTable) ? 4.0 : 0.0);
             break;
           default: break;

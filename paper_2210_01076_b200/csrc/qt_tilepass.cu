@@ -83,6 +83,24 @@ __device__ __forceinline__ void pair_real(double2 (&v)[1 << R], double m0, doubl
   }
 }
 
+// Real rotation [[c, -s], [s, c]] (|theta| <= pi/2) as three shears, each an
+// in-place FMA: x += a y; y += b x; x += a y with a = -tan(theta/2), b =
+// sin(theta) -- 3 FP64 ops per amplitude instead of 4, no temporaries.
+template <int R, int A>
+__device__ __forceinline__ void pair_shear(double2 (&v)[1 << R], double a, double b) {
+#pragma unroll
+  for (int s = 0; s < (1 << R); ++s) {
+    if (s & (1 << A)) continue;
+    const int s1 = s | (1 << A);
+    v[s].x = fma(a, v[s1].x, v[s].x);
+    v[s].y = fma(a, v[s1].y, v[s].y);
+    v[s1].x = fma(b, v[s].x, v[s1].x);
+    v[s1].y = fma(b, v[s].y, v[s1].y);
+    v[s].x = fma(a, v[s1].x, v[s].x);
+    v[s].y = fma(a, v[s1].y, v[s].y);
+  }
+}
+
 template <int R, int A, int CS, typename P>
 __device__ __forceinline__ void k_dense(double2 (&v)[1 << R], const P& p, int o) {
   pair_dense<R, A, CS>(v, p.pool[o], p.pool[o + 1], p.pool[o + 2], p.pool[o + 3],
@@ -240,9 +258,8 @@ __device__ __forceinline__ void layer_rot(double2 (&v)[1 << R], const P& p, uint
                                           int& o) {
   if constexpr (A < R) {
     if (mask & (1u << A)) {
-      // rotation [[c, -s], [s, c]] stored as (c, s)
-      const double c = p.pool[o], sn = p.pool[o + 1];
-      pair_real<R, A, -1>(v, c, -sn, sn, c);
+      // rotation as three in-place shears (a, b): see pair_shear
+      pair_shear<R, A>(v, p.pool[o], p.pool[o + 1]);
       o += 2;
     }
     layer_rot<R, A + 1>(v, p, mask, o);
@@ -265,7 +282,8 @@ __device__ __forceinline__ void layer_dense(double2 (&v)[1 << R], const P& p, ui
 // MULTIR): the layer's diagonal table (kOpTable), its sign terms (base mask
 // in dl, conditional terms counted in arg >> 16), then one 2x2 per register
 // slot in the slot mask, ascending slots (they commute exactly, so one fixed
-// order): real rotations (c, s) after the ZYZ split, or complex 2x2s. Pool
+// order): real rotations (three-shear form, after the ZYZ split) or complex
+// 2x2s. Pool
 // data in that order. A lone table / sign op is a layer with an empty mask.
 // The slot loop is a runtime (CTA-uniform) mask over R compiled slot bodies:
 // one copy of each body keeps the hot loop inside the instruction cache.
