@@ -231,6 +231,13 @@ __device__ __forceinline__ void k_dtab(double2 (&v)[1 << R], const P& p, int o) 
 // Sign terms: `base` = the unconditional terms (folded on the host) and nt
 // thread/tile-conditional terms at pool[o]; then one integer XOR per
 // component (branch-free: the mask differs between threads).
+// hi ^ (ms & 0x80000000) in one LOP3 (LUT 0x78 = a ^ (b & c))
+__device__ __forceinline__ int xor_sign(int hi, uint32_t ms) {
+  int r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(r) : "r"(hi), "r"(ms), "n"(0x80000000));
+  return r;
+}
+
 template <int R, typename P>
 __device__ __forceinline__ void apply_signs(double2 (&v)[1 << R], const P& p, int o,
                                             uint32_t nt, uint32_t base, uint32_t jb,
@@ -246,9 +253,11 @@ __device__ __forceinline__ void apply_signs(double2 (&v)[1 << R], const P& p, in
   }
 #pragma unroll
   for (int s = 0; s < (1 << R); ++s) {
-    const uint32_t sb = ((mask >> s) & 1u) << 31;
-    v[s] = make_double2(__hiloint2double(__double2hiint(v[s].x) ^ sb, __double2loint(v[s].x)),
-                        __hiloint2double(__double2hiint(v[s].y) ^ sb, __double2loint(v[s].y)));
+    // bit s of the mask to the sign bit: one shift, then one and-xor LOP3
+    // (hi ^ (ms & 0x80000000)) per high word
+    const uint32_t ms = mask << (31 - s);
+    v[s] = make_double2(__hiloint2double(xor_sign(__double2hiint(v[s].x), ms), __double2loint(v[s].x)),
+                        __hiloint2double(xor_sign(__double2hiint(v[s].y), ms), __double2loint(v[s].y)));
   }
 }
 
