@@ -164,7 +164,6 @@ namespace {
 // So a layered circuit pays one diagonal table per rotation layer (the
 // rotations' input phases) instead of an extra one at every round end.
 void push_phases(std::vector<LOp>& ops, int nqubits) {
-  if (std::getenv("QTB_NOPUSH")) return;  // A/B measurements only
   std::vector<LOp> out;
   out.reserve(ops.size() + static_cast<size_t>(nqubits));
   std::vector<cplx> d0(nqubits, cplx{1.0, 0.0}), d1(nqubits, cplx{1.0, 0.0});
@@ -528,29 +527,18 @@ void to_rotations(LayerState& L) {
       L.pre_signs.push_back(all);
     }
   }
-  static const bool nomix = std::getenv("QTB_NOMIX") != nullptr;  // A/B only
-  if (nomix && L.cmask) L.cmask = L.mmask;
 }
 
-// Emits the layer (pre part + 2x2s); the post part becomes the next
-// layer's pre part. QTB_NOLAYER=1 keeps table / signs / 2x2s as separate
-// dispatches (A/B measurements only).
+// Emits the layer (pre part + 2x2s) as one op; the post part becomes the
+// next layer's pre part.
 void close_layer(LayerState& L, EncRound& out) {
   to_rotations(L);
   fold_signs(L.pre, L.pre_signs);
-  static const bool separate = std::getenv("QTB_NOLAYER") != nullptr;
-  if (L.mmask && !separate) {
+  if (L.mmask) {
     emit_layer(L, out);
   } else {
     emit_table(L.pre, out);
     emit_signs(L.pre_signs, out);
-    if (L.mmask) {
-      std::vector<cplx> one(L.NS, cplx{1.0, 0.0});
-      L.pre.swap(one);
-      L.pre_signs.clear();
-      emit_layer(L, out);
-      L.pre.swap(one);
-    }
   }
   L.pre.swap(L.post);
   L.pre_signs.swap(L.post_signs);
@@ -764,10 +752,7 @@ void make_rounds(PlanPass& pass, int R, int nphys, const PlanOptions& opt, bool 
   for (int i = 0; i < k; ++i) tix[pass.tile_phys[i]] = i;
   std::vector<int> remaining(pass.ops.size());
   for (size_t i = 0; i < remaining.size(); ++i) remaining[i] = static_cast<int>(i);
-  static const int kCand = [] {
-    const char* e = std::getenv("QTB_ROUND_CAND");  // tuning only; <= R: plain greedy
-    return e ? std::atoi(e) : 8;
-  }();
+  constexpr int kCand = 8;  // candidate register bits (at most 70 R-subsets for R = 4)
   PlanRound best, trial;
   std::vector<int> best_rest, trial_rest;
   QR rl[3];
