@@ -362,7 +362,8 @@ def main():
                      "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms},
         "roofline_fp64": {"achieved_dfma_per_s": fp64_achieved, "peak_dfma_per_s": fp64_peak,
                           "frac": fp64_achieved / fp64_peak if fp64_peak else None,
-                          "note": "DFMA-pipe instructions (complex 2x2 = 8/amp, real = 4/amp); "
+                          "note": "DFMA-pipe instructions of the encoded ops (complex 2x2 = 8/amp, "
+                                  "real rotation = 3/amp as shears, diagonal table = 4/amp); "
                                   "peak from an FMA-chain probe on this GPU"},
         "e2e": {"value": e2e_steps * G * amps / e2e_sec, "unit": UNIT,
                 "h2d_bytes_per_step": int(w.gates.nbytes),
