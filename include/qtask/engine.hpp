@@ -93,6 +93,10 @@ class CircuitView {
 class Simulator {
  public:
   explicit Simulator(int num_qubits, Config cfg = Config{}) : cfg_(cfg) {
+    // validate_config (plan.cpp:7-13): the C ABI reads 0 as "default", the
+    // reference rejects it like any non power of two
+    if (cfg.block_size < 2 || (cfg.block_size & (cfg.block_size - 1)) != 0)
+      throw Error("block size must be a power of two >= 2");
     qt_config c{};
     c.block_size = cfg.block_size;
     c.threads = cfg.threads;

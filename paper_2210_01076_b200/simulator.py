@@ -20,6 +20,7 @@ import numpy as np
 
 from . import _ffi
 from ._ffi import GATE_DTYPE, check, lib
+from .errors import Error
 from .gates import GateKind, is_two_qubit
 
 
@@ -112,6 +113,9 @@ class Simulator:
 
     def __init__(self, num_qubits: int, cfg: Config | None = None):
         cfg = cfg or Config()
+        bs = cfg.block_size
+        if bs < 2 or bs & (bs - 1):  # validate_config (plan.cpp:7-13); the C ABI reads 0 as default
+            raise Error("block size must be a power of two >= 2")
         self._cfg = cfg
         c = _ffi.make_config(cfg.block_size, cfg.threads, cfg.device, cfg.tile_qubits,
                              cfg.max_checkpoints, cfg.checkpoint_fraction, cfg.segment_gates)

@@ -89,3 +89,12 @@ def test_bad_gate_rejected_by_planner():
 def test_gate_struct_layout():
     assert _ffi.GATE_DTYPE.itemsize == 40
     assert ctypes.sizeof(_ffi.QtConfig) == 48
+
+
+def test_config_block_size_validated_like_the_reference():
+    """validate_config (plan.cpp:7-13): non power of two (incl. 0) -> Error,
+    before any device work."""
+    from paper_2210_01076_b200 import Config, Error, Simulator
+    for bs in (0, 1, 3, 384):
+        with pytest.raises(Error):
+            Simulator(4, Config(block_size=bs))
