@@ -61,22 +61,20 @@ enum DType : uint32_t {
   D_ANTI = 5,    // scaled swap [[0,m01],[m10,0]] on slot a    (4 DFMA/amp)
   D_SWAP2 = 6,   // swap qubits on reg slots a and b
   D_PHASE1 = 7,  // multiply by d1 where bit set (S, T, phase) (4 DFMA/amp)
-  // fused layer ops built by the round compiler (qt_plan.cpp)
-  D_MULTI = 8,   // retired: complex layers are MULTIR layers with an lmask
-  D_MULTIR = 9,  // a LAYER: [diag table if kOpTable][sign terms: base mask dl,
-                 // arg >> 16 conditional terms][a real rotation [[c,-s],[s,c]]
-                 // (2 doubles) on every reg slot in mask a][a complex 2x2
-                 // (8 doubles) on every reg slot in lmask], ascending slots
-  // (a lone diagonal table or sign op is a MULTIR layer with an empty mask)
-  D_DTAB = 10,   // retired: was a separate table op
-  D_STAB = 11,   // retired: was a separate sign-term op
+  // the fused LAYER op built by the round compiler (qt_plan.cpp): [diag table
+  // if kOpTable][sign terms: base mask dl, arg >> 16 conditional terms][a
+  // real rotation (2 doubles: three-shear form) on every reg slot in mask a]
+  // [a complex 2x2 (8 doubles) on every reg slot in lmask], ascending slots.
+  // A lone diagonal table or sign op is a layer with empty masks.
+  D_LAYER = 9,
+  // (8, 10, 11: retired op types, kept unused so ids stay stable)
 };
 
 // Variant id of a device op: the kernel dispatches on it to a fully
 // specialised code path (register slots known at compile time, no per-slot
 // predication). cs / ds are -1 when the control / diagonal target is not a
-// register bit of the round; SWAP2 stores its second slot in ds; MULTI /
-// MULTIR store their slot mask in a.
+// register bit of the round; SWAP2 stores its second slot in ds; D_LAYER
+// stores its rotation-slot mask in a.
 constexpr uint32_t vid(uint32_t type, int a, int cs, int ds) {
   return (type << 10) | (uint32_t(a) << 6) | (uint32_t(cs + 1) << 3) | uint32_t(ds + 1);
 }
@@ -90,13 +88,13 @@ constexpr uint32_t kOpDg = 1u << 19;    // dg != 0
 constexpr uint32_t kOpFlagMask = kOpLctl | kOpGctl | kOpDl | kOpDg;
 // dense dispatch index of the variant (tools/gen_variants.py) in bits 20..27
 constexpr uint32_t kOpIndexShift = 20;
-constexpr uint32_t kOpTable = 1u << 28;  // MULTI/MULTIR: a 2^R-entry table leads the pool data
+constexpr uint32_t kOpTable = 1u << 28;  // D_LAYER: a 2^R-entry table leads the pool data
 
 // 32 bytes; lives in the kernel-parameter constant bank (read uniformly).
 // Matrices / tables / sign terms are in the pass's double pool at `arg`.
 struct alignas(8) DOp {
   uint32_t hdr;      // vid(type, a, cs, ds) | flags
-  uint32_t arg;      // pool offset (doubles); STAB / MULTI*: offset | nterms << 16
+  uint32_t arg;      // pool offset (doubles); D_LAYER: offset | nterms << 16
   uint32_t lmask;    // control bits among the round's NON-register tile bits
   uint32_t dl;       // diag target among non-register tile bits (mask) or 0
   uint64_t gmask;    // control bits outside the tile (global index bits)
@@ -104,7 +102,7 @@ struct alignas(8) DOp {
 };
 static_assert(sizeof(DOp) == 32, "DOp layout");
 
-// One sign term of a D_STAB op (two pool words): negate the register slots
+// One sign term of a D_LAYER op (two pool words): negate the register slots
 // in `slots` when (j & lcond) == lcond and (g & gcond) == gcond.
 struct SignTerm {
   uint32_t slots;    // bit s set: slot s is negated

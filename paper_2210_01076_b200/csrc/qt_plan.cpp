@@ -390,7 +390,7 @@ bool table_trivial(const std::vector<cplx>& t) {
 void emit_table(const std::vector<cplx>& t, EncRound& out) {
   if (table_trivial(t)) return;
   DOp d{};
-  d.hdr = vid(D_MULTIR, 0, -1, -1) | kOpTable;  // a layer with no 2x2s
+  d.hdr = vid(D_LAYER, 0, -1, -1) | kOpTable;  // a layer with no 2x2s
   d.arg = static_cast<uint32_t>(out.pool.size());
   for (const cplx& c : t) {
     out.pool.push_back(c.re);
@@ -412,7 +412,7 @@ void emit_signs(const std::vector<SignTerm>& terms, EncRound& out) {
   }
   if (base == 0 && cond.empty()) return;
   DOp d{};
-  d.hdr = vid(D_MULTIR, 0, -1, -1);  // a layer with no table and no 2x2s
+  d.hdr = vid(D_LAYER, 0, -1, -1);  // a layer with no table and no 2x2s
   d.dl = base;
   const uint32_t off = static_cast<uint32_t>(out.pool.size());
   d.arg = off | (static_cast<uint32_t>(cond.size()) << 16);
@@ -458,7 +458,7 @@ void emit_layer(LayerState& L, EncRound& out) {
     else cond.push_back(t);
   }
   const uint32_t rmask = L.mmask & ~L.cmask;
-  d.hdr = vid(D_MULTIR, static_cast<int>(rmask), -1, -1) |
+  d.hdr = vid(D_LAYER, static_cast<int>(rmask), -1, -1) |
           (tab ? kOpTable : 0u);
   d.dl = base;
   d.arg = static_cast<uint32_t>(out.pool.size()) | (static_cast<uint32_t>(cond.size()) << 16);
@@ -564,7 +564,7 @@ inline bool bit_of(int s, int slot) { return slot >= 0 && ((s >> slot) & 1); }
 void set_dispatch_index(EncRound& out, int R) {
   for (DOp& d : out.ops) {
     const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
-    if (type == D_MULTI || type == D_MULTIR || type == D_XPERM) continue;  // k_layer / k_perm
+    if (type == D_LAYER || type == D_XPERM) continue;  // k_layer / k_perm
     const uint16_t idx = variant_index(R, d.hdr & kOpVariantMask);
     if (idx == 0xffff) throw std::logic_error("device op without a kernel variant");
     d.hdr = (d.hdr & ~(0xffu << kOpIndexShift)) | (static_cast<uint32_t>(idx) << kOpIndexShift);
@@ -1004,8 +1004,8 @@ std::string plan_to_json(const Plan& p, bool detail) {
         switch (type) {
           case D_DENSE: fp += ctl ? 4.0 : 8.0; break;
           case D_REAL: case D_ANTI: fp += ctl ? 2.0 : 4.0; break;
-          case D_DIAG: case D_PHASE1: case D_DTAB: fp += 4.0; break;
-          case D_MULTIR:  // a layer: rotations (a), complex 2x2s (lmask), table
+          case D_DIAG: case D_PHASE1: fp += 4.0; break;
+          case D_LAYER:  // a layer: rotations (a), complex 2x2s (lmask), table
             fp += 3.0 * __builtin_popcount(a) + 8.0 * __builtin_popcount(d.lmask) +
                   ((d.hdr & kOpTable) ? 4.0 : 0.0);
             break;
@@ -1049,19 +1049,6 @@ std::string plan_to_json(const Plan& p, bool detail) {
              << "," << static_cast<int>(v & 7) - 1 << "," << d.lmask << "," << d.gmask
              << "," << d.dl << "," << d.dg << ",[";
           size_t off = d.arg & 0xffff, len = 8;
-          if (type == D_STAB) {
-            const uint32_t nt = d.arg >> 16;
-            os << "[" << d.dl << ",0,0]";  // base mask: unconditional terms
-            for (uint32_t t = 0; t < nt; ++t) {
-              uint64_t w0, w1;
-              std::memcpy(&w0, &pr.enc.pool[off + 2 * t], 8);
-              std::memcpy(&w1, &pr.enc.pool[off + 2 * t + 1], 8);
-              os << ",[" << (w0 & 0xffffffffull) << "," << (w0 >> 32) << ","
-                 << w1 << "]";
-            }
-            os << "]]";
-            continue;
-          }
           const bool tab = (d.hdr & kOpTable) != 0;
           auto put = [&](size_t from, size_t n) {
             for (size_t k = 0; k < n; ++k) {
@@ -1069,7 +1056,7 @@ std::string plan_to_json(const Plan& p, bool detail) {
               os << num;
             }
           };
-          if (type == D_MULTI || type == D_MULTIR) {
+          if (type == D_LAYER) {
             // layer: [..., [2x2 data], tabflag, [table], [[base,0,0], terms...]]
             const uint32_t nt = d.arg >> 16;
             const size_t toff = off, soff = off + (tab ? 2 * NS : 0), moff = soff + 2 * nt;
@@ -1086,7 +1073,6 @@ std::string plan_to_json(const Plan& p, bool detail) {
             os << "]]";
             continue;
           }
-          if (type == D_DTAB) len = 2 * NS;
           put(off, len);
           os << "]," << (tab ? 1 : 0) << "]";
         }

@@ -277,7 +277,7 @@ void fill_pass(P& kp, const PlanPass& ps) {
     for (DOp d : pr.enc.ops) {
       // pool offsets are round-relative: rebase onto the launch's pool
       const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
-      if (type == D_STAB || type == D_MULTI || type == D_MULTIR)
+      if (type == D_LAYER)
         d.arg = ((d.arg & 0xffff) + npool) | (d.arg & 0xffff0000u);  // offset | nterms << 16
       else d.arg += npool;
       kp.ops[nops++] = d;
@@ -370,7 +370,7 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
         if (type == D_XPERM)  // lean kernel: k_perm (controls: slot / thread / tile bits)
           generic = generic || (d.hdr & (kOpDl | kOpDg)) != 0;
         else
-          generic = generic || type < D_MULTI || (d.hdr & kOpFlagMask) != 0;
+          generic = generic || type != D_LAYER || (d.hdr & kOpFlagMask) != 0;
       }
     }
     const bool large = nops > static_cast<size_t>(kSmallOps) ||

@@ -16,16 +16,19 @@
 //       --> smem --> HBM
 // so a pass costs 32 B of HBM traffic per amplitude however many gates it
 // carries. Device ops live in the kernel-parameter constant bank (headers +
-// a pool of matrices / diagonal tables / sign terms). The host round
-// compiler (qt_plan.cpp) fuses each round into layers: one MULTI op applies
-// a 2x2 on every register slot (real rotations after the ZYZ split), one
-// DTAB op multiplies every amplitude by its merged diagonal factor, one STAB
-// op applies all sign flips (CZ, Z) with integer XORs. Each op is dispatched
-// (one switch per op) to a fully specialised variant: register slots are
-// template parameters, so no per-amplitude predication is executed; controls
-// / diagonal bits outside the register slots are thread- or tile-uniform
+// a pool of tables / rotations / matrices / sign terms). The host round
+// compiler (qt_plan.cpp) turns each round into LAYER ops: a diagonal table
+// over the round's register slots (every merged diagonal factor), integer
+// sign flips (CZ, Z), then one 2x2 per register slot -- real rotations as
+// three in-place shears after the ZYZ split, complex 2x2s otherwise -- all
+// in one dispatch (k_layer: runtime slot masks over compiled slot bodies).
+// X / CX are register permutations (k_perm). The generic instantiation adds
+// specialised single-op variants (controlled 2x2s, diagonals on
+// non-register bits, SWAP) for what a layer cannot hold. Controls /
+// diagonal bits outside the register slots are thread- or tile-uniform
 // predicates. Tensor cores do not apply (2x2 complex FP64 operands): a pass
-// is bounded by HBM when shallow and by the FP64 pipe when deep.
+// is bounded by HBM when shallow and by the FP64 pipe / issue when deep
+// (DESIGN.md).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -379,7 +382,7 @@ __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const
     k_perm<R>(v, hdr, d, jb, sg);
     return;
   }
-  if (!GENERIC || type == D_MULTI || type == D_MULTIR) {
+  if (!GENERIC || type == D_LAYER) {
     // the fused layer ops carry no flags
     k_layer<R>(v, p, hdr, d.arg, d.dl, d.lmask, jb, sg);
     return;

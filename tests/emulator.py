@@ -11,8 +11,8 @@ import json
 
 import numpy as np
 
-(D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1,
- D_MULTI, D_MULTIR, D_DTAB, D_STAB) = range(12)
+(D_DENSE, D_REAL, D_DIAG, D_SIGN, D_XPERM, D_ANTI, D_SWAP2, D_PHASE1) = range(8)
+D_LAYER = 9
 
 
 def _bit(idx, pos):
@@ -69,7 +69,7 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                 typ, a, cs, ds, lmask, gmask, dl, dg = (int(x) for x in op[:8])
                 data = op[8]
                 b = ds
-                if typ in (D_MULTI, D_MULTIR):
+                if typ == D_LAYER:
                     # a layer: [table][sign terms] then one 2x2 per slot in a
                     # (op[9] table flag, op[10] table, op[11] sign terms)
                     if int(op[9]):
@@ -99,13 +99,6 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                         x, y = psi[lo].copy(), psi[hi].copy()
                         psi[lo] = mm[0] * x + mm[1] * y
                         psi[hi] = mm[2] * x + mm[3] * y
-                    continue
-                if typ == D_DTAB:
-                    tab = np.array(data[0::2]) + 1j * np.array(data[1::2])
-                    psi = psi * tab[slot]
-                    continue
-                if typ == D_STAB:
-                    psi = _signs(psi, data, slot, idx, tile)
                     continue
                 m = np.array(data[0:8], dtype=np.float64)
                 m = m[0::2] + 1j * m[1::2]
