@@ -70,6 +70,29 @@ enum DType : uint32_t {
   // (8, 10, 11: retired op types, kept unused so ids stay stable)
 };
 
+// ---------------------------------------------------------------------------
+// Lean layer words: the lean kernel's instruction stream (qt_micro.cpp
+// lowers the D_LAYER / D_XPERM ops of a pass into them). One uint2 per layer:
+//   x = pool offset (doubles, even) | rotation slots << 16 | 2x2 slots << 20
+//       | flags | table-variant terms << 28
+//   y = unconditional sign-slot mask | conditional sign terms << 16 (M_SIGN),
+//       or the D_XPERM header (M_PERM)
+// Pool data of a layer, in order: [variant conditions (u64 each, padded to
+// even)][2^nv diagonal tables of 2^R entries][sign terms (2 words each)]
+// [(a, b) per rotation slot][8 doubles per 2x2 slot].
+// Table variants: sign terms whose condition is tile-uniform (global bits
+// only) select one of 2^nv precomputed tables instead of flipping signs
+// per amplitude.
+// ---------------------------------------------------------------------------
+constexpr uint32_t M_ROT_SHIFT = 16;     // rotation slot mask (4 bits)
+constexpr uint32_t M_DENSE_SHIFT = 20;   // complex 2x2 slot mask (4 bits)
+constexpr uint32_t M_STAB = 1u << 24;    // table of unit phases as shears (a, b)
+constexpr uint32_t M_CTAB = 1u << 25;    // table as complex multiplies (re, im)
+constexpr uint32_t M_SIGN = 1u << 26;    // sign flips (mask / terms in y)
+constexpr uint32_t M_PERM = 1u << 27;    // X / CX register permutation
+constexpr uint32_t M_NV_SHIFT = 28;      // table-variant terms (2 bits)
+constexpr int kMaxTableVariantTerms = 3;
+
 // Variant id of a device op: the kernel dispatches on it to a fully
 // specialised code path (register slots known at compile time, no per-slot
 // predication). cs / ds are -1 when the control / diagonal target is not a

@@ -26,7 +26,10 @@ struct KPassHead {
   // launch sequence checks: a non-finite amplitude never becomes finite again
   // under the (finite, linear) gate ops, so the final state shows it.
   uint32_t check;
-  uint32_t pad_;
+  // > 0: while a tile is processed, the CTA prefetches its NEXT tile into L2
+  // (cp.async.bulk.prefetch) as runs of 2^pf_bits contiguous amplitudes
+  // (the tile's lowest physical bits are 0 .. pf_bits-1); 0 = off
+  uint32_t pf_bits;
   uint64_t slot_gb[1 << kMaxRegBits];  // byte offset of load slot s (s deposited into hi_mask)
   uint32_t slot_sb[1 << kMaxRegBits];  // swz(s << (k - R)) * 16: smem byte term of slot s
 };
@@ -37,25 +40,33 @@ template <int OPS, int ROUNDS, int POOL>
 struct KPass {
   KPassHead h;
   DRound rounds[ROUNDS];
+  // generic kernel: device ops; lean kernel: the same bytes hold the pass's
+  // micro-ops (uint2, 4 per DOp slot; DRound op_first / op_count index them)
   DOp ops[OPS];
-  double pool[POOL];  // matrices, diagonal tables, sign terms
+  alignas(16) double pool[POOL];  // matrices, diagonal tables, sign terms
 };
 using KPassSmall = KPass<kSmallOps, kSmallRounds, kSmallPool>;
 using KPassLarge = KPass<kLargeOps, kLargeRounds, kLargePool>;
 static_assert(sizeof(KPassLarge) <= 32764, "kernel parameter limit");
+// micro-op capacity of a launch (lean kernel)
+template <typename P>
+constexpr int micro_capacity() { return static_cast<int>(sizeof(P::ops) / 8); }
 
 // Fused tile pass over a state of 2^nlocal amplitudes. generic = false
 // selects the lean instantiation that only handles the fused layer ops
 // (MULTI, MULTIR, DTAB, STAB).
+// pipe = true: the double-buffered instantiation (the next tile is copied
+// into a second smem buffer with cp.async while the current one is worked
+// on; 2x the dynamic shared memory).
 cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool generic,
-                             cudaStream_t s);
+                             bool pipe, cudaStream_t s);
 cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
-                             cudaStream_t s);
+                             bool pipe, cudaStream_t s);
 // Max threads per CTA of the tile-pass kernel for R register bits (its
 // launch bounds): a pass's tile has at most R + log2(this) bits.
 constexpr int tile_max_threads(int R) { return R >= 4 ? 256 : 512; }
 // Max resident CTAs per SM of the tile-pass kernel for (k, R).
-int tile_pass_occupancy(int k, int R, bool large, bool generic);
+int tile_pass_occupancy(int k, int R, bool large, bool generic, bool pipe);
 
 // Sets every amplitude to 0 and amplitude `index` to 1.
 cudaError_t launch_set_basis(double2* psi, uint64_t n, uint64_t index,

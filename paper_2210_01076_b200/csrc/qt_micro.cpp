@@ -1,0 +1,267 @@
+// qt_micro.cpp -- lean-kernel layer-word lowering (see qt_micro.hpp).
+#include "qt_micro.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace qtb {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+// largest shear factor |tan(phi/2)| accepted for a table entry (|phi| <=
+// ~0.94 pi); beyond it the table stays complex multiplies
+constexpr double kMaxShear = 12.0;
+
+bool is_layer_lean(const DOp& d) {
+  const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
+  if (type == D_XPERM) return (d.hdr & (kOpDl | kOpDg)) == 0;
+  return type == D_LAYER && (d.hdr & kOpFlagMask) == 0;
+}
+
+double bits_as_double(uint64_t w) {
+  double d;
+  std::memcpy(&d, &w, 8);
+  return d;
+}
+
+// A table's place in the lowered plan, for the final scalar fold.
+struct TableRef {
+  size_t pass = 0, word = 0, pool = 0;
+  std::vector<cplx> phases;  // every variant's centred entries, in pool order
+};
+
+// Centres the angles of all entries (every variant of a table): returns
+// false (keep complex multiplies) when an entry is not a unit phase or the
+// centred angles need shear factors above kMaxShear.
+bool centre_tables(std::vector<cplx>& t, cplx& removed) {
+  const size_t n = t.size();
+  std::vector<double> ang(n);
+  for (size_t s = 0; s < n; ++s) {
+    const double r = std::hypot(t[s].re, t[s].im);
+    if (!(std::fabs(r - 1.0) <= 1e-12)) return false;
+    ang[s] = std::atan2(t[s].im, t[s].re);
+  }
+  std::vector<double> srt(ang);
+  std::sort(srt.begin(), srt.end());
+  // largest circular gap between consecutive angles
+  double best = srt.front() + 2.0 * kPi - srt.back(), mid = srt.back() + 0.5 * best;
+  for (size_t s = 1; s < n; ++s) {
+    const double gap = srt[s] - srt[s - 1];
+    if (gap > best) {
+      best = gap;
+      mid = srt[s - 1] + 0.5 * gap;
+    }
+  }
+  if (std::tan(0.5 * (kPi - 0.5 * best)) > kMaxShear) return false;
+  const double gamma = mid + kPi;  // opposite the gap's middle
+  removed = cplx{std::cos(gamma), std::sin(gamma)};
+  const cplx inv{removed.re, -removed.im};
+  for (size_t s = 0; s < n; ++s) t[s] = cmul(t[s], inv);
+  return true;
+}
+
+void push_shear(std::vector<double>& pool, const cplx& t) {
+  // e^{i phi}: re += a im; im += b re; re += a im, a = -tan(phi/2), b = sin(phi)
+  const double phi = std::atan2(t.im, t.re);
+  pool.push_back(-std::tan(0.5 * phi));
+  pool.push_back(std::sin(phi));
+}
+
+void pad_even(std::vector<double>& pool) {
+  if (pool.size() & 1) pool.push_back(0.0);
+}
+
+}  // namespace
+
+bool pass_is_lean(const PlanPass& ps) {
+  if (ps.kind != PlanPass::Tile) return false;
+  for (const PlanRound& pr : ps.rounds)
+    for (const DOp& d : pr.enc.ops)
+      if (!is_layer_lean(d)) return false;
+  return true;
+}
+
+std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const MicroLimits& lim) {
+  std::vector<MicroPass> out(plan.passes.size());
+  cplx carried{1.0, 0.0};
+  TableRef last;
+  bool have_last = false;
+  for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
+    const PlanPass& ps = plan.passes[pi];
+    if (!pass_is_lean(ps)) continue;
+    const int R = std::min<int>(reg_bits, static_cast<int>(ps.tile_phys.size()));
+    const int NS = 1 << R;
+    MicroPass& mp = out[pi];
+    std::vector<double>& P = mp.pool;
+    bool ok = true;
+    cplx pass_carried = carried;
+    TableRef pass_last = last;
+    bool pass_have_last = have_last;
+    for (const PlanRound& pr : ps.rounds) {
+      if (static_cast<int>(pr.reg.size()) != R) {
+        ok = false;
+        break;
+      }
+      mp.round_first.push_back(static_cast<uint16_t>(mp.size()));
+      for (const DOp& d : pr.enc.ops) {
+        const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
+        const double* src = pr.enc.pool.data();
+        pad_even(P);
+        const uint32_t off = static_cast<uint32_t>(P.size());
+        if (type == D_XPERM) {
+          P.push_back(bits_as_double(d.lmask));
+          P.push_back(bits_as_double(d.gmask));
+          mp.words.push_back(off | M_PERM);
+          mp.words.push_back(d.hdr);
+          continue;
+        }
+        // D_LAYER pool: [table 2 NS][terms 2 nt][rotations 2 each][2x2s 8 each]
+        size_t o = d.arg & 0xffffu;
+        const uint32_t nt = d.arg >> 16;
+        const bool tab = (d.hdr & kOpTable) != 0;
+        std::vector<cplx> t;
+        if (tab) {
+          t.resize(NS);
+          for (int s = 0; s < NS; ++s) t[s] = cplx{src[o + 2 * s], src[o + 2 * s + 1]};
+          o += 2 * NS;
+        }
+        std::vector<SignTerm> gterms, lterms;
+        for (uint32_t k = 0; k < nt; ++k) {
+          uint64_t w0, w1;
+          std::memcpy(&w0, &src[o + 2 * k], 8);
+          std::memcpy(&w1, &src[o + 2 * k + 1], 8);
+          SignTerm st{static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32), w1};
+          (st.lcond == 0 && tab ? gterms : lterms).push_back(st);
+        }
+        o += 2 * nt;
+        uint32_t base = d.dl;
+        if (static_cast<int>(gterms.size()) > kMaxTableVariantTerms) {
+          lterms.insert(lterms.end(), gterms.begin(), gterms.end());
+          gterms.clear();
+        }
+        uint32_t x = off;
+        if (tab) {
+          // unconditional flips join the table; tile-uniform terms make
+          // 2^nv variants of it
+          for (int s = 0; s < NS; ++s)
+            if ((base >> s) & 1u) t[s] = cplx{-t[s].re, -t[s].im};
+          base = 0;
+          const size_t nv = gterms.size();
+          std::vector<cplx> all(NS << nv);
+          for (size_t v = 0; v < (size_t(1) << nv); ++v)
+            for (int s = 0; s < NS; ++s) {
+              cplx c = t[s];
+              for (size_t j = 0; j < nv; ++j)
+                if (((v >> j) & 1u) && ((gterms[j].slots >> s) & 1u)) c = cplx{-c.re, -c.im};
+              all[v * NS + s] = c;
+            }
+          for (const SignTerm& g : gterms) P.push_back(bits_as_double(g.gcond));
+          pad_even(P);
+          const size_t toff = P.size();
+          bool scalar = nv == 0;
+          for (int s = 1; s < NS && scalar; ++s)
+            scalar = t[s].re == t[0].re && t[s].im == t[0].im;
+          cplx removed;
+          if (scalar) {
+            // a pure scalar: carried, no table at all
+            pass_carried = cmul(pass_carried, t[0]);
+            P.resize(off);
+          } else if (centre_tables(all, removed)) {
+            pass_carried = cmul(pass_carried, removed);
+            for (const cplx& c : all) push_shear(P, c);
+            pass_last = TableRef{pi, mp.words.size(), toff, all};
+            pass_have_last = true;
+            x |= M_STAB | (static_cast<uint32_t>(nv) << M_NV_SHIFT);
+          } else {
+            for (const cplx& c : all) {
+              P.push_back(c.re);
+              P.push_back(c.im);
+            }
+            x |= M_CTAB | (static_cast<uint32_t>(nv) << M_NV_SHIFT);
+          }
+        }
+        uint32_t y = 0;
+        if (base || !lterms.empty()) {
+          if (lterms.size() > 0xffffu) {
+            ok = false;
+            break;
+          }
+          for (const SignTerm& st : lterms) {
+            const uint64_t w0 = static_cast<uint64_t>(st.slots) |
+                                (static_cast<uint64_t>(st.lcond) << 32);
+            P.push_back(bits_as_double(w0));
+            P.push_back(bits_as_double(st.gcond));
+          }
+          x |= M_SIGN;
+          y = base | (static_cast<uint32_t>(lterms.size()) << 16);
+        }
+        const uint32_t rmask = (d.hdr >> 6) & 15u;
+        for (int a = 0; a < R; ++a) {
+          if (!(rmask & (1u << a))) continue;
+          P.push_back(src[o]);
+          P.push_back(src[o + 1]);
+          o += 2;
+        }
+        for (int a = 0; a < R; ++a) {
+          if (!(d.lmask & (1u << a))) continue;
+          for (int k = 0; k < 8; ++k) P.push_back(src[o + k]);
+          o += 8;
+        }
+        x |= (rmask << M_ROT_SHIFT) | ((d.lmask & 15u) << M_DENSE_SHIFT);
+        if ((x & ~0xffffu) == 0) {
+          P.resize(off);  // nothing left (a scalar table)
+          continue;
+        }
+        mp.words.push_back(x);
+        mp.words.push_back(y);
+      }
+      if (!ok) break;
+      mp.round_count.push_back(
+          static_cast<uint16_t>(mp.size() - mp.round_first.back()));
+    }
+    if (!ok || P.size() > std::min<size_t>(0xffffu, lim.pool) || mp.size() > lim.ops ||
+        ps.rounds.size() > lim.rounds) {
+      out[pi] = MicroPass{};  // the generic kernel runs this pass
+      continue;
+    }
+    mp.ok = true;
+    carried = pass_carried;
+    last = std::move(pass_last);
+    have_last = pass_have_last;
+  }
+  if (carried.re == 1.0 && carried.im == 0.0) return out;
+  if (have_last) {
+    // the plan's last shear table absorbs every removed scalar: it becomes
+    // complex multiplies with the scalar folded in
+    MicroPass& mp = out[last.pass];
+    mp.words[last.word] = (mp.words[last.word] & ~M_STAB) | M_CTAB;
+    for (size_t s = 0; s < last.phases.size(); ++s) {
+      const cplx c = cmul(last.phases[s], carried);
+      mp.pool[last.pool + 2 * s] = c.re;
+      mp.pool[last.pool + 2 * s + 1] = c.im;
+    }
+    return out;
+  }
+  // only scalar tables were seen: one complex table of the scalar joins the
+  // last lowered round
+  for (size_t pi = out.size(); pi-- > 0;) {
+    MicroPass& mp = out[pi];
+    if (!mp.ok || mp.round_count.empty()) continue;
+    const int R = std::min<int>(reg_bits, static_cast<int>(plan.passes[pi].tile_phys.size()));
+    pad_even(mp.pool);
+    const uint32_t off = static_cast<uint32_t>(mp.pool.size());
+    for (int s = 0; s < (1 << R); ++s) {
+      mp.pool.push_back(carried.re);
+      mp.pool.push_back(carried.im);
+    }
+    mp.words.push_back(off | M_CTAB);
+    mp.words.push_back(0);
+    mp.round_count.back() += 1;
+    return out;
+  }
+  return out;
+}
+
+}  // namespace qtb

@@ -9,6 +9,7 @@
 // std::complex<double>); gate application is a sequence of fused tile passes
 // launched in order on one CUDA stream.
 #include "qt_state.hpp"
+#include "qt_micro.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -73,6 +74,8 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
     opt_.tile_bits = std::min(opt_.tile_bits, opt_.reg_bits + tb);
   }
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("QTB_PIPE")) pipe_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QTB_PF")) pf_ = std::atoi(e) != 0;
 
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaMalloc(&psi_, sizeof(double2) << buf_bits_), "state allocation");
@@ -287,6 +290,38 @@ void fill_pass(P& kp, const PlanPass& ps) {
   kp.h.nops = nops;
 }
 
+// The lean kernel's parameters: rounds index the pass's micro-ops, which
+// occupy the op array's bytes; the pool is the lowered one.
+template <typename P>
+void fill_pass_micro(P& kp, const PlanPass& ps, const MicroPass& mp) {
+  kp.h.nrounds = static_cast<uint32_t>(ps.rounds.size());
+  for (size_t r = 0; r < ps.rounds.size(); ++r) {
+    const PlanRound& pr = ps.rounds[r];
+    DRound& dr = kp.rounds[r];
+    dr = DRound{};
+    dr.op_first = mp.round_first[r];
+    dr.op_count = mp.round_count[r];
+    const size_t nreg = std::min(pr.reg.size(), static_cast<size_t>(kMaxRegBits));
+    std::vector<int> sorted(pr.reg.begin(), pr.reg.begin() + nreg);
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 0; i < nreg; ++i) {
+      dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
+      dr.sreg[i] = static_cast<uint8_t>(sorted[i]);
+      dr.sbit[i] = swz_host(1u << pr.reg[i]) << 4;
+    }
+  }
+  std::memcpy(reinterpret_cast<char*>(kp.ops), mp.words.data(), mp.words.size() * 4);
+  std::memcpy(kp.pool, mp.pool.data(), mp.pool.size() * sizeof(double));
+  kp.h.nops = static_cast<uint32_t>(mp.size());
+}
+
+template <typename P>
+bool micro_fits(const PlanPass& ps, const MicroPass& mp) {
+  return mp.ok && mp.size() <= static_cast<size_t>(micro_capacity<P>()) &&
+         mp.pool.size() <= sizeof(P::pool) / sizeof(double) &&
+         ps.rounds.size() <= sizeof(P::rounds) / sizeof(DRound);
+}
+
 }  // namespace
 
 void State::upload_and_launch(const Plan& plan, const double2* src) {
@@ -320,6 +355,11 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
   }
   if (!kp_small_) kp_small_.reset(new KPassSmall);
   if (!kp_large_) kp_large_.reset(new KPassLarge);
+  const std::vector<MicroPass> micro = lower_plan_micro(
+      plan, opt_.reg_bits,
+      MicroLimits{static_cast<size_t>(micro_capacity<KPassLarge>()),
+                  sizeof(KPassLarge::pool) / sizeof(double),
+                  sizeof(KPassLarge::rounds) / sizeof(DRound)});
   size_t last_tile = plan.passes.size();
   for (size_t pi = 0; pi < plan.passes.size(); ++pi)
     if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
@@ -350,6 +390,13 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     }
     h.outer_mask = buf_mask & ~tile_mask;
     h.check = pi == last_tile ? 1u : 0u;
+    if (pf_) {
+      // contiguous low run of the tile (physical bits 0, 1, ...), within the
+      // thread bits so a run starts at a thread's slot
+      int run = 0;
+      while (run < k - R && ps.tile_phys[run] == run) ++run;
+      h.pf_bits = static_cast<uint32_t>(run);
+    }
     for (uint32_t s = 0; s < (1u << R); ++s) {
       uint64_t off = 0;
       for (int i = 0; i < R; ++i)
@@ -359,35 +406,39 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     }
     h.ntiles = 1ull << (buf_bits_ - k);
     h.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
-    size_t nops = 0, npool = 0;
-    bool generic = false;  // any single-gate op -> the full-dispatch kernel
-    for (const PlanRound& pr : ps.rounds) {
-      nops += pr.enc.ops.size();
-      npool += pr.enc.pool.size();
-      for (const DOp& d : pr.enc.ops)
-      {
-        const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
-        if (type == D_XPERM)  // lean kernel: k_perm (controls: slot / thread / tile bits)
-          generic = generic || (d.hdr & (kOpDl | kOpDg)) != 0;
-        else
-          generic = generic || type != D_LAYER || (d.hdr & kOpFlagMask) != 0;
+    // lean kernel (micro-ops) when the pass lowered and fits a launch;
+    // otherwise the generic kernel decodes the device ops
+    const MicroPass& mp = micro[pi];
+    bool generic = !(micro_fits<KPassSmall>(ps, mp) || micro_fits<KPassLarge>(ps, mp));
+    bool large;
+    if (!generic) {
+      large = !micro_fits<KPassSmall>(ps, mp);
+    } else {
+      size_t nops = 0, npool = 0;
+      for (const PlanRound& pr : ps.rounds) {
+        nops += pr.enc.ops.size();
+        npool += pr.enc.pool.size();
       }
+      large = nops > static_cast<size_t>(kSmallOps) ||
+              npool > static_cast<size_t>(kSmallPool) ||
+              ps.rounds.size() > static_cast<size_t>(kSmallRounds);
     }
-    const bool large = nops > static_cast<size_t>(kSmallOps) ||
-                       npool > static_cast<size_t>(kSmallPool) ||
-                       ps.rounds.size() > static_cast<size_t>(kSmallRounds);
-    const int occ = std::max(1, tile_pass_occupancy(k, R, large, generic));
+    int occ_pipe = pipe_ ? tile_pass_occupancy(k, R, large, generic, true) : 0;
+    const bool pipe = occ_pipe > 0;
+    const int occ = std::max(1, pipe ? occ_pipe : tile_pass_occupancy(k, R, large, generic, false));
     const uint64_t cap = static_cast<uint64_t>(occ) * sms_;
     const int grid = static_cast<int>(std::min<uint64_t>(h.ntiles, cap));
     tstart(0);
     if (large) {
       kp_large_->h = h;
-      fill_pass(*kp_large_, ps);
-      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, generic, stream_), "tile pass launch");
+      if (generic) fill_pass(*kp_large_, ps);
+      else fill_pass_micro(*kp_large_, ps, mp);
+      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, generic, pipe, stream_), "tile pass launch");
     } else {
       kp_small_->h = h;
-      fill_pass(*kp_small_, ps);
-      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, generic, stream_), "tile pass launch");
+      if (generic) fill_pass(*kp_small_, ps);
+      else fill_pass_micro(*kp_small_, ps, mp);
+      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, generic, pipe, stream_), "tile pass launch");
     }
     tstop();
     stats.passes += 1;

@@ -126,6 +126,10 @@ class State {
   std::map<int, std::pair<double2*, std::vector<int>>> ckpt_;
   std::unique_ptr<Comm> comm_;
   PlanOptions opt_;
+  // tile-pass streaming mode: double-buffered cp.async (pipe_) and / or L2
+  // prefetch of the next tile (pf_); QTB_PIPE / QTB_PF override
+  bool pipe_ = false;
+  bool pf_ = false;
   int occupancy_ = 1, sms_ = 148;
   bool timing_ = false;
   std::vector<PassTiming> timings_;

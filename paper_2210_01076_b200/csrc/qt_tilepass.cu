@@ -402,6 +402,103 @@ __device__ __forceinline__ void apply_op(double2 (&v)[1 << R], const P& p, const
 #include "qt_variants.inc"
 }
 
+// ---- lean kernel: layer-word interpreter (qt_micro.cpp lowers the layers) ----
+
+// diagonal table of unit phases: each e^{i phi_s} rotates (re, im) by three
+// in-place shears (a, b) = (-tan(phi/2), sin(phi)), |phi| well inside pi
+template <int R>
+__device__ __forceinline__ void m_stab(double2 (&v)[1 << R], const double2* t) {
+#pragma unroll
+  for (int s = 0; s < (1 << R); ++s) {
+    const double2 ab = t[s];
+    v[s].x = fma(ab.x, v[s].y, v[s].x);
+    v[s].y = fma(ab.y, v[s].x, v[s].y);
+    v[s].x = fma(ab.x, v[s].y, v[s].x);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void m_ctab(double2 (&v)[1 << R], const double2* t) {
+#pragma unroll
+  for (int s = 0; s < (1 << R); ++s) {
+    const double2 c = t[s];
+    cscale(v[s], c.x, c.y);
+  }
+}
+
+template <int R, int A>
+__device__ __forceinline__ void m_rots(double2 (&v)[1 << R], const double2*& q, uint32_t x) {
+  if constexpr (A < R) {
+    if (x & (1u << (M_ROT_SHIFT + A))) {
+      const double2 ab = *q++;
+      pair_shear<R, A>(v, ab.x, ab.y);
+    }
+    m_rots<R, A + 1>(v, q, x);
+  }
+}
+
+template <int R, int A>
+__device__ __forceinline__ void m_denses(double2 (&v)[1 << R], const double2*& q, uint32_t x) {
+  if constexpr (A < R) {
+    if (x & (1u << (M_DENSE_SHIFT + A))) {
+      const double2 m0 = q[0], m1 = q[1], m2 = q[2], m3 = q[3];
+      q += 4;
+      pair_dense<R, A, -1>(v, m0.x, m0.y, m1.x, m1.y, m2.x, m2.y, m3.x, m3.y);
+    }
+    m_denses<R, A + 1>(v, q, x);
+  }
+}
+
+// Runs the layer words [o, o1) of a round. Each word's flag bits select the
+// compiled bodies: [table (variant chosen by tile-uniform conditions)]
+// [sign flips][rotation per slot][complex 2x2 per slot] (qt_ir.hpp).
+template <int R, typename P>
+__device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uint32_t o,
+                                           uint32_t o1, uint32_t jb, const uint64_t* sg) {
+  constexpr int NS = 1 << R;
+  const uint2* mw = reinterpret_cast<const uint2*>(p.ops);
+  const double2* pl = reinterpret_cast<const double2*>(p.pool);
+  for (; o < o1; ++o) {
+    const uint2 w = mw[o];
+    const uint32_t x = w.x;
+    uint32_t off = x & 0xffffu;  // doubles, even
+    if (x & M_PERM) {
+      DOp d{};
+      d.lmask = static_cast<uint32_t>(__double_as_longlong(p.pool[off]));
+      d.gmask = static_cast<uint64_t>(__double_as_longlong(p.pool[off + 1]));
+      k_perm<R>(v, w.y, d, jb, sg);
+      continue;
+    }
+    if (x & (M_STAB | M_CTAB)) {
+      const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
+      uint32_t vi = 0;
+      if (nv) {
+        const uint64_t g = *sg;
+#pragma unroll
+        for (uint32_t j = 0; j < kMaxTableVariantTerms; ++j) {
+          if (j < nv) {
+            const uint64_t gc = static_cast<uint64_t>(__double_as_longlong(p.pool[off + j]));
+            vi |= ((g & gc) == gc ? 1u : 0u) << j;
+          }
+        }
+        off += (nv + 1) & ~1u;
+      }
+      const double2* t = pl + (off >> 1) + vi * NS;
+      if (x & M_STAB) m_stab<R>(v, t);
+      else m_ctab<R>(v, t);
+      off += (2 * NS) << nv;
+    }
+    if (x & M_SIGN) {
+      const uint32_t nt = w.y >> 16;
+      apply_signs<R>(v, p, static_cast<int>(off), nt, w.y & 0xffffu, jb, sg);
+      off += 2 * nt;
+    }
+    const double2* q = pl + (off >> 1);
+    m_rots<R, 0>(v, q, x);
+    if (x & (15u << M_DENSE_SHIFT)) m_denses<R, 0>(v, q, x);
+  }
+}
+
 // R = 3: 8 amplitudes per thread in registers, up to 512 threads (2^12
 // tiles) at <= 64 registers (32 warps per SM); R = 4: 16 amplitudes per
 // thread, up to 256 threads (2^12 tiles) at <= 128 registers. The kernel is
@@ -412,18 +509,41 @@ constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? 2 : 4);
 template <int R>
 constexpr int kMaxThreads = R >= 4 ? 256 : 512;
 
-// GENERIC = false: the lean instantiation that only knows the fused layer
-// ops (MULTI / MULTIR / DTAB / STAB); every extra variant body costs
-// registers and instruction cache in the hot loop, so passes made only of
-// layer ops (e.g. every pass of config 3) run this one.
-template <int R, bool GENERIC, typename P>
+// async 16-B global -> shared copy (LDGSTS, L1 bypass)
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// bulk L2 prefetch of `bytes` (multiple of 16) at a 16-B aligned address
+__device__ __forceinline__ void prefetch_l2(const void* g, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ uint64_t next_tile_base(uint64_t base, uint64_t outer) {
+  return ((base | ~outer) + 1) & outer;
+}
+
+// GENERIC = false: the lean instantiation: it runs the pass's layer words
+// (qt_micro.cpp: table / sign / per-slot rotation and 2x2 bodies, X / CX
+// permutations); every extra variant body costs registers and
+// instruction cache in the hot loop, so passes made only of layer ops (e.g.
+// every pass of config 3) run this one.
+// PIPE = true: two smem tile buffers; tile i+1 streams in with cp.async
+// (no register staging) while tile i runs its register rounds, so every CTA
+// keeps a tile of loads in flight through its compute phase.
+template <int R, bool GENERIC, bool PIPE, typename P>
 __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
     tile_pass_kernel(double2* psi, const __grid_constant__ P p) {
   extern __shared__ double2 sm[];
   constexpr int NS = 1 << R;
   const KPassHead& h = p.h;
   const uint32_t t = threadIdx.x;
-  char* const smb = reinterpret_cast<char*>(sm);
 
   // global offset of this thread's load slots: tile bits [0, k-R) from the
   // thread index (coalesced: low tile bits are the low physical bits), tile
@@ -433,6 +553,10 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
   // smem byte offset of the thread's slots: swz is GF(2)-linear, so
   // swz(t | s << (k-R)) * 16 = st4 ^ h.slot_sb[s]
   const uint32_t st4 = swz(t) << 4;
+  // L2 prefetch of the next tile: the threads whose low pf_bits are zero
+  // each cover one contiguous run per slot
+  const bool pf_lead = h.pf_bits != 0 && (t & ((1u << h.pf_bits) - 1u)) == 0;
+  const uint32_t pf_bytes = 16u << h.pf_bits;
 
   // per-tile uniform values live in smem while the register rounds run
   __shared__ uint64_t s_tile[2];  // [0] tile base, [1] global base (+ rank bits)
@@ -443,18 +567,46 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
   const uint64_t t0 = uint64_t(blockIdx.x) * per;
   const uint64_t t1 = t0 + per < h.ntiles ? t0 + per : h.ntiles;
   uint64_t base = pdep64(t0, h.outer_mask);
+  const uint32_t sm0 = static_cast<uint32_t>(__cvta_generic_to_shared(sm));
+  const uint32_t tbytes = 16u << h.k;
+  if (PIPE && t0 < t1) {
+    const char* src = reinterpret_cast<const char*>(h.src + base + off_t);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) cp_async16(sm0 + (st4 ^ h.slot_sb[s]), src + h.slot_gb[s]);
+    cp_async_commit();
+  }
+  uint32_t cur = 0;  // PIPE: byte offset of the current buffer
   bool bad = false;
   for (uint64_t tile = t0; tile < t1; ++tile) {
+    char* const smb = reinterpret_cast<char*>(sm) + cur;
     if (t == 0) {
       s_tile[0] = base;
       s_tile[1] = h.gbase_hi | base;
     }
-    {
+    if (PIPE) {
+      if (tile + 1 < t1) {
+        const char* src = reinterpret_cast<const char*>(
+            h.src + next_tile_base(base, h.outer_mask) + off_t);
+        const uint32_t nb = sm0 + (cur ^ tbytes);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) cp_async16(nb + (st4 ^ h.slot_sb[s]), src + h.slot_gb[s]);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+    } else {
       const char* src = reinterpret_cast<const char*>(h.src + base + off_t);
       double2 ld[NS];
 #pragma unroll
       for (int s = 0; s < NS; ++s)
         ld[s] = __ldcs(reinterpret_cast<const double2*>(src + h.slot_gb[s]));
+      if (pf_lead && tile + 1 < t1) {
+        const char* nsrc = reinterpret_cast<const char*>(
+            h.src + next_tile_base(base, h.outer_mask) + off_t);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) prefetch_l2(nsrc + h.slot_gb[s], pf_bytes);
+      }
 #pragma unroll
       for (int s = 0; s < NS; ++s)
         *reinterpret_cast<double2*>(smb + (st4 ^ h.slot_sb[s])) = ld[s];
@@ -479,14 +631,18 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
         v[s] = *reinterpret_cast<const double2*>(smb + a);
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
-      // the next op's header is loaded while the current op runs (the
-      // dispatch chain of an op starts from it; the op array always has a
-      // readable slot after the last op: pool data follows it)
-      uint32_t hdr = p.ops[rd.op_first].hdr;
-      for (uint32_t o = rd.op_first; o < o1; ++o) {
-        const uint32_t hdr_next = p.ops[o + 1].hdr;
-        apply_op<R, GENERIC>(v, p, p.ops[o], hdr, jb, &s_tile[1]);
-        hdr = hdr_next;
+      if constexpr (!GENERIC) {
+        run_layers<R>(v, p, rd.op_first, o1, jb, &s_tile[1]);
+      } else {
+        // the next op's header is loaded while the current op runs (the
+        // dispatch chain of an op starts from it; the op array always has a
+        // readable slot after the last op: pool data follows it)
+        uint32_t hdr = p.ops[rd.op_first].hdr;
+        for (uint32_t o = rd.op_first; o < o1; ++o) {
+          const uint32_t hdr_next = p.ops[o + 1].hdr;
+          apply_op<R, GENERIC>(v, p, p.ops[o], hdr, jb, &s_tile[1]);
+          hdr = hdr_next;
+        }
       }
       // opaque copy: forces the 2^R store addresses to be regenerated here
       // instead of being kept live (2^R registers) across the op loop
@@ -522,49 +678,63 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
                  *reinterpret_cast<const double2*>(smb + (st4 ^ h.slot_sb[s])));
       }
     }
-    base = ((base | ~h.outer_mask) + 1) & h.outer_mask;
+    base = next_tile_base(base, h.outer_mask);
+    if (PIPE) cur ^= tbytes;
     __syncthreads();  // smem reuse by the next tile
   }
   if (__syncthreads_or(bad) && t == 0) atomicOr(h.flag, 1);
 }
 
-template <typename P, bool G>
+template <typename P, bool G, bool PIPE>
 void* kernel_ptr(int R) {
   switch (R) {
-    case 1: return reinterpret_cast<void*>(&tile_pass_kernel<1, G, P>);
-    case 2: return reinterpret_cast<void*>(&tile_pass_kernel<2, G, P>);
-    case 3: return reinterpret_cast<void*>(&tile_pass_kernel<3, G, P>);
-    default: return reinterpret_cast<void*>(&tile_pass_kernel<4, G, P>);
+    case 1: return reinterpret_cast<void*>(&tile_pass_kernel<1, G, PIPE, P>);
+    case 2: return reinterpret_cast<void*>(&tile_pass_kernel<2, G, PIPE, P>);
+    case 3: return reinterpret_cast<void*>(&tile_pass_kernel<3, G, PIPE, P>);
+    default: return reinterpret_cast<void*>(&tile_pass_kernel<4, G, PIPE, P>);
   }
 }
 
-template <typename P, bool G>
+template <typename P>
+void* kernel_ptr(int R, bool generic, bool pipe) {
+  if (generic) return pipe ? kernel_ptr<P, true, true>(R) : kernel_ptr<P, true, false>(R);
+  return pipe ? kernel_ptr<P, false, true>(R) : kernel_ptr<P, false, false>(R);
+}
+
+template <typename P, bool G, bool PIPE>
 cudaError_t launch(double2* psi, const P& p, int grid, cudaStream_t s) {
-  const size_t smem = sizeof(double2) << p.h.k;
+  const size_t smem = (PIPE ? 2 : 1) * (sizeof(double2) << p.h.k);
   const int threads = 1 << (p.h.k - p.h.reg_bits);
   switch (p.h.reg_bits) {
     case 1:
-      tile_pass_kernel<1, G, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<1, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     case 2:
-      tile_pass_kernel<2, G, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<2, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     case 3:
-      tile_pass_kernel<3, G, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<3, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     default:
-      tile_pass_kernel<4, G, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<4, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
   }
   return cudaGetLastError();
 }
 
+template <typename P>
+cudaError_t launch_any(double2* psi, const P& p, int grid, bool generic, bool pipe,
+                       cudaStream_t s) {
+  if (generic) return pipe ? launch<P, true, true>(psi, p, grid, s) : launch<P, true, false>(psi, p, grid, s);
+  return pipe ? launch<P, false, true>(psi, p, grid, s) : launch<P, false, false>(psi, p, grid, s);
+}
+
 }  // namespace
 
-int tile_pass_occupancy(int k, int R, bool large, bool generic) {
-  // per-device cache: (generic, large, k, R) -> resident CTAs per SM
+int tile_pass_occupancy(int k, int R, bool large, bool generic, bool pipe) {
+  // per-device cache: (pipe, generic, large, k, R) -> resident CTAs per SM
   static thread_local int cache_dev = -1;
-  static thread_local int cache[4][kMaxTileBits + 1][kMaxRegBits + 1];
+  static thread_local int cache[8][kMaxTileBits + 1][kMaxRegBits + 1];
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev != cache_dev) {
@@ -573,36 +743,35 @@ int tile_pass_occupancy(int k, int R, bool large, bool generic) {
         for (int& v : row) v = -1;
     cache_dev = dev;
   }
-  int& slot = cache[(large ? 1 : 0) + (generic ? 2 : 0)][k][R];
+  int& slot = cache[(large ? 1 : 0) + (generic ? 2 : 0) + (pipe ? 4 : 0)][k][R];
   if (slot >= 0) return slot;
-  const size_t smem = sizeof(double2) << k;
+  const size_t smem = (pipe ? 2 : 1) * (sizeof(double2) << k);
   const int threads = 1 << (k - R);
-  void* fn = large ? (generic ? kernel_ptr<KPassLarge, true>(R) : kernel_ptr<KPassLarge, false>(R))
-                   : (generic ? kernel_ptr<KPassSmall, true>(R) : kernel_ptr<KPassSmall, false>(R));
+  void* fn = large ? kernel_ptr<KPassLarge>(R, generic, pipe)
+                   : kernel_ptr<KPassSmall>(R, generic, pipe);
   int occ = 0;
-  // the attribute is per function: always allow the largest tile (2^13)
+  // the attribute is per function: always allow the largest tile (2^13
+  // single-buffered, 2^12 double-buffered)
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(sizeof(double2) << kMaxTileBits)) !=
           cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) !=
           cudaSuccess) {
     cudaGetLastError();
-    occ = 1;
+    occ = 0;
   }
   slot = occ;
   return occ;
 }
 
 cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool generic,
-                             cudaStream_t s) {
-  return generic ? launch<KPassSmall, true>(psi, p, grid, s)
-                 : launch<KPassSmall, false>(psi, p, grid, s);
+                             bool pipe, cudaStream_t s) {
+  return launch_any(psi, p, grid, generic, pipe, s);
 }
 
 cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
-                             cudaStream_t s) {
-  return generic ? launch<KPassLarge, true>(psi, p, grid, s)
-                 : launch<KPassLarge, false>(psi, p, grid, s);
+                             bool pipe, cudaStream_t s) {
+  return launch_any(psi, p, grid, generic, pipe, s);
 }
 
 }  // namespace qtb
