@@ -85,7 +85,10 @@ typedef struct qt_config {
   int32_t max_checkpoints;   /* incremental checkpoint slots (0 = auto)    */
   double checkpoint_fraction;/* share of free HBM for checkpoints (0=auto) */
   int32_t segment_gates;     /* gates per checkpoint segment (0 = auto)    */
-  int32_t reserved[3];
+  int32_t compiled;          /* 1: compile each tile pass into its own
+                                straight-line kernel (NVRTC, cached by
+                                source), for circuits run more than once   */
+  int32_t reserved[2];
 } qt_config;
 
 /* Result of the last qt_apply / update (UpdateStats, engine.hpp:32-39, in
@@ -175,6 +178,19 @@ int qt_plan_json(const qt_state* st, const qt_gate* gates, size_t count,
 int qt_plan_probe(int num_qubits, int global_qubits, int tile_qubits,
                   const qt_gate* gates, size_t count, char* buf, size_t cap,
                   size_t* needed);
+
+/* Compiled-pass probe (no device needed): plans `gates` for a one-GPU state
+ * of num_qubits (tile / register / low-bit settings, 0 = defaults), lowers
+ * every tile pass and generates its compiled kernel; compile != 0 also runs
+ * NVRTC on each. JSON {"passes","lowered","source_bytes","compiled",
+ * "compile_ms","cubin_bytes"}; source_pass >= 0 returns that pass's CUDA
+ * source instead. */
+int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits,
+                 int compile, int source_pass, const qt_gate* gates,
+                 size_t count, char* buf, size_t cap, size_t* needed);
+/* Process-wide compiled-pass statistics (qt_config.compiled states): passes
+ * compiled, compile-cache hits, total NVRTC + load milliseconds. */
+int qt_jit_stats(uint64_t* compiled, uint64_t* cache_hits, double* compile_ms);
 
 /* ======================================================================= */
 /* 2. Incremental simulator: qtask::Simulator (engine.hpp:46-100)          */

@@ -30,7 +30,8 @@ class QtConfig(ctypes.Structure):
                 ("device", ctypes.c_int32), ("tile_qubits", ctypes.c_int32),
                 ("max_checkpoints", ctypes.c_int32),
                 ("checkpoint_fraction", ctypes.c_double),
-                ("segment_gates", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("segment_gates", ctypes.c_int32), ("compiled", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class QtRunStats(ctypes.Structure):
@@ -54,7 +55,7 @@ HEADER_SYMBOLS = [
     "qt_state_create", "qt_state_create_sharded", "qt_state_create_loopback",
     "qt_nccl_unique_id", "qt_state_destroy", "qt_state_num_qubits", "qt_set_basis",
     "qt_write", "qt_read", "qt_apply", "qt_norm_squared", "qt_sync", "qt_last_stats",
-    "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe",
+    "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe", "qt_jit_probe", "qt_jit_stats",
     "qt_sim_create", "qt_sim_destroy", "qt_sim_num_qubits", "qt_sim_block_size",
     "qt_sim_total_blocks", "qt_sim_insert_net_front", "qt_sim_insert_net_back",
     "qt_sim_insert_net_after", "qt_sim_remove_net", "qt_sim_insert_gate",
@@ -95,6 +96,10 @@ _SIGS = {
                        _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
     "qt_plan_probe_ex": ([_c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp, _c.c_size_t,
                           _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
+    "qt_jit_probe": ([_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_int, _vp,
+                      _c.c_size_t, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
+    "qt_jit_stats": ([_c.POINTER(_c.c_uint64), _c.POINTER(_c.c_uint64), _c.POINTER(_c.c_double)],
+                     _c.c_int),
     "qt_state_stream": ([_vp], _vp),
     "qt_set_timing": ([_vp, _c.c_int], _c.c_int),
     "qt_last_timings": ([_vp, _vp, _vp, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
@@ -163,7 +168,7 @@ def check(rc: int) -> int:
 
 
 def make_config(block_size=256, threads=0, device=-1, tile_qubits=0, max_checkpoints=0,
-                checkpoint_fraction=0.0, segment_gates=0) -> QtConfig:
+                checkpoint_fraction=0.0, segment_gates=0, compiled=False) -> QtConfig:
     cfg = QtConfig()
     cfg.block_size = block_size
     cfg.threads = threads
@@ -172,6 +177,7 @@ def make_config(block_size=256, threads=0, device=-1, tile_qubits=0, max_checkpo
     cfg.max_checkpoints = max_checkpoints
     cfg.checkpoint_fraction = checkpoint_fraction
     cfg.segment_gates = segment_gates
+    cfg.compiled = 1 if compiled else 0
     return cfg
 
 
@@ -197,6 +203,27 @@ def plan_probe(n: int, gates, global_qubits: int = 0, tile_qubits: int = 0,
     check(lib().qt_plan_probe_ex(n, global_qubits, tile_qubits, d, g.ctypes.data, len(g),
                                  buf, need.value, ctypes.byref(need)))
     return buf.value.decode()
+
+
+def jit_probe(n: int, gates, tile_qubits: int = 0, reg_bits: int = 0, low_bits: int = 0,
+              compile: bool = False, source_pass: int = -1) -> str:
+    """Host-only compiled-pass probe (JSON stats, or one pass's CUDA source)
+    -- no GPU needed; compile=True runs NVRTC on every pass."""
+    g = gates_array(gates)
+    need = ctypes.c_size_t(0)
+    args = (n, tile_qubits, reg_bits, low_bits, 1 if compile else 0, source_pass, g.ctypes.data, len(g))
+    check(lib().qt_jit_probe(*args, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    check(lib().qt_jit_probe(*args, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
+
+
+def jit_stats() -> dict:
+    """Process-wide compiled-pass statistics: passes compiled, cache hits and
+    total NVRTC + load time."""
+    c, h, ms = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_double(0.0)
+    check(lib().qt_jit_stats(ctypes.byref(c), ctypes.byref(h), ctypes.byref(ms)))
+    return {"compiled": c.value, "cache_hits": h.value, "compile_ms": ms.value}
 
 
 def exchange_schedule(rank: int, nlocal: int, pairs, tmp_amps: int):

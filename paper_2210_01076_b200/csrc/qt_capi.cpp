@@ -6,12 +6,17 @@
 // back onto the reference exception types (types.hpp:21-64).
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
 
 #include "qt_gates.hpp"
+#include "qt_jit.hpp"
 #include "qt_kernels.hpp"
+#include "qt_micro.hpp"
 #include "qt_plan.hpp"
 #include "qt_sim.hpp"
 #include "qt_state.hpp"
@@ -519,3 +524,79 @@ int qt_qasm_build(qt_sim* sim, const char* text, size_t len, int* err_line, int*
 }
 
 }  // extern "C"
+
+int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, int compile,
+                 int source_pass, const qt_gate* gates, size_t count, char* buf, size_t cap,
+                 size_t* needed) {
+  if (!gates && count) return null_arg();
+  return guard([&] {
+    if (num_qubits < 1 || num_qubits > 40) qtb::fail(QT_ERR_BAD_QUBIT, "bad qubit count");
+    std::vector<qtb::LOp> ops;
+    std::string err;
+    for (size_t i = 0; i < count; ++i) {
+      const int rc = qtb::lower_gate(gates[i], num_qubits, static_cast<uint32_t>(i), ops, &err);
+      if (rc != QT_OK) qtb::fail(rc, err);
+    }
+    qtb::fuse_ops(ops, num_qubits);
+    qtb::PlanOptions opt;
+    if (reg_bits > 0) opt.reg_bits = std::min(reg_bits, qtb::kMaxRegBits);
+    if (tile_qubits > 0) opt.tile_bits = std::min(tile_qubits, qtb::kMaxTileBits);
+    if (low_bits > 0) opt.low_bits = low_bits;
+    std::vector<int> perm(num_qubits);
+    for (int q = 0; q < num_qubits; ++q) perm[q] = q;
+    const qtb::Plan p = qtb::make_plan(ops, num_qubits, num_qubits, perm, opt);
+    const std::vector<qtb::MicroPass> mp = qtb::lower_plan_micro(
+        p, opt.reg_bits,
+        qtb::MicroLimits{static_cast<size_t>(qtb::micro_capacity<qtb::KPassLarge>()),
+                         sizeof(qtb::KPassLarge::pool) / sizeof(double),
+                         sizeof(qtb::KPassLarge::rounds) / sizeof(qtb::DRound)});
+    size_t last_tile = p.passes.size();
+    for (size_t i = 0; i < p.passes.size(); ++i)
+      if (p.passes[i].kind == qtb::PlanPass::Tile) last_tile = i;
+    size_t lowered = 0, bytes = 0, compiled = 0, cubin = 0;
+    double ms = 0.0, fp = 0.0;
+    std::string per = "[";
+    for (size_t i = 0; i < p.passes.size(); ++i) {
+      if (!mp[i].ok) continue;
+      ++lowered;
+      const double f = qtb::micro_fp64_per_amp(mp[i], std::min<int>(opt.reg_bits, static_cast<int>(p.passes[i].tile_phys.size())));
+      fp += f;
+      per += (per.size() > 1 ? "," : "") + std::to_string(f);
+      qtb::JitPassSpec sp = qtb::make_jit_spec(p.passes[i], opt.reg_bits, num_qubits, i == last_tile);
+      // the state's tuning overrides (QTB_PIPE / QTB_JIT_MINB), as qt_state.cpp applies them
+      if (const char* e = std::getenv("QTB_PIPE")) sp.pipe = std::atoi(e) != 0 && 2 * (16u << sp.k) <= 200u * 1024u;
+      if (const char* e = std::getenv("QTB_JIT_MINB")) sp.min_blocks = std::atoi(e);
+      const std::string src = qtb::jit_source(sp, mp[i]);
+      if (source_pass >= 0) {
+        if (static_cast<size_t>(source_pass) == i) {
+          copy_out(src, buf, cap, needed);
+          return;
+        }
+        continue;
+      }
+      bytes += src.size();
+      if (compile) {
+        const auto t0 = std::chrono::steady_clock::now();
+        cubin += qtb::jit_compile_cubin(src).size();
+        ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++compiled;
+      }
+    }
+    if (source_pass >= 0) qtb::fail(QT_ERR_ARG, "source_pass is not a lowered tile pass");
+    char js[256];
+    std::snprintf(js, sizeof(js),
+                  "{\"passes\":%zu,\"lowered\":%zu,\"source_bytes\":%zu,\"compiled\":%zu,"
+                  "\"compile_ms\":%.1f,\"cubin_bytes\":%zu,\"fp64_per_amp\":%.1f,",
+                  p.passes.size(), lowered, bytes, compiled, ms, cubin, fp);
+    copy_out(std::string(js) + "\"pass_fp64\":" + per + "]}", buf, cap, needed);
+  });
+}
+
+int qt_jit_stats(uint64_t* compiled, uint64_t* cache_hits, double* compile_ms) {
+  if (!compiled || !cache_hits || !compile_ms) return null_arg();
+  const qtb::JitStats st = qtb::jit_stats();
+  *compiled = st.compiled;
+  *cache_hits = st.cache_hits;
+  *compile_ms = st.compile_ms;
+  return QT_OK;
+}

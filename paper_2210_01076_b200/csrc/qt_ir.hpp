@@ -141,6 +141,11 @@ constexpr int kMaxRegBits = 4;
 // C3 on B200 (the pass is latency-bound, so resident warps win over R = 4).
 constexpr int kDefaultTileBits = 10;
 constexpr int kDefaultRegBits = 3;
+// compiled passes (qt_jit.cpp): R = 4, 2^12-amplitude tiles whose lowest 3
+// physical bits are always in the tile (128-B runs) -- measured best on C3
+constexpr int kJitTileBits = 12;
+constexpr int kJitRegBits = 4;
+constexpr int kJitLowBits = 3;
 
 struct DRound {
   uint16_t op_first;  // into the pass's op array

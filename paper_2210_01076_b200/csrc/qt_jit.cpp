@@ -1,0 +1,532 @@
+// qt_jit.cpp -- compiled tile passes: source generation, NVRTC, cache.
+#include "qt_jit.hpp"
+
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <future>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <thread>
+#include <unordered_map>
+
+#include "qt_gates.hpp"
+
+namespace qtb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Device prelude of every compiled pass (NVRTC has no standard headers).
+// The bodies mirror qt_tilepass.cu; in straight-line code register swaps are
+// plain renames, so no XOR-swap tricks are needed.
+// ---------------------------------------------------------------------------
+const char* kPrelude = R"PRE(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+#define FI __device__ __forceinline__
+FI u64 pdep64(u64 x, u64 mask) {
+  u64 r = 0;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    if (!mask) break;
+    const u64 low = mask & (~mask + 1);
+    if (x & 1) r |= low;
+    x >>= 1;
+    mask ^= low;
+  }
+  return r;
+}
+FI u32 swz(u32 j) { return j ^ ((j >> 3) & 7u) ^ ((j >> 6) & 7u) ^ ((j >> 9) & 7u) ^ ((j >> 12) & 7u); }
+FI u32 insert_zero(u32 x, u32 p) { return ((x >> p) << (p + 1)) | (x & ((1u << p) - 1u)); }
+FI bool finite2(double2 v) {
+  const u32 hx = __double2hiint(v.x), hy = __double2hiint(v.y);
+  return ((hx & 0x7ff00000u) != 0x7ff00000u) && ((hy & 0x7ff00000u) != 0x7ff00000u);
+}
+// x += a y; y += b x; x += a y on the pair (v[s], v[s1])
+FI void shear(double2& x, double2& y, double a, double b) {
+  x.x = fma(a, y.x, x.x); x.y = fma(a, y.y, x.y);
+  y.x = fma(b, x.x, y.x); y.y = fma(b, x.y, y.y);
+  x.x = fma(a, y.x, x.x); x.y = fma(a, y.y, x.y);
+}
+// e^{i phi} on one amplitude as shears of (re, im)
+FI void pshear(double2& v, double a, double b) {
+  v.x = fma(a, v.y, v.x); v.y = fma(b, v.x, v.y); v.x = fma(a, v.y, v.x);
+}
+FI void cscale(double2& x, double br, double bi) {
+  const double p0 = -bi * x.y, p1 = bi * x.x;
+  x.x = fma(br, x.x, p0); x.y = fma(br, x.y, p1);
+}
+FI void dense(double2& a, double2& b, double m0r, double m0i, double m1r, double m1i,
+              double m2r, double m2i, double m3r, double m3i) {
+  const double p0 = fma(m1r, b.x, fma(-m1i, b.y, -m0i * a.y));
+  const double p1 = fma(m1r, b.y, fma(m1i, b.x, m0i * a.x));
+  const double p2 = fma(m2r, a.x, fma(-m2i, a.y, -m3i * b.y));
+  const double p3 = fma(m2r, a.y, fma(m2i, a.x, m3i * b.x));
+  a.x = fma(m0r, a.x, p0); a.y = fma(m0r, a.y, p1);
+  b.x = fma(m3r, b.x, p2); b.y = fma(m3r, b.y, p3);
+}
+FI void swap2(double2& a, double2& b) { const double2 t = a; a = b; b = t; }
+FI void cswap2(double2& a, double2& b, bool c) {
+  const double2 x = a, y = b;
+  a = c ? y : x; b = c ? x : y;
+}
+FI double flipd(double d, u32 sg) { return __hiloint2double(__double2hiint(d) ^ sg, __double2loint(d)); }
+FI void flip2(double2& v, u32 sg) { v.x = flipd(v.x, sg); v.y = flipd(v.y, sg); }
+FI void neg2(double2& v) { flip2(v, 0x80000000u); }
+)PRE";
+
+std::string hexd(double d) {
+  char b[48];
+  std::snprintf(b, sizeof(b), "%a", d);
+  std::string s(b);
+  if (s == "inf" || s == "-inf" || s == "nan" || s == "-nan") throw std::runtime_error("non-finite literal");
+  return s;
+}
+
+std::string hexu(uint64_t x) {
+  char b[32];
+  std::snprintf(b, sizeof(b), "0x%llxull", static_cast<unsigned long long>(x));
+  return b;
+}
+
+uint64_t raw_bits(double d) {
+  uint64_t w;
+  std::memcpy(&w, &d, 8);
+  return w;
+}
+
+// Code of one layer word.
+void emit_word(std::ostringstream& os, int R, uint32_t x, uint32_t y, const std::vector<double>& P) {
+  const int NS = 1 << R;
+  uint32_t off = x & 0xffffu;
+  if (x & M_PERM) {
+    const uint32_t a = (y >> 6) & 15u;
+    const int cs = static_cast<int>((y >> 3) & 7u) - 1;
+    const bool masked = (y & kOpLctl) != 0, gctl = (y & kOpGctl) != 0;
+    const uint64_t lm = raw_bits(P[off]) & 0xffffffffull, gm = raw_bits(P[off + 1]);
+    os << "  {";
+    std::string pre;
+    if (gctl) os << " if ((g & " << hexu(gm) << ") == " << hexu(gm) << ")";
+    os << " {";
+    if (masked) os << " const bool c = (jb & " << lm << "u) == " << lm << "u;";
+    for (int s = 0; s < NS; ++s) {
+      if (s & (1 << a)) continue;
+      if (cs >= 0 && !((s >> cs) & 1)) continue;
+      const int s1 = s | (1 << a);
+      if (masked) os << " cswap2(v" << s << ", v" << s1 << ", c);";
+      else os << " swap2(v" << s << ", v" << s1 << ");";
+    }
+    os << " } }\n";
+    return;
+  }
+  if (x & (M_STAB | M_CTAB)) {
+    const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
+    std::vector<uint64_t> gc(nv);
+    for (uint32_t j = 0; j < nv; ++j) gc[j] = raw_bits(P[off + j]);
+    if (nv) off += (nv + 1) & ~1u;
+    auto table = [&](uint32_t toff) {
+      for (int s = 0; s < NS; ++s) {
+        const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
+        if (x & M_STAB) {
+          if (a == 0.0 && b == 0.0) continue;  // identity entry
+          os << " pshear(v" << s << ", " << hexd(a) << ", " << hexd(b) << ");";
+        } else {
+          if (a == 1.0 && b == 0.0) continue;
+          os << " cscale(v" << s << ", " << hexd(a) << ", " << hexd(b) << ");";
+        }
+      }
+    };
+    if (nv == 0) {
+      os << " ";
+      table(off);
+      os << "\n";
+    } else {
+      os << "  { const u32 vi =";
+      for (uint32_t j = 0; j < nv; ++j)
+        os << (j ? " | " : " ") << "(((g & " << hexu(gc[j]) << ") == " << hexu(gc[j]) << ") ? " << (1u << j)
+           << "u : 0u)";
+      os << ";\n    switch (vi) {\n";
+      for (uint32_t v = 0; v < (1u << nv); ++v) {
+        os << "    case " << v << "u: {";
+        table(off + v * 2 * NS);
+        os << " break; }\n";
+      }
+      os << "    } }\n";
+    }
+    off += (2 * NS) << nv;
+  }
+  if (x & M_SIGN) {
+    const uint32_t nt = y >> 16, base = y & 0xffffu;
+    if (nt == 0) {
+      os << " ";
+      for (int s = 0; s < NS; ++s)
+        if ((base >> s) & 1u) os << " neg2(v" << s << ");";
+      os << "\n";
+    } else {
+      os << "  { u32 m = " << base << "u;";
+      for (uint32_t k = 0; k < nt; ++k) {
+        const uint64_t w0 = raw_bits(P[off + 2 * k]), gcond = raw_bits(P[off + 2 * k + 1]);
+        const uint32_t slots = static_cast<uint32_t>(w0), lc = static_cast<uint32_t>(w0 >> 32);
+        os << " m ^= (";
+        if (lc) os << "(jb & " << lc << "u) == " << lc << "u";
+        if (lc && gcond) os << " && ";
+        if (gcond) os << "(g & " << hexu(gcond) << ") == " << hexu(gcond);
+        if (!lc && !gcond) os << "true";
+        os << ") ? " << slots << "u : 0u;";
+      }
+      for (int s = 0; s < NS; ++s) os << " flip2(v" << s << ", (m << " << (31 - s) << ") & 0x80000000u);";
+      os << " }\n";
+    }
+    off += 2 * nt;
+  }
+  const uint32_t rmask = (x >> M_ROT_SHIFT) & 15u, dmask = (x >> M_DENSE_SHIFT) & 15u;
+  for (int a = 0; a < R; ++a) {
+    if (!(rmask & (1u << a))) continue;
+    const double ca = P[off], cb = P[off + 1];
+    off += 2;
+    os << " ";
+    for (int s = 0; s < NS; ++s) {
+      if (s & (1 << a)) continue;
+      os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << hexd(ca) << ", " << hexd(cb) << ");";
+    }
+    os << "\n";
+  }
+  for (int a = 0; a < R; ++a) {
+    if (!(dmask & (1u << a))) continue;
+    std::string m;
+    for (int k = 0; k < 8; ++k) m += ", " + hexd(P[off + k]);
+    off += 8;
+    os << " ";
+    for (int s = 0; s < NS; ++s) {
+      if (s & (1 << a)) continue;
+      os << " dense(v" << s << ", v" << (s | (1 << a)) << m << ");";
+    }
+    os << "\n";
+  }
+}
+
+// ---- NVRTC (dlopen) --------------------------------------------------------
+struct Nvrtc {
+  decltype(&nvrtcCreateProgram) create = nullptr;
+  decltype(&nvrtcCompileProgram) compile = nullptr;
+  decltype(&nvrtcGetProgramLogSize) logsize = nullptr;
+  decltype(&nvrtcGetProgramLog) log = nullptr;
+  decltype(&nvrtcGetCUBINSize) cubinsize = nullptr;
+  decltype(&nvrtcGetCUBIN) cubin = nullptr;
+  decltype(&nvrtcDestroyProgram) destroy = nullptr;
+  decltype(&nvrtcGetErrorString) errstr = nullptr;
+  std::string why;
+  bool ok = false;
+};
+
+const Nvrtc& nvrtc() {
+  static Nvrtc n = [] {
+    Nvrtc r;
+    void* h = nullptr;
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      r.why = "libnvrtc.so.12 not found";
+      return r;
+    }
+#define QT_SYM(f, s)                                           \
+  r.f = reinterpret_cast<decltype(r.f)>(dlsym(h, #s));         \
+  if (!r.f) {                                                  \
+    r.why = "nvrtc symbol " #s " missing";                     \
+    return r;                                                  \
+  }
+    QT_SYM(create, nvrtcCreateProgram)
+    QT_SYM(compile, nvrtcCompileProgram)
+    QT_SYM(logsize, nvrtcGetProgramLogSize)
+    QT_SYM(log, nvrtcGetProgramLog)
+    QT_SYM(cubinsize, nvrtcGetCUBINSize)
+    QT_SYM(cubin, nvrtcGetCUBIN)
+    QT_SYM(destroy, nvrtcDestroyProgram)
+    QT_SYM(errstr, nvrtcGetErrorString)
+#undef QT_SYM
+    r.ok = true;
+    return r;
+  }();
+  return n;
+}
+
+std::vector<char> compile_cubin(const std::string& src) {
+  const Nvrtc& n = nvrtc();
+  if (!n.ok) throw std::runtime_error("compiled passes unavailable: " + n.why);
+  nvrtcProgram prog;
+  if (n.create(&prog, src.c_str(), "qtjit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    throw std::runtime_error("nvrtcCreateProgram failed");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--device-as-default-execution-space"};
+  const nvrtcResult rc = n.compile(prog, 3, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t ls = 0;
+    n.logsize(prog, &ls);
+    std::string log(ls, '\0');
+    n.log(prog, &log[0]);
+    n.destroy(&prog);
+    throw std::runtime_error(std::string("nvrtc: ") + n.errstr(rc) + "\n" + log.substr(0, 2000));
+  }
+  size_t cs = 0;
+  n.cubinsize(prog, &cs);
+  std::vector<char> bin(cs);
+  n.cubin(prog, bin.data());
+  n.destroy(&prog);
+  return bin;
+}
+
+struct CacheEntry {
+  cudaLibrary_t lib = nullptr;
+  JitKernel k;
+};
+
+std::mutex g_mu;
+std::unordered_map<std::string, CacheEntry>& cache() {
+  static auto* m = new std::unordered_map<std::string, CacheEntry>();  // never destroyed
+  return *m;
+}
+JitStats g_stats;
+
+}  // namespace
+
+// What a compiled pass bakes in: the same tile geometry the interpreter
+// kernel gets in its KPassHead, plus the rounds.
+JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool check) {
+  JitPassSpec sp;
+  const int k = static_cast<int>(ps.tile_phys.size());
+  const int R = std::min(reg_bits, k);
+  sp.k = k;
+  sp.R = R;
+  sp.check = check;
+  sp.ntiles = 1ull << (buf_bits - k);
+  uint64_t tile_mask = 0;
+  for (int i = 0; i < k; ++i) {
+    const uint64_t b = 1ull << ps.tile_phys[i];
+    tile_mask |= b;
+    if (i < k - R) sp.lo_mask |= b;
+  }
+  sp.outer_mask = ((1ull << buf_bits) - 1) & ~tile_mask;
+  for (uint32_t s = 0; s < (1u << R); ++s) {
+    uint64_t off = 0;
+    for (int i = 0; i < R; ++i)
+      if ((s >> i) & 1u) off |= 1ull << ps.tile_phys[k - R + i];
+    sp.slot_gb[s] = off * sizeof(double2);
+    sp.slot_sb[s] = swz_host(s << (k - R)) << 4;
+  }
+  sp.rounds.resize(ps.rounds.size());
+  for (size_t r = 0; r < ps.rounds.size(); ++r) {
+    const PlanRound& pr = ps.rounds[r];
+    DRound& dr = sp.rounds[r];
+    dr = DRound{};
+    std::vector<int> sorted(pr.reg.begin(), pr.reg.end());
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 0; i < pr.reg.size() && i < static_cast<size_t>(kMaxRegBits); ++i) {
+      dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
+      dr.sreg[i] = static_cast<uint8_t>(sorted[i]);
+      dr.sbit[i] = swz_host(1u << pr.reg[i]) << 4;
+    }
+  }
+  return sp;
+}
+
+std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
+  const int R = sp.R, NS = 1 << R, k = sp.k;
+  const int threads = 1 << (k - R);
+  std::ostringstream os;
+  os << kPrelude;
+  // launch bounds: <= 64 registers for R <= 3, <= 128 for R = 4
+  const int minb = sp.min_blocks > 0 ? sp.min_blocks : std::max(1, (R >= 4 ? 512 : 1024) / threads);
+  os << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ")\n"
+     << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per) {\n"
+     << "  extern __shared__ double2 sm[];\n"
+     << (sp.pipe ? "" : "  char* const smb = reinterpret_cast<char*>(sm);\n")
+     << "  const u32 t = threadIdx.x;\n"
+     << "  const u64 off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
+     << "  const u32 st4 = swz(t) << 4;\n"
+     << "  const u64 t0 = u64(blockIdx.x) * per;\n"
+     << "  const u64 t1 = t0 + per < " << hexu(sp.ntiles) << " ? t0 + per : " << hexu(sp.ntiles) << ";\n"
+     << "  u64 base = pdep64(t0, " << hexu(sp.outer_mask) << ");\n"
+     << "  bool bad = false;\n";
+  const std::string outer = hexu(sp.outer_mask);
+  const uint32_t tbytes = 16u << k;
+  auto cp_tile = [&](const std::string& basev, const std::string& dst) {
+    os << "      { const char* s = reinterpret_cast<const char*>(src + " << basev << " + off_t);\n"
+       << "        const u32 d0 = static_cast<u32>(__cvta_generic_to_shared(" << dst << "));\n";
+    for (int s = 0; s < NS; ++s)
+      os << "        asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(d0 + (st4 ^ "
+         << sp.slot_sb[s] << "u)), \"l\"(s + " << sp.slot_gb[s] << "ull) : \"memory\");\n";
+    os << "        asm volatile(\"cp.async.commit_group;\" ::: \"memory\"); }\n";
+  };
+  if (sp.pipe) {
+    os << "  char* const sm0 = reinterpret_cast<char*>(sm);\n"
+       << "  u32 cur = 0;\n"
+       << "  if (t0 < t1) {\n";
+    cp_tile("base", "sm0");
+    os << "  }\n";
+  }
+  os << "  for (u64 tile = t0; tile < t1; ++tile) {\n";
+  if (sp.pipe) {
+    os << "    char* const smb = sm0 + cur;\n"
+       << "    if (tile + 1 < t1) {\n"
+       << "      const u64 nb = ((base | ~" << outer << ") + 1) & " << outer << ";\n";
+    cp_tile("nb", "sm0 + (cur ^ " + std::to_string(tbytes) + "u)");
+    os << "      asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n"
+       << "    } else {\n"
+       << "      asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n"
+       << "    }\n";
+  } else {
+    os << "    {\n      const char* s = reinterpret_cast<const char*>(src + base + off_t);\n";
+    for (int s = 0; s < NS; ++s)
+      os << "      const double2 l" << s << " = __ldcs(reinterpret_cast<const double2*>(s + "
+         << sp.slot_gb[s] << "ull));\n";
+    if (sp.pf_bits > 0) {
+      const uint32_t run = 1u << sp.pf_bits;
+      os << "      if ((t & " << (run - 1) << "u) == 0 && tile + 1 < t1) {\n"
+         << "        const char* n = reinterpret_cast<const char*>(src + (((base | ~" << outer << ") + 1) & "
+         << outer << ") + off_t);\n";
+      for (int s = 0; s < NS; ++s)
+        os << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(n + "
+           << sp.slot_gb[s] << "ull), \"r\"(" << (16u * run) << "u) : \"memory\");\n";
+      os << "      }\n";
+    }
+    for (int s = 0; s < NS; ++s)
+      os << "      *reinterpret_cast<double2*>(smb + (st4 ^ " << sp.slot_sb[s] << "u)) = l" << s << ";\n";
+    os << "    }\n";
+  }
+  os << "    __syncthreads();\n"
+     << "    const u64 g = gbase_hi | base;\n";
+  for (size_t r = 0; r < sp.rounds.size(); ++r) {
+    const DRound& rd = sp.rounds[r];
+    os << "    { // round " << r << "\n      u32 jb = t;";
+    for (int i = 0; i < R; ++i) os << " jb = insert_zero(jb, " << int(rd.sreg[i]) << "u);";
+    os << "\n      const u32 a = swz(jb) << 4;\n     ";
+    std::vector<uint32_t> sb(NS, 0);
+    for (int s = 0; s < NS; ++s) {
+      for (int i = 0; i < R; ++i)
+        if (s & (1 << i)) sb[s] ^= rd.sbit[i];
+      os << " double2 v" << s << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s] << "u));";
+    }
+    os << "\n";
+    const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
+    for (uint32_t w = w0; w < w1; ++w) emit_word(os, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
+    os << "     ";
+    for (int s = 0; s < NS; ++s)
+      os << " *reinterpret_cast<double2*>(smb + (a ^ " << sb[s] << "u)) = v" << s << ";";
+    os << "\n      __syncthreads();\n    }\n";
+  }
+  os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
+  for (int s = 0; s < NS; ++s) {
+    os << "      { const double2 x = *reinterpret_cast<const double2*>(smb + (st4 ^ " << sp.slot_sb[s]
+       << "u));";
+    if (sp.check) os << " bad = bad || !finite2(x);";
+    os << " __stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s] << "ull), x); }\n";
+  }
+  os << "    }\n"
+     << "    base = ((base | ~" << outer << ") + 1) & " << outer << ";\n"
+     << (sp.pipe ? "    cur ^= " + std::to_string(tbytes) + "u;\n" : std::string())
+     << "    __syncthreads();\n  }\n";
+  if (sp.check) os << "  if (__syncthreads_or(bad) && t == 0) atomicOr(flag, 1);\n";
+  os << "}\n";
+  return os.str();
+}
+
+std::vector<JitKernel> jit_kernels(const std::vector<std::string>& sources,
+                                   const std::vector<JitPassSpec*>& specs) {
+  std::vector<JitKernel> out(sources.size());
+  std::vector<size_t> todo;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i = 0; i < sources.size(); ++i) {
+      auto it = cache().find(sources[i]);
+      if (it != cache().end()) {
+        out[i] = it->second.k;
+        ++g_stats.cache_hits;
+      } else {
+        todo.push_back(i);
+      }
+    }
+  }
+  if (todo.empty()) return out;
+  const auto t0 = std::chrono::steady_clock::now();
+  // parallel NVRTC compiles (independent programs)
+  std::vector<std::vector<char>> bins(sources.size());
+  const size_t nthr = std::max<size_t>(1, std::min<size_t>(todo.size(), std::thread::hardware_concurrency()));
+  std::vector<std::future<void>> fs;
+  std::atomic<size_t> next{0};
+  std::mutex err_mu;
+  std::string err;
+  for (size_t w = 0; w < nthr; ++w)
+    fs.push_back(std::async(std::launch::async, [&] {
+      for (size_t j; (j = next.fetch_add(1)) < todo.size();) {
+        try {
+          bins[todo[j]] = compile_cubin(sources[todo[j]]);
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (err.empty()) err = e.what();
+        }
+      }
+    }));
+  for (auto& f : fs) f.get();
+  if (!err.empty()) throw std::runtime_error(err);
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (size_t i : todo) {
+    CacheEntry e;
+    if (cudaLibraryLoadData(&e.lib, bins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+        cudaLibraryGetKernel(&e.k.fn, e.lib, "qtjit") != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error("loading a compiled pass failed");
+    }
+    const JitPassSpec& sp = *specs[i];
+    e.k.threads = 1 << (sp.k - sp.R);
+    e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
+    const void* fn = reinterpret_cast<const void*>(e.k.fn);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(e.k.smem)) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&e.k.occupancy, fn, e.k.threads, e.k.smem) !=
+            cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error("compiled pass: attribute / occupancy query failed");
+    }
+    e.k.occupancy = std::max(1, e.k.occupancy);
+    out[i] = e.k;
+    cache().emplace(sources[i], e);
+    ++g_stats.compiled;
+  }
+  g_stats.compile_ms +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return out;
+}
+
+cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* psi,
+                       const double2* src, int* flag, uint64_t gbase_hi, cudaStream_t s) {
+  const uint64_t cap = static_cast<uint64_t>(k.occupancy) * static_cast<uint64_t>(sms);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, cap));
+  uint64_t per = (ntiles + grid - 1) / grid;
+  void* args[] = {&psi, &src, &flag, &gbase_hi, &per};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(k.fn), dim3(grid), dim3(k.threads), args,
+                          k.smem, s);
+}
+
+bool jit_available(std::string* why) {
+  const Nvrtc& n = nvrtc();
+  if (why) *why = n.why;
+  return n.ok;
+}
+
+std::vector<char> jit_compile_cubin(const std::string& src) { return compile_cubin(src); }
+
+JitStats jit_stats() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return g_stats;
+}
+
+}  // namespace qtb

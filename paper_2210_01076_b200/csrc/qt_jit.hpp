@@ -1,0 +1,78 @@
+// qt_jit.hpp -- compiled tile passes (host).
+//
+// The lean tile kernel interprets layer words (qt_micro.cpp): every op pays
+// a dispatch, and every matrix / table constant a uniform constant load. A
+// circuit that is simulated more than once can instead be compiled: each
+// lowered pass becomes one straight-line sm_100a kernel (NVRTC, loaded with
+// cudaLibraryLoadData) whose register rounds, slot addresses and FP64
+// constants are literals -- the DFMAs read their constants straight from the
+// constant bank and no dispatch instruction is left in the hot loop. Compiled
+// passes are cached process-wide by their generated source, so re-running a
+// circuit (or the same pass in another circuit) skips compilation.
+//
+// NVRTC is loaded at run time (dlopen libnvrtc.so.12); without it compiled
+// mode reports an error and the interpreter kernel runs instead.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "qt_ir.hpp"
+#include "qt_kernels.hpp"
+#include "qt_micro.hpp"
+
+namespace qtb {
+
+// Everything a compiled pass bakes in (besides the lowered layer words).
+struct JitPassSpec {
+  int k = 0, R = 0;
+  uint64_t ntiles = 0;
+  uint64_t lo_mask = 0, outer_mask = 0;
+  uint64_t slot_gb[1 << kMaxRegBits] = {};
+  uint32_t slot_sb[1 << kMaxRegBits] = {};
+  bool check = false;
+  bool pipe = false;    // double-buffered tiles: the next tile streams in (cp.async) during the rounds
+  int pf_bits = 0;      // > 0: L2 prefetch of the next tile in runs of 2^pf_bits amplitudes
+  int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
+  std::vector<DRound> rounds;  // reg / sreg / sbit per round
+};
+
+struct JitKernel {
+  cudaKernel_t fn = nullptr;
+  int threads = 0;
+  size_t smem = 0;
+  int occupancy = 0;  // resident CTAs per SM
+};
+
+// Tile geometry of a planned pass (buf_bits = log2 of the local buffer).
+JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool check);
+
+// CUDA C++ source of one compiled pass.
+std::string jit_source(const JitPassSpec& spec, const MicroPass& mp);
+
+// Compiles (or finds in the cache) the kernels of `sources`, in parallel.
+// Throws on compile / load failure.
+std::vector<JitKernel> jit_kernels(const std::vector<std::string>& sources,
+                                   const std::vector<JitPassSpec*>& specs);
+
+// Launches a compiled pass (grid = occupancy x SMs, capped by the tiles).
+cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* psi,
+                       const double2* src, int* flag, uint64_t gbase_hi, cudaStream_t s);
+
+// NVRTC compile only (no device needed): CUBIN bytes of a source.
+std::vector<char> jit_compile_cubin(const std::string& src);
+
+// True if NVRTC could be loaded (compiled mode available).
+bool jit_available(std::string* why = nullptr);
+
+// Process-wide compile statistics (for benchmarks).
+struct JitStats {
+  uint64_t compiled = 0, cache_hits = 0;
+  double compile_ms = 0.0;
+};
+JitStats jit_stats();
+
+}  // namespace qtb

@@ -120,7 +120,7 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
         // D_LAYER pool: [table 2 NS][terms 2 nt][rotations 2 each][2x2s 8 each]
         size_t o = d.arg & 0xffffu;
         const uint32_t nt = d.arg >> 16;
-        const bool tab = (d.hdr & kOpTable) != 0;
+        bool tab = (d.hdr & kOpTable) != 0;
         std::vector<cplx> t;
         if (tab) {
           t.resize(NS);
@@ -137,6 +137,21 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
         }
         o += 2 * nt;
         uint32_t base = d.dl;
+        if (tab) {
+          // a table of exact +-1 entries is a set of sign flips (integer ops)
+          bool signs_only = true;
+          uint32_t neg = 0;
+          for (int s = 0; s < NS && signs_only; ++s) {
+            signs_only = t[s].im == 0.0 && (t[s].re == 1.0 || t[s].re == -1.0);
+            if (t[s].re == -1.0) neg |= 1u << s;
+          }
+          if (signs_only) {
+            base ^= neg;
+            tab = false;
+            lterms.insert(lterms.end(), gterms.begin(), gterms.end());
+            gterms.clear();
+          }
+        }
         if (static_cast<int>(gterms.size()) > kMaxTableVariantTerms) {
           lterms.insert(lterms.end(), gterms.begin(), gterms.end());
           gterms.clear();
@@ -262,6 +277,31 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
     return out;
   }
   return out;
+}
+
+double micro_fp64_per_amp(const MicroPass& mp, int R) {
+  const int NS = 1 << R;
+  double fp = 0.0;
+  for (size_t w = 0; w < mp.size(); ++w) {
+    const uint32_t x = mp.words[2 * w], y = mp.words[2 * w + 1];
+    (void)y;
+    if (x & M_PERM) continue;
+    uint32_t off = x & 0xffffu;
+    if (x & (M_STAB | M_CTAB)) {
+      const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
+      if (nv) off += (nv + 1) & ~1u;
+      int live = 0;
+      for (int s = 0; s < NS; ++s) {
+        const double a = mp.pool[off + 2 * s], b = mp.pool[off + 2 * s + 1];
+        const bool ident = (x & M_STAB) ? (a == 0.0 && b == 0.0) : (a == 1.0 && b == 0.0);
+        live += ident ? 0 : 1;
+      }
+      fp += ((x & M_STAB) ? 3.0 : 4.0) * live / NS;
+    }
+    fp += 3.0 * __builtin_popcount((x >> M_ROT_SHIFT) & 15u) +
+          8.0 * __builtin_popcount((x >> M_DENSE_SHIFT) & 15u);
+  }
+  return fp;
 }
 
 }  // namespace qtb

@@ -10,6 +10,7 @@
 // launched in order on one CUDA stream.
 #include "qt_state.hpp"
 #include "qt_micro.hpp"
+#include "qt_jit.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -60,8 +61,18 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_);
 
-  opt_.reg_bits = kDefaultRegBits;
-  opt_.tile_bits = kDefaultTileBits;
+  // compiled passes (qt_jit.cpp): straight-line kernels per pass; they
+  // default to wider rounds and tiles (R = 4, 2^12 tiles, 128-B runs):
+  // without per-op dispatch the 128-register rounds win
+  jit_ = cfg && cfg->compiled == 1;
+  if (const char* e = std::getenv("QTB_JIT")) jit_ = std::atoi(e) != 0;
+  if (jit_) {
+    std::string why;
+    if (!jit_available(&why)) fail(QT_ERR_ARG, "compiled passes unavailable: " + why);
+  }
+  opt_.reg_bits = jit_ ? kJitRegBits : kDefaultRegBits;
+  opt_.tile_bits = jit_ ? kJitTileBits : kDefaultTileBits;
+  if (jit_) opt_.low_bits = kJitLowBits;
   if (cfg && cfg->tile_qubits > 0)
     opt_.tile_bits = std::min(cfg->tile_qubits, kMaxTileBits);
   // tuning overrides (benchmark sweeps only)
@@ -74,6 +85,7 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
     opt_.tile_bits = std::min(opt_.tile_bits, opt_.reg_bits + tb);
   }
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("QTB_JIT_MINB")) jit_min_blocks_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PIPE")) pipe_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_PF")) pf_ = std::atoi(e) != 0;
 
@@ -363,6 +375,33 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
   size_t last_tile = plan.passes.size();
   for (size_t pi = 0; pi < plan.passes.size(); ++pi)
     if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
+  std::vector<JitKernel> jk(plan.passes.size());
+  if (jit_) {
+    std::vector<JitPassSpec> specs(plan.passes.size());
+    std::vector<std::string> srcs;
+    std::vector<JitPassSpec*> sp_ptr;
+    std::vector<size_t> idx;
+    for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
+      const PlanPass& ps = plan.passes[pi];
+      if (ps.kind != PlanPass::Tile || !micro[pi].ok) continue;
+      JitPassSpec& sp = specs[pi];
+      sp = make_jit_spec(ps, opt_.reg_bits, buf_bits_, pi == last_tile);
+      sp.pipe = pipe_ && (2 * (sizeof(double2) << sp.k)) <= 200 * 1024;
+      sp.min_blocks = jit_min_blocks_;
+      if (pf_ && !sp.pipe) {
+        int run = 0;
+        while (run < sp.k - sp.R && ps.tile_phys[run] == run) ++run;
+        sp.pf_bits = run;
+      }
+      srcs.push_back(jit_source(sp, micro[pi]));
+      sp_ptr.push_back(&sp);
+      idx.push_back(pi);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<JitKernel> ks = jit_kernels(srcs, sp_ptr);
+    stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    for (size_t i = 0; i < idx.size(); ++i) jk[idx[i]] = ks[i];
+  }
   for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
     const PlanPass& ps = plan.passes[pi];
     if (ps.kind == PlanPass::Exchange) {
@@ -371,6 +410,20 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       tstop();
       stats.swaps += 1;
       stats.kernel_launches += ps.exchange.size();
+      continue;
+    }
+    if (jk[pi].fn) {
+      tstart(0);
+      cuda_check(jit_launch(jk[pi], 1ull << (buf_bits_ - static_cast<int>(ps.tile_phys.size())), sms_,
+                            psi_, src ? src : psi_, d_flag_,
+                            mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0,
+                            stream_),
+                 "compiled pass launch");
+      src = nullptr;
+      tstop();
+      stats.passes += 1;
+      stats.kernel_launches += 1;
+      stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
       continue;
     }
     const int k = static_cast<int>(ps.tile_phys.size());

@@ -12,6 +12,7 @@
 #include "qt_ir.hpp"
 #include "qt_kernels.hpp"
 #include "qt_plan.hpp"
+#include "qt_jit.hpp"
 #include "qtask_c.h"
 
 namespace qtb {
@@ -130,6 +131,10 @@ class State {
   // prefetch of the next tile (pf_); QTB_PIPE / QTB_PF override
   bool pipe_ = false;
   bool pf_ = false;
+  // compiled passes (qt_jit.cpp): every lowered tile pass runs its own
+  // straight-line kernel (cfg->compiled or QTB_JIT=1)
+  bool jit_ = false;
+  int jit_min_blocks_ = 0;  // compiled passes' launch-bound override (QTB_JIT_MINB)
   int occupancy_ = 1, sms_ = 148;
   bool timing_ = false;
   std::vector<PassTiming> timings_;

@@ -16,13 +16,15 @@ class StateVector:
     mode: "single" (one GPU), "loopback" (``shards`` emulated ranks on one
     GPU, exchanges by device copies) or "sharded" (one rank of a
     ``world``-GPU state, NCCL exchanges; pass ``rank``, ``world``, ``nccl_id``).
+    compiled=True runs every tile pass as its own NVRTC-compiled straight-line
+    kernel (cached by source: for circuits applied more than once).
     """
 
     def __init__(self, num_qubits: int, mode: str = "single", shards: int = 1,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 device: int = -1, tile_qubits: int = 0):
+                 device: int = -1, tile_qubits: int = 0, compiled: bool = False):
         self._h = ctypes.c_void_p()
-        cfg = _ffi.make_config(device=device, tile_qubits=tile_qubits)
+        cfg = _ffi.make_config(device=device, tile_qubits=tile_qubits, compiled=compiled)
         if mode == "single":
             check(lib().qt_state_create(num_qubits, ctypes.byref(cfg), ctypes.byref(self._h)))
         elif mode == "loopback":
