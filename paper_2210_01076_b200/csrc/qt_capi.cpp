@@ -192,7 +192,18 @@ int qt_plan_json(const qt_state* st, const qt_gate* gates, size_t count,
       if (rc != QT_OK) qtb::fail(rc, err);
     }
     qtb::fuse_ops(ops, n);
-    copy_out(qtb::plan_to_json(st->s->plan(ops)), buf, cap, needed);
+    const qtb::Plan p = st->s->plan(ops);
+    const int R = st->s->options().reg_bits;
+    const std::vector<qtb::MicroPass> mp = qtb::lower_plan_micro(
+        p, R,
+        qtb::MicroLimits{static_cast<size_t>(qtb::micro_capacity<qtb::KPassLarge>()),
+                         sizeof(qtb::KPassLarge::pool) / sizeof(double),
+                         sizeof(qtb::KPassLarge::rounds) / sizeof(qtb::DRound)});
+    std::vector<double> fp(p.passes.size(), -1.0);
+    for (size_t i = 0; i < p.passes.size(); ++i)
+      if (mp[i].ok)
+        fp[i] = qtb::micro_fp64_per_amp(mp[i], std::min<int>(R, static_cast<int>(p.passes[i].tile_phys.size())));
+    copy_out(qtb::plan_to_json(p, false, &fp), buf, cap, needed);
   });
 }
 

@@ -976,7 +976,7 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
   return plan;
 }
 
-std::string plan_to_json(const Plan& p, bool detail) {
+std::string plan_to_json(const Plan& p, bool detail, const std::vector<double>* fp64_lowered) {
   std::ostringstream os;
   const unsigned long long amps = 1ull << p.nlocal;
   os << "{\"nqubits\":" << p.nqubits << ",\"nlocal\":" << p.nlocal
@@ -1028,6 +1028,7 @@ std::string plan_to_json(const Plan& p, bool detail) {
       if (t) os << ",";
       os << gs[t];
     }
+    if (fp64_lowered && i < fp64_lowered->size() && (*fp64_lowered)[i] >= 0.0) fp = (*fp64_lowered)[i];
     os << "],\"read_amps\":" << amps << ",\"write_amps\":" << amps
        << ",\"fp64_per_amp\":" << fp;
     if (detail) {

@@ -50,7 +50,11 @@ EncRound compile_round(const PlanPass& pass, const PlanRound& round, bool fuse);
 uint32_t dtype_of(const LOp& op);
 
 // detail=true adds every round's register bits and encoded device ops.
-std::string plan_to_json(const Plan& p, bool detail = false);
+// fp64_lowered (optional, per pass, < 0 = none): FP64 ops per amplitude of
+// the pass as lowered for the lean / compiled kernels (qt_micro.cpp), which
+// then replaces the device-op accounting in "fp64_per_amp".
+std::string plan_to_json(const Plan& p, bool detail = false,
+                         const std::vector<double>* fp64_lowered = nullptr);
 
 // FP64 pipe operations per amplitude of an op (roofline accounting).
 double op_fp64_per_amp(const LOp& op);
