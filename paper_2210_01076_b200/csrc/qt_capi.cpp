@@ -577,6 +577,8 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
       // the state's tuning overrides (QTB_PIPE / QTB_JIT_MINB), as qt_state.cpp applies them
       if (const char* e = std::getenv("QTB_PIPE")) sp.pipe = std::atoi(e) != 0 && 2 * (16u << sp.k) <= 200u * 1024u;
       if (const char* e = std::getenv("QTB_JIT_MINB")) sp.min_blocks = std::atoi(e);
+      sp.coalesce_bits = qtb::kJitDirectBits;
+      if (const char* e = std::getenv("QTB_DIRECT_BITS")) sp.coalesce_bits = std::atoi(e);
       const std::string src = qtb::jit_source(sp, mp[i]);
       if (source_pass >= 0) {
         if (static_cast<size_t>(source_pass) == i) {

@@ -146,6 +146,7 @@ constexpr int kDefaultRegBits = 3;
 constexpr int kJitTileBits = 12;
 constexpr int kJitRegBits = 4;
 constexpr int kJitLowBits = 3;
+constexpr int kJitDirectBits = 3;
 
 struct DRound {
   uint16_t op_first;  // into the pass's op array

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <atomic>
@@ -103,8 +104,17 @@ uint64_t raw_bits(double d) {
   return w;
 }
 
+// FP64 constants of a pass, as hex-float literals in the instruction stream.
+// (A __constant__ array read with LDCU measured slower on C3: the pass's
+// constants overflow the per-SM constant cache; literals ride the
+// instruction fetch, two uniform moves per non-encodable double.)
+struct Consts {
+  std::string operator()(double d) const { return hexd(d); }
+};
+
 // Code of one layer word.
-void emit_word(std::ostringstream& os, int R, uint32_t x, uint32_t y, const std::vector<double>& P) {
+void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y,
+               const std::vector<double>& P) {
   const int NS = 1 << R;
   uint32_t off = x & 0xffffu;
   if (x & M_PERM) {
@@ -137,29 +147,28 @@ void emit_word(std::ostringstream& os, int R, uint32_t x, uint32_t y, const std:
         const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
         if (x & M_STAB) {
           if (a == 0.0 && b == 0.0) continue;  // identity entry
-          os << " pshear(v" << s << ", " << hexd(a) << ", " << hexd(b) << ");";
+          os << " pshear(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
         } else {
           if (a == 1.0 && b == 0.0) continue;
-          os << " cscale(v" << s << ", " << hexd(a) << ", " << hexd(b) << ");";
+          os << " cscale(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
         }
       }
     };
-    if (nv == 0) {
-      os << " ";
-      table(off);
-      os << "\n";
-    } else {
-      os << "  { const u32 vi =";
-      for (uint32_t j = 0; j < nv; ++j)
-        os << (j ? " | " : " ") << "(((g & " << hexu(gc[j]) << ") == " << hexu(gc[j]) << ") ? " << (1u << j)
-           << "u : 0u)";
-      os << ";\n    switch (vi) {\n";
-      for (uint32_t v = 0; v < (1u << nv); ++v) {
-        os << "    case " << v << "u: {";
-        table(off + v * 2 * NS);
-        os << " break; }\n";
-      }
-      os << "    } }\n";
+    // variant 0 (every tile-uniform condition false) as the table; each
+    // condition then flips the signs of the slots where its variant differs
+    // (integer ops, branch-free: no predicated duplicate tables)
+    os << " ";
+    table(off);
+    os << "\n";
+    for (uint32_t j = 0; j < nv; ++j) {
+      const uint32_t vo = off + (1u << j) * 2 * NS;
+      std::string flips;
+      for (int s = 0; s < NS; ++s)
+        if (P[vo + 2 * s] != P[off + 2 * s] || P[vo + 2 * s + 1] != P[off + 2 * s + 1])
+          flips += " flip2(v" + std::to_string(s) + ", sg);";
+      if (flips.empty()) continue;
+      os << "  { const u32 sg = ((g & " << hexu(gc[j]) << ") == " << hexu(gc[j]) << ") ? 0x80000000u : 0u;"
+         << flips << " }\n";
     }
     off += (2 * NS) << nv;
   }
@@ -195,14 +204,14 @@ void emit_word(std::ostringstream& os, int R, uint32_t x, uint32_t y, const std:
     os << " ";
     for (int s = 0; s < NS; ++s) {
       if (s & (1 << a)) continue;
-      os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << hexd(ca) << ", " << hexd(cb) << ");";
+      os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << kc(ca) << ", " << kc(cb) << ");";
     }
     os << "\n";
   }
   for (int a = 0; a < R; ++a) {
     if (!(dmask & (1u << a))) continue;
     std::string m;
-    for (int k = 0; k < 8; ++k) m += ", " + hexd(P[off + k]);
+    for (int k = 0; k < 8; ++k) m += ", " + kc(P[off + k]);
     off += 8;
     os << " ";
     for (int s = 0; s < NS; ++s) {
@@ -322,6 +331,7 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     sp.slot_gb[s] = off * sizeof(double2);
     sp.slot_sb[s] = swz_host(s << (k - R)) << 4;
   }
+  sp.tile_phys = ps.tile_phys;
   sp.rounds.resize(ps.rounds.size());
   for (size_t r = 0; r < ps.rounds.size(); ++r) {
     const PlanRound& pr = ps.rounds[r];
@@ -338,11 +348,55 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
   return sp;
 }
 
+namespace {
+
+// Round r reads (writes) its 2^R amplitudes straight from (to) HBM when its
+// register bits avoid the tile's coalescing bits: the thread bits then start
+// with the lowest physical bits, so a warp's 16-B accesses cover whole runs.
+struct Direct {
+  bool ok = false;
+  uint64_t tmask = 0;                 // physical bits of the thread (non-register) tile bits
+  uint64_t off[1 << kMaxRegBits] = {};  // byte offset of slot s
+};
+
+Direct direct_round(const JitPassSpec& sp, const DRound& rd) {
+  Direct d;
+  const int k = sp.k, R = sp.R;
+  if (static_cast<int>(sp.tile_phys.size()) != k || sp.coalesce_bits <= 0) return d;
+  for (int i = 1; i < k; ++i)
+    if (sp.tile_phys[i] <= sp.tile_phys[i - 1]) return d;  // tile bits ascending
+  uint32_t regs = 0;
+  for (int i = 0; i < R; ++i) regs |= 1u << rd.reg[i];
+  for (int b = 0; b < sp.coalesce_bits; ++b) {
+    // physical bit b must be a thread bit of the tile
+    int ti = -1;
+    for (int i = 0; i < k; ++i)
+      if (sp.tile_phys[i] == b) ti = i;
+    if (ti < 0 || ((regs >> ti) & 1u)) return d;
+  }
+  for (int i = 0; i < k; ++i)
+    if (!((regs >> i) & 1u)) d.tmask |= 1ull << sp.tile_phys[i];
+  for (int s = 0; s < (1 << R); ++s) {
+    uint64_t o = 0;
+    for (int i = 0; i < R; ++i)
+      if ((s >> i) & 1) o |= 1ull << sp.tile_phys[rd.reg[i]];
+    d.off[s] = o * 16;
+  }
+  d.ok = true;
+  return d;
+}
+
+}  // namespace
+
 std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   const int R = sp.R, NS = 1 << R, k = sp.k;
   const int threads = 1 << (k - R);
+  const size_t nr = sp.rounds.size();
   std::ostringstream os;
-  os << kPrelude;
+  Consts kc;
+  // first / last round straight from / to HBM (no staging through smem)
+  const Direct d0 = (!sp.pipe && nr) ? direct_round(sp, sp.rounds.front()) : Direct{};
+  const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
   // launch bounds: <= 64 registers for R <= 3, <= 128 for R = 4
   const int minb = sp.min_blocks > 0 ? sp.min_blocks : std::max(1, (R >= 4 ? 512 : 1024) / threads);
   os << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ")\n"
@@ -351,8 +405,10 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
      << (sp.pipe ? "" : "  char* const smb = reinterpret_cast<char*>(sm);\n")
      << "  const u32 t = threadIdx.x;\n"
      << "  const u64 off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
-     << "  const u32 st4 = swz(t) << 4;\n"
-     << "  const u64 t0 = u64(blockIdx.x) * per;\n"
+     << "  const u32 st4 = swz(t) << 4;\n";
+  if (d0.ok) os << "  const u64 off_d0 = pdep64(t, " << hexu(d0.tmask) << ");\n";
+  if (dl.ok) os << "  const u64 off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
+  os << "  const u64 t0 = u64(blockIdx.x) * per;\n"
      << "  const u64 t1 = t0 + per < " << hexu(sp.ntiles) << " ? t0 + per : " << hexu(sp.ntiles) << ";\n"
      << "  u64 base = pdep64(t0, " << hexu(sp.outer_mask) << ");\n"
      << "  bool bad = false;\n";
@@ -382,8 +438,9 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
     os << "      asm volatile(\"cp.async.wait_group 1;\" ::: \"memory\");\n"
        << "    } else {\n"
        << "      asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n"
-       << "    }\n";
-  } else {
+       << "    }\n"
+       << "    __syncthreads();\n";
+  } else if (!d0.ok) {
     os << "    {\n      const char* s = reinterpret_cast<const char*>(src + base + off_t);\n";
     for (int s = 0; s < NS; ++s)
       os << "      const double2 l" << s << " = __ldcs(reinterpret_cast<const double2*>(s + "
@@ -400,43 +457,63 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
     }
     for (int s = 0; s < NS; ++s)
       os << "      *reinterpret_cast<double2*>(smb + (st4 ^ " << sp.slot_sb[s] << "u)) = l" << s << ";\n";
-    os << "    }\n";
+    os << "    }\n    __syncthreads();\n";
   }
-  os << "    __syncthreads();\n"
-     << "    const u64 g = gbase_hi | base;\n";
-  for (size_t r = 0; r < sp.rounds.size(); ++r) {
+  os << "    const u64 g = gbase_hi | base;\n";
+  for (size_t r = 0; r < nr; ++r) {
     const DRound& rd = sp.rounds[r];
+    const bool first_direct = r == 0 && d0.ok, last_direct = r + 1 == nr && dl.ok;
     os << "    { // round " << r << "\n      u32 jb = t;";
     for (int i = 0; i < R; ++i) os << " jb = insert_zero(jb, " << int(rd.sreg[i]) << "u);";
     os << "\n      const u32 a = swz(jb) << 4;\n     ";
     std::vector<uint32_t> sb(NS, 0);
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < NS; ++s)
       for (int i = 0; i < R; ++i)
         if (s & (1 << i)) sb[s] ^= rd.sbit[i];
-      os << " double2 v" << s << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s] << "u));";
+    if (first_direct) {
+      os << " const char* gs = reinterpret_cast<const char*>(src + base + off_d0);\n     ";
+      for (int s = 0; s < NS; ++s)
+        os << " double2 v" << s << " = __ldcs(reinterpret_cast<const double2*>(gs + " << d0.off[s] << "ull));";
+    } else {
+      for (int s = 0; s < NS; ++s)
+        os << " double2 v" << s << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s] << "u));";
     }
     os << "\n";
     const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
-    for (uint32_t w = w0; w < w1; ++w) emit_word(os, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
-    os << "     ";
-    for (int s = 0; s < NS; ++s)
-      os << " *reinterpret_cast<double2*>(smb + (a ^ " << sb[s] << "u)) = v" << s << ";";
-    os << "\n      __syncthreads();\n    }\n";
+    for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
+    if (last_direct) {
+      os << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
+      for (int s = 0; s < NS; ++s) {
+        if (sp.check) os << " bad = bad || !finite2(v" << s << ");";
+        os << " __stcs(reinterpret_cast<double2*>(gd + " << dl.off[s] << "ull), v" << s << ");";
+      }
+      os << " }\n    }\n";
+    } else {
+      os << "     ";
+      for (int s = 0; s < NS; ++s)
+        os << " *reinterpret_cast<double2*>(smb + (a ^ " << sb[s] << "u)) = v" << s << ";";
+      os << "\n      __syncthreads();\n    }\n";
+    }
   }
-  os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
-  for (int s = 0; s < NS; ++s) {
-    os << "      { const double2 x = *reinterpret_cast<const double2*>(smb + (st4 ^ " << sp.slot_sb[s]
-       << "u));";
-    if (sp.check) os << " bad = bad || !finite2(x);";
-    os << " __stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s] << "ull), x); }\n";
+  if (!dl.ok) {
+    os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
+    for (int s = 0; s < NS; ++s) {
+      os << "      { const double2 x = *reinterpret_cast<const double2*>(smb + (st4 ^ " << sp.slot_sb[s]
+         << "u));";
+      if (sp.check) os << " bad = bad || !finite2(x);";
+      os << " __stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s] << "ull), x); }\n";
+    }
+    os << "    }\n";
   }
-  os << "    }\n"
-     << "    base = ((base | ~" << outer << ") + 1) & " << outer << ";\n"
-     << (sp.pipe ? "    cur ^= " + std::to_string(tbytes) + "u;\n" : std::string())
-     << "    __syncthreads();\n  }\n";
+  os << "    base = ((base | ~" << outer << ") + 1) & " << outer << ";\n"
+     << (sp.pipe ? "    cur ^= " + std::to_string(tbytes) + "u;\n" : std::string());
+  // smem reuse by the next tile (not needed when no round touches smem)
+  const bool smem_used = !(d0.ok && dl.ok && nr == 1);
+  if (smem_used) os << "    __syncthreads();\n";
+  os << "  }\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && t == 0) atomicOr(flag, 1);\n";
   os << "}\n";
-  return os.str();
+  return kPrelude + os.str();
 }
 
 std::vector<JitKernel> jit_kernels(const std::vector<std::string>& sources,

@@ -38,6 +38,10 @@ struct JitPassSpec {
   int pf_bits = 0;      // > 0: L2 prefetch of the next tile in runs of 2^pf_bits amplitudes
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
   std::vector<DRound> rounds;  // reg / sreg / sbit per round
+  std::vector<int> tile_phys;  // physical bit of each tile bit (ascending)
+  // first / last round read / write HBM directly when their register bits
+  // leave physical bits [0, coalesce_bits) to the threads (0 = never)
+  int coalesce_bits = 0;
 };
 
 struct JitKernel {

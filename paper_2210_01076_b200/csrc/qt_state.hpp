@@ -131,10 +131,16 @@ class State {
   // prefetch of the next tile (pf_); QTB_PIPE / QTB_PF override
   bool pipe_ = false;
   bool pf_ = false;
+  // compiled passes: double-buffer only passes with at most this many FP64
+  // ops per amplitude (<= 0: every pass when pipe_)
+  double pipe_max_fp64_ = 0.0;
   // compiled passes (qt_jit.cpp): every lowered tile pass runs its own
   // straight-line kernel (cfg->compiled or QTB_JIT=1)
   bool jit_ = false;
   int jit_min_blocks_ = 0;  // compiled passes' launch-bound override (QTB_JIT_MINB)
+  // compiled passes: first / last round straight from / to HBM when physical
+  // bits [0, direct_bits_) stay thread bits (128-B runs); 0 = always stage
+  int direct_bits_ = kJitDirectBits;
   int occupancy_ = 1, sms_ = 148;
   bool timing_ = false;
   std::vector<PassTiming> timings_;
