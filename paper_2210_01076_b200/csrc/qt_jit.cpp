@@ -399,6 +399,7 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
   // launch bounds: <= 64 registers for R <= 3, <= 128 for R = 4
   const int minb = sp.min_blocks > 0 ? sp.min_blocks : std::max(1, (R >= 4 ? 512 : 1024) / threads);
+  if (sp.stagger_ns > 0) os << "__device__ u32 qt_smctr[256];\n";
   os << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ")\n"
      << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per) {\n"
      << "  extern __shared__ double2 sm[];\n"
@@ -408,6 +409,15 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
      << "  const u32 st4 = swz(t) << 4;\n";
   if (d0.ok) os << "  const u64 off_d0 = pdep64(t, " << hexu(d0.tmask) << ");\n";
   if (dl.ok) os << "  const u64 off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
+  if (sp.stagger_ns > 0) {
+    // the second CTA of each SM starts late, so the two CTAs' load and
+    // compute phases interleave instead of running in lock step
+    os << "  { __shared__ u32 s_rank;\n"
+       << "    if (t == 0) { u32 smid; asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(smid));\n"
+       << "      s_rank = atomicAdd(&qt_smctr[smid & 255u], 1u) & 1u; }\n"
+       << "    __syncthreads();\n"
+       << "    if (s_rank) __nanosleep(" << sp.stagger_ns << "u); }\n";
+  }
   os << "  const u64 t0 = u64(blockIdx.x) * per;\n"
      << "  const u64 t1 = t0 + per < " << hexu(sp.ntiles) << " ? t0 + per : " << hexu(sp.ntiles) << ";\n"
      << "  u64 base = pdep64(t0, " << hexu(sp.outer_mask) << ");\n"

@@ -42,6 +42,7 @@ struct JitPassSpec {
   // first / last round read / write HBM directly when their register bits
   // leave physical bits [0, coalesce_bits) to the threads (0 = never)
   int coalesce_bits = 0;
+  int stagger_ns = 0;   // > 0: every second CTA of an SM starts this late
 };
 
 struct JitKernel {

@@ -136,3 +136,20 @@ def test_compiled_matches_interpreted_and_caches(gpu):
     assert after["compiled"] == before["compiled"]
     assert after["cache_hits"] > before["cache_hits"]
     assert got2.tobytes() == got.tobytes()
+
+
+@pytest.mark.gpu
+def test_compiled_config3_full_size_mirror(gpu):
+    """The headline config at its full size (30 q, 16 GiB) in compiled mode:
+    C then C^dagger returns |0...0> (no CPU state needed), norm after C."""
+    from tests.test_gpu_state import inverse
+    w = W.config3()
+    st = StateVector(30, compiled=True)
+    st.apply(w.gates)
+    nrm = st.norm_squared()
+    st.apply(inverse(w.gates))
+    head = st.read(0, 1 << 12)
+    nrm2 = st.norm_squared()
+    st.close()
+    assert abs(nrm - 1) <= NORM_TOL and abs(nrm2 - 1) <= NORM_TOL
+    assert abs(head[0] - 1) <= TOL and np.abs(head[1:]).max() <= TOL

@@ -58,39 +58,45 @@ def inverse(gates):
 
 def c2():
     w = W.config2()
-    st = StateVector(w.n)
-    st.set_basis(0)
-    st.apply(w.gates)
-    st.sync()
-    t0 = time.perf_counter()
-    st.set_basis(0)
-    st.apply(w.gates)
-    st.sync()
-    sec = time.perf_counter() - t0
-    got = st.read()
-    dev = float(np.abs(got - W.qft_closed_form(w.n, w.basis)).max())
-    out = {"workload": w.name, "gates": w.metric_gates, "seconds": sec,
-           "amp_gate_per_s": w.metric_gates * (1 << w.n) / sec,
-           "passes": st.stats()["passes"], "max_abs_diff_vs_closed_form": dev,
-           "norm_error": abs(st.norm_squared() - 1.0)}
-    st.close()
+    out = {"workload": w.name, "gates": w.metric_gates}
+    for mode in ("interpreted", "compiled"):
+        st = StateVector(w.n, compiled=mode == "compiled")
+        st.set_basis(0)
+        st.apply(w.gates)          # compiled: builds the passes (process cache)
+        st.sync()
+        t0 = time.perf_counter()
+        st.set_basis(0)
+        st.apply(w.gates)
+        st.sync()
+        sec = time.perf_counter() - t0
+        got = st.read()
+        dev = float(np.abs(got - W.qft_closed_form(w.n, w.basis)).max())
+        out[mode] = {"seconds": sec, "amp_gate_per_s": w.metric_gates * (1 << w.n) / sec,
+                     "passes": st.stats()["passes"], "max_abs_diff_vs_closed_form": dev,
+                     "norm_error": abs(st.norm_squared() - 1.0)}
+        st.close()
     return out
 
 
 def c4():
     w = W.config4()
-    st = StateVector(w.n)
-    sec = timed_apply(st, w.gates, reps=1)
-    passes = st.stats()["passes"]
-    nrm = st.norm_squared()
-    st.apply(inverse(w.gates))
-    head = st.read(0, 1 << 10)
-    mirror = max(abs(head[0] - 1.0), float(np.abs(head[1:]).max()))
-    st.close()
     out = {"workload": w.name, "qubits": w.n, "state_gib": 16 * (1 << w.n) / 2**30,
-           "gates": w.metric_gates, "seconds": sec, "passes": passes,
-           "amp_gate_per_s": w.metric_gates * (1 << w.n) / sec,
-           "norm_error": abs(nrm - 1.0), "mirror_max_abs_diff": mirror}
+           "gates": w.metric_gates}
+    for mode in ("interpreted", "compiled"):
+        st = StateVector(w.n, compiled=mode == "compiled")
+        if mode == "compiled":
+            st.apply(w.gates)      # build the passes (outside the timing)
+            st.sync()
+        sec = timed_apply(st, w.gates, reps=1)
+        passes = st.stats()["passes"]
+        nrm = st.norm_squared()
+        st.apply(inverse(w.gates))
+        head = st.read(0, 1 << 10)
+        mirror = max(abs(head[0] - 1.0), float(np.abs(head[1:]).max()))
+        st.close()
+        out[mode] = {"seconds": sec, "passes": passes,
+                     "amp_gate_per_s": w.metric_gates * (1 << w.n) / sec,
+                     "norm_error": abs(nrm - 1.0), "mirror_max_abs_diff": mirror}
     # the sharded scheduler at 30 qubits: loopback 8 shards vs unsharded
     w30 = W.config4(n=30, ngates=1500)
     single = StateVector(30)
