@@ -350,6 +350,14 @@ def main():
         return 0
 
     hbm_peak, peak_kind = load_peaks()
+    traffic = None  # DRAM bytes per launch of the dominant kernel, from an ncu --set full capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if ("qtjit" in tj.get("kernel", "")) == compiled and args.workload == "c3" and world == 1:
+            traffic = float(tj["bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        pass
     avg_pass_ms = statistics.mean(pass_ms) if pass_ms else float("nan")
     local_amps = amps / world
     bytes_per_pass = 32.0 * local_amps
@@ -372,7 +380,7 @@ def main():
                    "parallelism": f"sharded{world}" if world > 1 else "single",
                    "passes_per_step": len(tiles), "note": w.note},
         "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": None,
+                     "unit": "GB/s", "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                      "kernel": ("qtjit: compiled tile passes (qt_jit.cpp)" if compiled
                                 else "tile_pass_kernel (qt_tilepass.cu)"), "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms},
