@@ -566,13 +566,14 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
       if (p.passes[i].kind == qtb::PlanPass::Tile) last_tile = i;
     size_t lowered = 0, bytes = 0, compiled = 0, cubin = 0;
     double ms = 0.0, fp = 0.0;
-    std::string per = "[";
+    std::string per = "[", rounds = "[";
     for (size_t i = 0; i < p.passes.size(); ++i) {
       if (!mp[i].ok) continue;
       ++lowered;
       const double f = qtb::micro_fp64_per_amp(mp[i], std::min<int>(opt.reg_bits, static_cast<int>(p.passes[i].tile_phys.size())));
       fp += f;
       per += (per.size() > 1 ? "," : "") + std::to_string(f);
+      rounds += (rounds.size() > 1 ? "," : "") + std::to_string(p.passes[i].rounds.size());
       qtb::JitPassSpec sp = qtb::make_jit_spec(p.passes[i], opt.reg_bits, num_qubits, i == last_tile);
       // the state's tuning overrides (QTB_PIPE / QTB_JIT_MINB), as qt_state.cpp applies them
       if (const char* e = std::getenv("QTB_PIPE")) sp.pipe = std::atoi(e) != 0 && 2 * (16u << sp.k) <= 200u * 1024u;
@@ -601,7 +602,8 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
                   "{\"passes\":%zu,\"lowered\":%zu,\"source_bytes\":%zu,\"compiled\":%zu,"
                   "\"compile_ms\":%.1f,\"cubin_bytes\":%zu,\"fp64_per_amp\":%.1f,",
                   p.passes.size(), lowered, bytes, compiled, ms, cubin, fp);
-    copy_out(std::string(js) + "\"pass_fp64\":" + per + "]}", buf, cap, needed);
+    copy_out(std::string(js) + "\"pass_fp64\":" + per + "],\"pass_rounds\":" + rounds + "]}", buf, cap,
+             needed);
   });
 }
 

@@ -91,6 +91,7 @@ constexpr uint32_t M_CTAB = 1u << 25;    // table as complex multiplies (re, im)
 constexpr uint32_t M_SIGN = 1u << 26;    // sign flips (mask / terms in y)
 constexpr uint32_t M_PERM = 1u << 27;    // X / CX register permutation
 constexpr uint32_t M_NV_SHIFT = 28;      // table-variant terms (2 bits)
+constexpr uint32_t M_LAST = 1u << 30;    // the round's last word (every round has one)
 constexpr int kMaxTableVariantTerms = 3;
 
 // Variant id of a device op: the kernel dispatches on it to a fully

@@ -484,6 +484,20 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
       os << " const char* gs = reinterpret_cast<const char*>(src + base + off_d0);\n     ";
       for (int s = 0; s < NS; ++s)
         os << " double2 v" << s << " = __ldcs(reinterpret_cast<const double2*>(gs + " << d0.off[s] << "ull));";
+      if (sp.pf_bits > 0) {
+        // L2 prefetch of the next tile's round-0 data while this tile computes:
+        // the threads whose low run bits are zero cover one run per slot
+        int run = 0;
+        while (run < 12 && ((d0.tmask >> run) & 1ull)) ++run;
+        run = std::min(run, sp.pf_bits);
+        os << "\n      if ((t & " << ((1u << run) - 1) << "u) == 0 && tile + 1 < t1) {\n"
+           << "        const char* n = reinterpret_cast<const char*>(src + (((base | ~" << outer << ") + 1) & "
+           << outer << ") + off_d0);\n";
+        for (int s = 0; s < NS; ++s)
+          os << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(n + "
+             << d0.off[s] << "ull), \"r\"(" << (16u << run) << "u) : \"memory\");\n";
+        os << "      }\n     ";
+      }
     } else {
       for (int s = 0; s < NS; ++s)
         os << " double2 v" << s << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s] << "u));";

@@ -233,6 +233,11 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
         mp.words.push_back(y);
       }
       if (!ok) break;
+      if (mp.size() == mp.round_first.back()) {  // an empty round: one no-op word
+        mp.words.push_back(0);
+        mp.words.push_back(0);
+      }
+      mp.words[mp.words.size() - 2] |= M_LAST;
       mp.round_count.push_back(
           static_cast<uint16_t>(mp.size() - mp.round_first.back()));
     }
@@ -271,7 +276,8 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
       mp.pool.push_back(carried.re);
       mp.pool.push_back(carried.im);
     }
-    mp.words.push_back(off | M_CTAB);
+    mp.words[mp.words.size() - 2] &= ~M_LAST;
+    mp.words.push_back(off | M_CTAB | M_LAST);
     mp.words.push_back(0);
     mp.round_count.back() += 1;
     return out;

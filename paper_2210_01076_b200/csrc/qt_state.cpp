@@ -90,7 +90,10 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   if (const char* e = std::getenv("QTB_JIT_STAGGER")) stagger_ns_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PIPE")) pipe_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_PIPE_MAXFP")) pipe_max_fp64_ = std::atof(e);
-  if (const char* e = std::getenv("QTB_PF")) pf_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QTB_PF")) {
+    pf_bits_ = std::atoi(e);
+    pf_ = pf_bits_ != 0;
+  }
 
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
   cuda_check(cudaMalloc(&psi_, sizeof(double2) << buf_bits_), "state allocation");
@@ -397,7 +400,7 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       if (pf_ && !sp.pipe) {
         int run = 0;
         while (run < sp.k - sp.R && ps.tile_phys[run] == run) ++run;
-        sp.pf_bits = run;
+        sp.pf_bits = std::max(run, pf_bits_);
       }
       srcs.push_back(jit_source(sp, micro[pi]));
       sp_ptr.push_back(&sp);

@@ -131,6 +131,7 @@ class State {
   // prefetch of the next tile (pf_); QTB_PIPE / QTB_PF override
   bool pipe_ = false;
   bool pf_ = false;
+  int pf_bits_ = 0;  // QTB_PF=b: prefetch runs of up to 2^b amplitudes (compiled direct rounds)
   // compiled passes: double-buffer only passes with at most this many FP64
   // ops per amplitude (<= 0: every pass when pipe_)
   double pipe_max_fp64_ = 0.0;

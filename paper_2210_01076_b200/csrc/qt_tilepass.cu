@@ -454,13 +454,15 @@ __device__ __forceinline__ void m_denses(double2 (&v)[1 << R], const double2*& q
 // [sign flips][rotation per slot][complex 2x2 per slot] (qt_ir.hpp).
 template <int R, typename P>
 __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uint32_t o,
-                                           uint32_t o1, uint32_t jb, const uint64_t* sg) {
+                                           uint32_t jb, const uint64_t* sg) {
   constexpr int NS = 1 << R;
-  const uint2* mw = reinterpret_cast<const uint2*>(p.ops);
+  const unsigned long long* mw = reinterpret_cast<const unsigned long long*>(p.ops);
   const double2* pl = reinterpret_cast<const double2*>(p.pool);
-  for (; o < o1; ++o) {
-    const uint2 w = mw[o];
-    const uint32_t x = w.x;
+  // the round's words end with the one flagged M_LAST (no loop bound to keep)
+  for (uint32_t x = 0; !(x & M_LAST); ++o) {
+    const unsigned long long wv = mw[o];  // one 64-bit uniform load
+    const uint2 w = make_uint2(static_cast<uint32_t>(wv), static_cast<uint32_t>(wv >> 32));
+    x = w.x;
     uint32_t off = x & 0xffffu;  // doubles, even
     if (x & M_PERM) {
       DOp d{};
@@ -632,7 +634,7 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
       if constexpr (!GENERIC) {
-        run_layers<R>(v, p, rd.op_first, o1, jb, &s_tile[1]);
+        run_layers<R>(v, p, rd.op_first, jb, &s_tile[1]);
       } else {
         // the next op's header is loaded while the current op runs (the
         // dispatch chain of an op starts from it; the op array always has a
