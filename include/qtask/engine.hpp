@@ -29,6 +29,7 @@ struct Config {
   int max_checkpoints = 0;
   double checkpoint_fraction = 0.0;
   int segment_gates = 0;
+  int compiled = 0;  // 0: hybrid compiled passes (NVRTC, cached segments), -1: interpreter only
 };
 
 // Reference UpdateStats (engine.hpp:32-39) in GPU terms.
@@ -105,6 +106,7 @@ class Simulator {
     c.max_checkpoints = cfg.max_checkpoints;
     c.checkpoint_fraction = cfg.checkpoint_fraction;
     c.segment_gates = cfg.segment_gates;
+    c.compiled = cfg.compiled;
     detail::check(qt_sim_create(num_qubits, &c, &s_));
   }
   ~Simulator() { qt_sim_destroy(s_); }

@@ -87,7 +87,13 @@ typedef struct qt_config {
   int32_t segment_gates;     /* gates per checkpoint segment (0 = auto)    */
   int32_t compiled;          /* 1: compile each tile pass into its own
                                 straight-line kernel (NVRTC, cached by
-                                source), for circuits run more than once   */
+                                pass), for circuits run more than once;
+                                2: hybrid -- cached passes run compiled,
+                                the others on the interpreter kernel while
+                                they compile in the background. qt_state:
+                                0 = interpreter. qt_sim: 0 = hybrid (its
+                                re-simulated segments repeat), -1 =
+                                interpreter only                            */
   int32_t reserved[2];
 } qt_config;
 
@@ -191,6 +197,8 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits,
 /* Process-wide compiled-pass statistics (qt_config.compiled states): passes
  * compiled, compile-cache hits, total NVRTC + load milliseconds. */
 int qt_jit_stats(uint64_t* compiled, uint64_t* cache_hits, double* compile_ms);
+/* Passes queued or compiling in the background (hybrid mode). */
+int qt_jit_pending(uint64_t* pending);
 
 /* ======================================================================= */
 /* 2. Incremental simulator: qtask::Simulator (engine.hpp:46-100)          */

@@ -6,7 +6,7 @@ The compute lives in ``libqtask_b200.so`` (CUDA, built in-tree by
 ``csrc/Makefile``); this package is the host mirror of the reference's
 interface over its C ABI (``include/qtask_c.h``).
 """
-from ._ffi import GATE_DTYPE, device_count, jit_probe, jit_stats, lib, plan_probe  # noqa: F401
+from ._ffi import GATE_DTYPE, device_count, jit_probe, jit_stats, jit_wait, lib, plan_probe  # noqa: F401
 from .errors import (BadQubitError, Error, InvalidPositionError,  # noqa: F401
                      NetConflictError, NumericError, StaleStateError,
                      SuperpositionGateError, UnknownGateError, UnknownNetError)

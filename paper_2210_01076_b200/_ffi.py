@@ -55,7 +55,7 @@ HEADER_SYMBOLS = [
     "qt_state_create", "qt_state_create_sharded", "qt_state_create_loopback",
     "qt_nccl_unique_id", "qt_state_destroy", "qt_state_num_qubits", "qt_set_basis",
     "qt_write", "qt_read", "qt_apply", "qt_norm_squared", "qt_sync", "qt_last_stats",
-    "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe", "qt_jit_probe", "qt_jit_stats",
+    "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe", "qt_jit_probe", "qt_jit_stats", "qt_jit_pending",
     "qt_sim_create", "qt_sim_destroy", "qt_sim_num_qubits", "qt_sim_block_size",
     "qt_sim_total_blocks", "qt_sim_insert_net_front", "qt_sim_insert_net_back",
     "qt_sim_insert_net_after", "qt_sim_remove_net", "qt_sim_insert_gate",
@@ -100,6 +100,7 @@ _SIGS = {
                       _c.c_size_t, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
     "qt_jit_stats": ([_c.POINTER(_c.c_uint64), _c.POINTER(_c.c_uint64), _c.POINTER(_c.c_double)],
                      _c.c_int),
+    "qt_jit_pending": ([_c.POINTER(_c.c_uint64)], _c.c_int),
     "qt_state_stream": ([_vp], _vp),
     "qt_set_timing": ([_vp, _c.c_int], _c.c_int),
     "qt_last_timings": ([_vp, _vp, _vp, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
@@ -177,7 +178,7 @@ def make_config(block_size=256, threads=0, device=-1, tile_qubits=0, max_checkpo
     cfg.max_checkpoints = max_checkpoints
     cfg.checkpoint_fraction = checkpoint_fraction
     cfg.segment_gates = segment_gates
-    cfg.compiled = 1 if compiled else 0
+    cfg.compiled = int(compiled) if not isinstance(compiled, bool) else (1 if compiled else 0)
     return cfg
 
 
@@ -224,6 +225,21 @@ def jit_stats() -> dict:
     c, h, ms = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_double(0.0)
     check(lib().qt_jit_stats(ctypes.byref(c), ctypes.byref(h), ctypes.byref(ms)))
     return {"compiled": c.value, "cache_hits": h.value, "compile_ms": ms.value}
+
+
+def jit_wait(timeout_s: float = 120.0) -> bool:
+    """Waits until no pass is queued or compiling in the background (hybrid
+    mode); False on timeout."""
+    import time
+    n = ctypes.c_uint64(0)
+    t_end = time.time() + timeout_s
+    while True:
+        check(lib().qt_jit_pending(ctypes.byref(n)))
+        if n.value == 0:
+            return True
+        if time.time() > t_end:
+            return False
+        time.sleep(0.05)
 
 
 def exchange_schedule(rank: int, nlocal: int, pairs, tmp_amps: int):

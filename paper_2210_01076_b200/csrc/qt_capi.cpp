@@ -615,3 +615,9 @@ int qt_jit_stats(uint64_t* compiled, uint64_t* cache_hits, double* compile_ms) {
   *compile_ms = st.compile_ms;
   return QT_OK;
 }
+
+int qt_jit_pending(uint64_t* pending) {
+  if (!pending) return null_arg();
+  *pending = qtb::jit_pending();
+  return QT_OK;
+}

@@ -74,14 +74,15 @@ enum DType : uint32_t {
 // Lean layer words: the lean kernel's instruction stream (qt_micro.cpp
 // lowers the D_LAYER / D_XPERM ops of a pass into them). One uint2 per layer:
 //   x = pool offset (doubles, even) | rotation slots << 16 | 2x2 slots << 20
-//       | flags | table-variant terms << 28
+//       | flags | tile-uniform sign terms << 28 | M_LAST
 //   y = unconditional sign-slot mask | conditional sign terms << 16 (M_SIGN),
 //       or the D_XPERM header (M_PERM)
-// Pool data of a layer, in order: [variant conditions (u64 each, padded to
-// even)][2^nv diagonal tables of 2^R entries][sign terms (2 words each)]
+// Pool data of a layer, in order: [nv tile-uniform sign terms (global-bit
+// condition, slot mask: 2 words each)][diagonal table of 2^R entries]
+// [sign terms (2 words each)]
 // [(a, b) per rotation slot][8 doubles per 2x2 slot].
-// Table variants: sign terms whose condition is tile-uniform (global bits
-// only) select one of 2^nv precomputed tables instead of flipping signs
+// Tile-uniform sign terms (condition on global bits only) negate the
+// table's output slots with one uniform test per term instead of flipping signs
 // per amplitude.
 // ---------------------------------------------------------------------------
 constexpr uint32_t M_ROT_SHIFT = 16;     // rotation slot mask (4 bits)
@@ -90,7 +91,7 @@ constexpr uint32_t M_STAB = 1u << 24;    // table of unit phases as shears (a, b
 constexpr uint32_t M_CTAB = 1u << 25;    // table as complex multiplies (re, im)
 constexpr uint32_t M_SIGN = 1u << 26;    // sign flips (mask / terms in y)
 constexpr uint32_t M_PERM = 1u << 27;    // X / CX register permutation
-constexpr uint32_t M_NV_SHIFT = 28;      // table-variant terms (2 bits)
+constexpr uint32_t M_NV_SHIFT = 28;      // tile-uniform sign terms of the table (2 bits)
 constexpr uint32_t M_LAST = 1u << 30;    // the round's last word (every round has one)
 constexpr int kMaxTableVariantTerms = 3;
 

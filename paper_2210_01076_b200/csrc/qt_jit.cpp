@@ -8,14 +8,20 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <future>
 #include <memory>
 #include <mutex>
 #include <sstream>
 #include <stdexcept>
 #include <thread>
+
+#include <pthread.h>
 #include <unordered_map>
 
 #include "qt_gates.hpp"
@@ -139,38 +145,31 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
   }
   if (x & (M_STAB | M_CTAB)) {
     const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
-    std::vector<uint64_t> gc(nv);
-    for (uint32_t j = 0; j < nv; ++j) gc[j] = raw_bits(P[off + j]);
-    if (nv) off += (nv + 1) & ~1u;
-    auto table = [&](uint32_t toff) {
-      for (int s = 0; s < NS; ++s) {
-        const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
-        if (x & M_STAB) {
-          if (a == 0.0 && b == 0.0) continue;  // identity entry
-          os << " pshear(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
-        } else {
-          if (a == 1.0 && b == 0.0) continue;
-          os << " cscale(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
-        }
-      }
-    };
-    // variant 0 (every tile-uniform condition false) as the table; each
-    // condition then flips the signs of the slots where its variant differs
-    // (integer ops, branch-free: no predicated duplicate tables)
+    const uint32_t toff = off + 2 * nv;  // after nv (condition, slots) pairs
     os << " ";
-    table(off);
+    for (int s = 0; s < NS; ++s) {
+      const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
+      if (x & M_STAB) {
+        if (a == 0.0 && b == 0.0) continue;  // identity entry
+        os << " pshear(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
+      } else {
+        if (a == 1.0 && b == 0.0) continue;
+        os << " cscale(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
+      }
+    }
     os << "\n";
+    // tile-uniform sign terms: branch-free integer flips of the table's output
     for (uint32_t j = 0; j < nv; ++j) {
-      const uint32_t vo = off + (1u << j) * 2 * NS;
+      const uint64_t gc = raw_bits(P[off + 2 * j]);
+      const uint32_t slots = static_cast<uint32_t>(raw_bits(P[off + 2 * j + 1]));
       std::string flips;
       for (int s = 0; s < NS; ++s)
-        if (P[vo + 2 * s] != P[off + 2 * s] || P[vo + 2 * s + 1] != P[off + 2 * s + 1])
-          flips += " flip2(v" + std::to_string(s) + ", sg);";
+        if ((slots >> s) & 1u) flips += " flip2(v" + std::to_string(s) + ", sg);";
       if (flips.empty()) continue;
-      os << "  { const u32 sg = ((g & " << hexu(gc[j]) << ") == " << hexu(gc[j]) << ") ? 0x80000000u : 0u;"
+      os << "  { const u32 sg = ((g & " << hexu(gc) << ") == " << hexu(gc) << ") ? 0x80000000u : 0u;"
          << flips << " }\n";
     }
-    off += (2 * NS) << nv;
+    off = toff + 2 * NS;
   }
   if (x & M_SIGN) {
     const uint32_t nt = y >> 16, base = y & 0xffffu;
@@ -298,7 +297,7 @@ struct CacheEntry {
   JitKernel k;
 };
 
-std::mutex g_mu;
+std::mutex& g_mu = *new std::mutex();  // never destroyed (background workers)
 std::unordered_map<std::string, CacheEntry>& cache() {
   static auto* m = new std::unordered_map<std::string, CacheEntry>();  // never destroyed
   return *m;
@@ -540,14 +539,133 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   return kPrelude + os.str();
 }
 
-std::vector<JitKernel> jit_kernels(const std::vector<std::string>& sources,
+std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
+  // every input of jit_source, as bytes (exact: no hash collisions)
+  std::string k;
+  auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks,
+                          sp.coalesce_bits, sp.stagger_ns,
+                          static_cast<int32_t>(sp.rounds.size()),
+                          static_cast<int32_t>(sp.tile_phys.size()),
+                          static_cast<int32_t>(mp.words.size()),
+                          static_cast<int32_t>(mp.pool.size())};
+  put(head, sizeof(head));
+  put(&sp.ntiles, 8);
+  put(&sp.lo_mask, 8);
+  put(&sp.outer_mask, 8);
+  put(sp.slot_gb, sizeof(sp.slot_gb));
+  put(sp.slot_sb, sizeof(sp.slot_sb));
+  put(sp.rounds.data(), sp.rounds.size() * sizeof(DRound));
+  put(sp.tile_phys.data(), sp.tile_phys.size() * sizeof(int));
+  put(mp.round_first.data(), mp.round_first.size() * 2);
+  put(mp.round_count.data(), mp.round_count.size() * 2);
+  put(mp.words.data(), mp.words.size() * 4);
+  put(mp.pool.data(), mp.pool.size() * 8);
+  return k;
+}
+
+namespace {
+
+// Loads a CUBIN and fills the launch facts; caller holds no lock.
+CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp) {
+  CacheEntry e;
+  if (cudaLibraryLoadData(&e.lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+      cudaLibraryGetKernel(&e.k.fn, e.lib, "qtjit") != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error("loading a compiled pass failed");
+  }
+  e.k.threads = 1 << (sp.k - sp.R);
+  e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
+  const void* fn = reinterpret_cast<const void*>(e.k.fn);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(e.k.smem)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&e.k.occupancy, fn, e.k.threads, e.k.smem) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error("compiled pass: attribute / occupancy query failed");
+  }
+  e.k.occupancy = std::max(1, e.k.occupancy);
+  return e;
+}
+
+// ---- background compiles (hybrid mode) --------------------------------------
+struct Job {
+  std::string key, src;
+  JitPassSpec spec;
+  int device;
+};
+// heap-allocated and never destroyed: the detached workers may still wait on
+// them while the process exits
+std::mutex& q_mu = *new std::mutex();
+std::condition_variable& q_cv = *new std::condition_variable();
+std::deque<Job>* g_queue = nullptr;
+std::unordered_map<std::string, int>* g_queued = nullptr;  // keys queued or compiling
+int g_workers = 0;
+int g_active = 0;       // jobs being compiled / loaded
+bool g_exiting = false;
+unsigned g_reregs = 0;  // background compiles finished (drain re-registration)
+
+// At exit: drop the queue and wait for the jobs in flight, so no worker is
+// inside NVRTC or the CUDA runtime while the runtime tears down.
+bool g_trace = false;  // QTB_SEGV_TRACE: log the drain
+
+void drain_at_exit() {
+  std::unique_lock<std::mutex> lk(q_mu);
+  g_exiting = true;
+  if (g_trace) std::fprintf(stderr, "qtask-b200: exit drain: %d active, %zu queued\n", g_active, g_queue->size());
+  g_queue->clear();
+  q_cv.wait_for(lk, std::chrono::seconds(60), [] { return g_active == 0; });
+  if (g_trace) std::fprintf(stderr, "qtask-b200: exit drain done (%d active)\n", g_active);
+}
+
+void worker() {
+  for (;;) {
+    Job j;
+    {
+      std::unique_lock<std::mutex> lk(q_mu);
+      q_cv.wait(lk, [] { return !g_queue->empty() && !g_exiting; });
+      j = std::move(g_queue->front());
+      g_queue->pop_front();
+      ++g_active;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+      const std::vector<char> bin = compile_cubin(j.src);
+      cudaSetDevice(j.device);
+      CacheEntry e = load_entry(bin, j.spec);
+      std::lock_guard<std::mutex> lk(g_mu);
+      cache().emplace(j.key, e);
+      ++g_stats.compiled;
+      ++g_stats.background;
+      g_stats.compile_ms +=
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    } catch (const std::exception&) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      ++g_stats.failed;  // that pass keeps running on the interpreter
+    }
+    std::lock_guard<std::mutex> lk(q_mu);
+    g_queued->erase(j.key);
+    --g_active;
+    // NVRTC may register more exit-time destructors lazily (new code paths
+    // in a compile); re-registering the drain after a compile keeps it ahead
+    // of them in the (reverse-order) exit sequence
+    if (!g_exiting && (g_reregs < 64 || (g_reregs & 15) == 0)) std::atexit(drain_at_exit);
+    ++g_reregs;
+    q_cv.notify_all();
+  }
+}
+
+}  // namespace
+
+std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
+                                   const std::vector<std::function<std::string()>>& sources,
                                    const std::vector<JitPassSpec*>& specs) {
-  std::vector<JitKernel> out(sources.size());
+  std::vector<JitKernel> out(keys.size());
   std::vector<size_t> todo;
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    for (size_t i = 0; i < sources.size(); ++i) {
-      auto it = cache().find(sources[i]);
+    for (size_t i = 0; i < keys.size(); ++i) {
+      auto it = cache().find(keys[i]);
       if (it != cache().end()) {
         out[i] = it->second.k;
         ++g_stats.cache_hits;
@@ -559,52 +677,118 @@ std::vector<JitKernel> jit_kernels(const std::vector<std::string>& sources,
   if (todo.empty()) return out;
   const auto t0 = std::chrono::steady_clock::now();
   // parallel NVRTC compiles (independent programs)
-  std::vector<std::vector<char>> bins(sources.size());
+  std::vector<std::vector<char>> bins(keys.size());
   const size_t nthr = std::max<size_t>(1, std::min<size_t>(todo.size(), std::thread::hardware_concurrency()));
-  std::vector<std::future<void>> fs;
   std::atomic<size_t> next{0};
   std::mutex err_mu;
   std::string err;
-  for (size_t w = 0; w < nthr; ++w)
-    fs.push_back(std::async(std::launch::async, [&] {
-      for (size_t j; (j = next.fetch_add(1)) < todo.size();) {
-        try {
-          bins[todo[j]] = compile_cubin(sources[todo[j]]);
-        } catch (const std::exception& e) {
-          std::lock_guard<std::mutex> lk(err_mu);
-          if (err.empty()) err = e.what();
-        }
+  struct Ctx {
+    std::function<void()> fn;
+  } ctx{[&] {
+    for (size_t j; (j = next.fetch_add(1)) < todo.size();) {
+      try {
+        bins[todo[j]] = compile_cubin(sources[todo[j]]());
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (err.empty()) err = e.what();
       }
-    }));
-  for (auto& f : fs) f.get();
+    }
+  }};
+  std::vector<pthread_t> ths;
+  for (size_t w = 0; w < nthr; ++w) {
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, kJitStackBytes);
+    pthread_t th;
+    if (pthread_create(&th, &attr, [](void* c) -> void* { static_cast<Ctx*>(c)->fn(); return nullptr; },
+                       &ctx) == 0)
+      ths.push_back(th);
+    pthread_attr_destroy(&attr);
+  }
+  if (ths.empty()) ctx.fn();
+  for (pthread_t th : ths) pthread_join(th, nullptr);
   if (!err.empty()) throw std::runtime_error(err);
-  std::lock_guard<std::mutex> lk(g_mu);
   for (size_t i : todo) {
-    CacheEntry e;
-    if (cudaLibraryLoadData(&e.lib, bins[i].data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
-        cudaLibraryGetKernel(&e.k.fn, e.lib, "qtjit") != cudaSuccess) {
-      cudaGetLastError();
-      throw std::runtime_error("loading a compiled pass failed");
-    }
-    const JitPassSpec& sp = *specs[i];
-    e.k.threads = 1 << (sp.k - sp.R);
-    e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
-    const void* fn = reinterpret_cast<const void*>(e.k.fn);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(e.k.smem)) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&e.k.occupancy, fn, e.k.threads, e.k.smem) !=
-            cudaSuccess) {
-      cudaGetLastError();
-      throw std::runtime_error("compiled pass: attribute / occupancy query failed");
-    }
-    e.k.occupancy = std::max(1, e.k.occupancy);
+    CacheEntry e = load_entry(bins[i], *specs[i]);
     out[i] = e.k;
-    cache().emplace(sources[i], e);
+    std::lock_guard<std::mutex> lk(g_mu);
+    cache().emplace(keys[i], e);
     ++g_stats.compiled;
   }
+  std::lock_guard<std::mutex> lk(g_mu);
   g_stats.compile_ms +=
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return out;
+}
+
+bool jit_lookup(const std::string& key, JitKernel* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = cache().find(key);
+  if (it == cache().end()) {
+    ++g_stats.misses;
+    return false;
+  }
+  *out = it->second.k;
+  ++g_stats.cache_hits;
+  return true;
+}
+
+void jit_compile_async(const std::string& key, const std::string& src, const JitPassSpec& spec,
+                       int device) {
+  static std::once_flag first;
+  std::call_once(first, [&] {
+    // The first pass compiles synchronously, BEFORE the exit drain is
+    // registered: NVRTC registers exit-time destructors lazily during its
+    // first compile, and exit handlers run in reverse order -- ours must run
+    // first, so that no background compile is still inside NVRTC when its
+    // state is torn down.
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+      const std::vector<char> bin = compile_cubin(src);
+      CacheEntry e = load_entry(bin, spec);
+      std::lock_guard<std::mutex> lk(g_mu);
+      cache().emplace(key, e);
+      ++g_stats.compiled;
+      g_stats.compile_ms +=
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    } catch (const std::exception&) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      ++g_stats.failed;
+    }
+    std::lock_guard<std::mutex> lk(q_mu);
+    g_queue = new std::deque<Job>();
+    g_queued = new std::unordered_map<std::string, int>();
+    if (const char* e = std::getenv("QTB_SEGV_TRACE")) g_trace = std::atoi(e) != 0;
+    std::atexit(drain_at_exit);
+  });
+  std::lock_guard<std::mutex> lk(q_mu);
+  {
+    std::lock_guard<std::mutex> lk2(g_mu);
+    if (cache().count(key)) return;  // (the synchronous first compile)
+  }
+  if (g_exiting) return;
+  if (g_queued->count(key)) return;
+  (*g_queued)[key] = 1;
+  g_queue->push_back(Job{key, src, spec, device});
+  if (g_workers < kJitBackgroundThreads) {
+    ++g_workers;
+    // NVRTC recurses deeply on long straight-line kernels: give the
+    // compile threads a large stack (the default 8 MB can overflow)
+    pthread_attr_t attr;
+    pthread_attr_init(&attr);
+    pthread_attr_setstacksize(&attr, kJitStackBytes);
+    pthread_attr_setdetachstate(&attr, PTHREAD_CREATE_DETACHED);
+    pthread_t th;
+    if (pthread_create(&th, &attr, [](void*) -> void* { worker(); return nullptr; }, nullptr) != 0)
+      --g_workers;
+    pthread_attr_destroy(&attr);
+  }
+  q_cv.notify_all();
+}
+
+size_t jit_pending() {
+  std::lock_guard<std::mutex> lk(q_mu);
+  return g_queued ? g_queued->size() : 0;
 }
 
 cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* psi,
@@ -631,3 +815,25 @@ JitStats jit_stats() {
 }
 
 }  // namespace qtb
+
+// ---- diagnostics: QTB_SEGV_TRACE=1 prints a native backtrace on SIGSEGV ----
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+namespace {
+void segv_trace(int sig) {
+  void* bt[64];
+  const int n = backtrace(bt, 64);
+  const char msg[] = "qtask-b200: fatal signal, native backtrace:\n";
+  (void)!write(2, msg, sizeof(msg) - 1);
+  backtrace_symbols_fd(bt, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+struct SegvTraceInit {
+  SegvTraceInit() {
+    if (const char* e = std::getenv("QTB_SEGV_TRACE"))
+      if (std::atoi(e) != 0) signal(SIGSEGV, segv_trace);
+  }
+} g_segv_trace_init;
+}  // namespace

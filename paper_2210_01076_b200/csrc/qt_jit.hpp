@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -58,10 +59,27 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
 // CUDA C++ source of one compiled pass.
 std::string jit_source(const JitPassSpec& spec, const MicroPass& mp);
 
-// Compiles (or finds in the cache) the kernels of `sources`, in parallel.
-// Throws on compile / load failure.
-std::vector<JitKernel> jit_kernels(const std::vector<std::string>& sources,
+// Exact cache key of a compiled pass: the bytes of every input of
+// jit_source (looking a pass up costs no source generation).
+std::string jit_key(const JitPassSpec& spec, const MicroPass& mp);
+
+// Compiles (or finds in the cache) the kernels of `keys` (sources generated
+// on a miss only), in parallel. Throws on compile / load failure.
+std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
+                                   const std::vector<std::function<std::string()>>& sources,
                                    const std::vector<JitPassSpec*>& specs);
+
+// Hybrid mode: a cached kernel, or false (the caller runs the interpreter
+// kernel and may queue the pass with jit_compile_async).
+bool jit_lookup(const std::string& key, JitKernel* out);
+// Compiles a pass on a background thread into the cache (no-op when it is
+// queued or compiling already).
+void jit_compile_async(const std::string& key, const std::string& src, const JitPassSpec& spec,
+                       int device);
+// Passes queued or compiling in the background.
+size_t jit_pending();
+constexpr int kJitBackgroundThreads = 4;
+constexpr size_t kJitStackBytes = size_t(256) << 20;  // per compile thread (reserved, not touched)
 
 // Launches a compiled pass (grid = occupancy x SMs, capped by the tiles).
 cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* psi,
@@ -75,7 +93,7 @@ bool jit_available(std::string* why = nullptr);
 
 // Process-wide compile statistics (for benchmarks).
 struct JitStats {
-  uint64_t compiled = 0, cache_hits = 0;
+  uint64_t compiled = 0, cache_hits = 0, misses = 0, background = 0, failed = 0;
   double compile_ms = 0.0;
 };
 JitStats jit_stats();

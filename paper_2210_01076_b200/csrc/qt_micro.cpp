@@ -29,10 +29,10 @@ double bits_as_double(uint64_t w) {
 // A table's place in the lowered plan, for the final scalar fold.
 struct TableRef {
   size_t pass = 0, word = 0, pool = 0;
-  std::vector<cplx> phases;  // every variant's centred entries, in pool order
+  std::vector<cplx> phases;  // the table's centred entries
 };
 
-// Centres the angles of all entries (every variant of a table): returns
+// Centres the angles of a table's entries: returns
 // false (keep complex multiplies) when an entry is not a unit phase or the
 // centred angles need shear factors above kMaxShear.
 bool centre_tables(std::vector<cplx>& t, cplx& removed) {
@@ -158,22 +158,17 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
         }
         uint32_t x = off;
         if (tab) {
-          // unconditional flips join the table; tile-uniform terms make
-          // 2^nv variants of it
+          // unconditional flips join the table; each tile-uniform term
+          // becomes (condition, slot mask): the table's output is negated on
+          // those slots when the tile's global bits meet the condition
           for (int s = 0; s < NS; ++s)
             if ((base >> s) & 1u) t[s] = cplx{-t[s].re, -t[s].im};
           base = 0;
           const size_t nv = gterms.size();
-          std::vector<cplx> all(NS << nv);
-          for (size_t v = 0; v < (size_t(1) << nv); ++v)
-            for (int s = 0; s < NS; ++s) {
-              cplx c = t[s];
-              for (size_t j = 0; j < nv; ++j)
-                if (((v >> j) & 1u) && ((gterms[j].slots >> s) & 1u)) c = cplx{-c.re, -c.im};
-              all[v * NS + s] = c;
-            }
-          for (const SignTerm& g : gterms) P.push_back(bits_as_double(g.gcond));
-          pad_even(P);
+          for (const SignTerm& g : gterms) {
+            P.push_back(bits_as_double(g.gcond));
+            P.push_back(bits_as_double(g.slots));
+          }
           const size_t toff = P.size();
           bool scalar = nv == 0;
           for (int s = 1; s < NS && scalar; ++s)
@@ -183,14 +178,14 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
             // a pure scalar: carried, no table at all
             pass_carried = cmul(pass_carried, t[0]);
             P.resize(off);
-          } else if (centre_tables(all, removed)) {
+          } else if (centre_tables(t, removed)) {
             pass_carried = cmul(pass_carried, removed);
-            for (const cplx& c : all) push_shear(P, c);
-            pass_last = TableRef{pi, mp.words.size(), toff, all};
+            for (const cplx& c : t) push_shear(P, c);
+            pass_last = TableRef{pi, mp.words.size(), toff, t};
             pass_have_last = true;
             x |= M_STAB | (static_cast<uint32_t>(nv) << M_NV_SHIFT);
           } else {
-            for (const cplx& c : all) {
+            for (const cplx& c : t) {
               P.push_back(c.re);
               P.push_back(c.im);
             }
@@ -295,7 +290,7 @@ double micro_fp64_per_amp(const MicroPass& mp, int R) {
     uint32_t off = x & 0xffffu;
     if (x & (M_STAB | M_CTAB)) {
       const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
-      if (nv) off += (nv + 1) & ~1u;
+      off += 2 * nv;
       int live = 0;
       for (int s = 0; s < NS; ++s) {
         const double a = mp.pool[off + 2 * s], b = mp.pool[off + 2 * s + 1];

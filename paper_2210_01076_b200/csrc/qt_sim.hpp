@@ -39,7 +39,7 @@ class Sim {
   const std::vector<uint32_t>& net_order() const { return order_; }
   const std::vector<uint32_t>& net_gates(uint32_t net) const;
   void gate_info(uint32_t gate, qt_gate* out, uint32_t* net) const;
-  std::vector<qt_gate> flatten() const;
+  std::vector<qt_gate> flatten(std::vector<uint32_t>* ids = nullptr) const;
   State& state() { return *st_; }
 
  private:
@@ -68,6 +68,7 @@ class Sim {
   };
   std::unique_ptr<State> st_;
   std::vector<Ckpt> chain_;  // valid checkpoints, increasing pos
+  std::vector<uint32_t> bound_ids_;  // first gate of each segment of the last run (pos > 0)
   int nbuf_ = 1;
   qt_run_stats last_{};
 };

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 
 #include "qt_gates.hpp"
 #include "qt_kernels.hpp"
@@ -64,15 +65,23 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   // compiled passes (qt_jit.cpp): straight-line kernels per pass; they
   // default to wider rounds and tiles (R = 4, 2^12 tiles, 128-B runs):
   // without per-op dispatch the 128-register rounds win
-  jit_ = cfg && cfg->compiled == 1;
-  if (const char* e = std::getenv("QTB_JIT")) jit_ = std::atoi(e) != 0;
-  if (jit_) {
+  jit_mode_ = cfg ? std::max(0, std::min(2, static_cast<int>(cfg->compiled))) : 0;
+  if (const char* e = std::getenv("QTB_JIT")) jit_mode_ = std::max(0, std::min(2, std::atoi(e)));
+  if (jit_mode_) {
     std::string why;
-    if (!jit_available(&why)) fail(QT_ERR_ARG, "compiled passes unavailable: " + why);
+    if (!jit_available(&why)) {
+      // hybrid mode is an optimisation of the interpreter path: without
+      // NVRTC it is just the interpreter; explicit compiled mode fails
+      if (jit_mode_ == 2) jit_mode_ = 0;
+      else fail(QT_ERR_ARG, "compiled passes unavailable: " + why);
+    }
   }
-  opt_.reg_bits = jit_ ? kJitRegBits : kDefaultRegBits;
-  opt_.tile_bits = jit_ ? kJitTileBits : kDefaultTileBits;
-  if (jit_) opt_.low_bits = kJitLowBits;
+  // geometry: compiled R = 4 / 2^12 tiles / 128-B runs; hybrid R = 3 (its
+  // misses run on the interpreter, whose R = 4 variant is slow) with 2^12
+  // tiles / 128-B runs; interpreter R = 3 / 2^10 tiles / 256-B runs
+  opt_.reg_bits = jit_mode_ == 1 ? kJitRegBits : kDefaultRegBits;
+  opt_.tile_bits = jit_mode_ ? kJitTileBits : kDefaultTileBits;
+  if (jit_mode_) opt_.low_bits = kJitLowBits;
   if (cfg && cfg->tile_qubits > 0)
     opt_.tile_bits = std::min(cfg->tile_qubits, kMaxTileBits);
   // tuning overrides (benchmark sweeps only)
@@ -382,9 +391,11 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
   for (size_t pi = 0; pi < plan.passes.size(); ++pi)
     if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
   std::vector<JitKernel> jk(plan.passes.size());
-  if (jit_) {
+  if (jit_mode_) {
+    const auto t0 = std::chrono::steady_clock::now();
     std::vector<JitPassSpec> specs(plan.passes.size());
-    std::vector<std::string> srcs;
+    std::vector<std::string> keys;
+    std::vector<std::function<std::string()>> srcs;
     std::vector<JitPassSpec*> sp_ptr;
     std::vector<size_t> idx;
     for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
@@ -402,14 +413,25 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
         while (run < sp.k - sp.R && ps.tile_phys[run] == run) ++run;
         sp.pf_bits = std::max(run, pf_bits_);
       }
-      srcs.push_back(jit_source(sp, micro[pi]));
+      std::string key = jit_key(sp, micro[pi]);
+      if (jit_mode_ == 2) {
+        // hybrid: cached passes run compiled, the others on the interpreter
+        // while they compile in the background for the next update
+        if (!jit_lookup(key, &jk[pi])) jit_compile_async(key, jit_source(sp, micro[pi]), sp, device_);
+        continue;
+      }
+      keys.push_back(std::move(key));
+      const MicroPass* m = &micro[pi];
+      const JitPassSpec* spc = &sp;
+      srcs.push_back([m, spc] { return jit_source(*spc, *m); });
       sp_ptr.push_back(&sp);
       idx.push_back(pi);
     }
-    const auto t0 = std::chrono::steady_clock::now();
-    std::vector<JitKernel> ks = jit_kernels(srcs, sp_ptr);
+    if (!keys.empty()) {
+      std::vector<JitKernel> ks = jit_kernels(keys, srcs, sp_ptr);
+      for (size_t i = 0; i < idx.size(); ++i) jk[idx[i]] = ks[i];
+    }
     stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    for (size_t i = 0; i < idx.size(); ++i) jk[idx[i]] = ks[i];
   }
   for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
     const PlanPass& ps = plan.passes[pi];

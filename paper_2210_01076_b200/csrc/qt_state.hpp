@@ -135,9 +135,11 @@ class State {
   // compiled passes: double-buffer only passes with at most this many FP64
   // ops per amplitude (<= 0: every pass when pipe_)
   double pipe_max_fp64_ = 0.0;
-  // compiled passes (qt_jit.cpp): every lowered tile pass runs its own
-  // straight-line kernel (cfg->compiled or QTB_JIT=1)
-  bool jit_ = false;
+  // compiled passes (qt_jit.cpp; cfg->compiled or QTB_JIT): 1 = every
+  // lowered tile pass runs its own straight-line kernel (compiled on first
+  // use); 2 = hybrid: passes found in the compile cache run compiled, the
+  // others on the interpreter while they compile in the background
+  int jit_mode_ = 0;
   int jit_min_blocks_ = 0;  // compiled passes' launch-bound override (QTB_JIT_MINB)
   // compiled passes: first / last round straight from / to HBM when physical
   // bits [0, direct_bits_) stay thread bits (128-B runs); 0 = always stage

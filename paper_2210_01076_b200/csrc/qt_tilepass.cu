@@ -473,22 +473,29 @@ __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uin
     }
     if (x & (M_STAB | M_CTAB)) {
       const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
-      uint32_t vi = 0;
+      const double2* t = pl + (off >> 1) + nv;  // after nv (condition, slots) pairs
+      if (x & M_STAB) m_stab<R>(v, t);
+      else m_ctab<R>(v, t);
       if (nv) {
+        // tile-uniform sign terms: negate the slots of every term whose
+        // condition the tile's global bits meet (exact, so after the table)
         const uint64_t g = *sg;
+        uint32_t fl = 0;
 #pragma unroll
         for (uint32_t j = 0; j < kMaxTableVariantTerms; ++j) {
           if (j < nv) {
-            const uint64_t gc = static_cast<uint64_t>(__double_as_longlong(p.pool[off + j]));
-            vi |= ((g & gc) == gc ? 1u : 0u) << j;
+            const uint64_t gc = static_cast<uint64_t>(__double_as_longlong(p.pool[off + 2 * j]));
+            if ((g & gc) == gc)
+              fl ^= static_cast<uint32_t>(__double_as_longlong(p.pool[off + 2 * j + 1]));
           }
         }
-        off += (nv + 1) & ~1u;
+        if (fl) {
+#pragma unroll
+          for (int s = 0; s < NS; ++s)
+            if (fl & (1u << s)) v[s] = neg2(v[s]);
+        }
       }
-      const double2* t = pl + (off >> 1) + vi * NS;
-      if (x & M_STAB) m_stab<R>(v, t);
-      else m_ctab<R>(v, t);
-      off += (2 * NS) << nv;
+      off += 2 * nv + 2 * NS;
     }
     if (x & M_SIGN) {
       const uint32_t nt = w.y >> 16;

@@ -34,6 +34,7 @@ class Config:
     max_checkpoints: int = 0
     checkpoint_fraction: float = 0.0
     segment_gates: int = 0
+    compiled: int = 0          # 0: hybrid compiled passes (default), -1: interpreter only
 
 
 @dataclass
@@ -118,7 +119,8 @@ class Simulator:
             raise Error("block size must be a power of two >= 2")
         self._cfg = cfg
         c = _ffi.make_config(cfg.block_size, cfg.threads, cfg.device, cfg.tile_qubits,
-                             cfg.max_checkpoints, cfg.checkpoint_fraction, cfg.segment_gates)
+                             cfg.max_checkpoints, cfg.checkpoint_fraction, cfg.segment_gates,
+                             cfg.compiled)
         self._h = ctypes.c_void_p()
         check(lib().qt_sim_create(num_qubits, ctypes.byref(c), ctypes.byref(self._h)))
 

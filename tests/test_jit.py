@@ -153,3 +153,27 @@ def test_compiled_config3_full_size_mirror(gpu):
     st.close()
     assert abs(nrm - 1) <= NORM_TOL and abs(nrm2 - 1) <= NORM_TOL
     assert abs(head[0] - 1) <= TOL and np.abs(head[1:]).max() <= TOL
+
+
+@pytest.mark.gpu
+def test_hybrid_compiled_bitwise_equals_interpreter(gpu):
+    """Hybrid mode: the first apply runs every pass on the interpreter kernel
+    while the passes compile in the background; once they are cached the
+    same apply runs compiled. Both paths do the same FP64 operations in the
+    same order, so the states are bit-identical (the incremental engine's
+    results do not depend on the cache state)."""
+    from paper_2210_01076_b200 import jit_wait
+    w = W.config3(n=20, layers=12)
+    st = StateVector(20, compiled=2)
+    st.apply(w.gates)
+    first = st.read()
+    assert jit_wait(300)
+    before = jit_stats()
+    st.set_basis(0)
+    st.apply(w.gates)
+    second = st.read()
+    after = jit_stats()
+    st.close()
+    assert after["cache_hits"] > before["cache_hits"]
+    assert first.tobytes() == second.tobytes()
+    assert np.abs(first - oracle.simulate(20, w.gates)).max() <= TOL
