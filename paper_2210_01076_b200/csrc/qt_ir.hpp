@@ -149,6 +149,8 @@ constexpr int kJitTileBits = 12;
 constexpr int kJitRegBits = 4;
 constexpr int kJitLowBits = 3;
 constexpr int kJitDirectBits = 3;
+// hybrid compiled passes (incremental engine) from this many local qubits up
+constexpr int kHybridMinQubits = 20;
 
 struct DRound {
   uint16_t op_first;  // into the pass's op array

@@ -590,8 +590,9 @@ CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp) {
 
 // ---- background compiles (hybrid mode) --------------------------------------
 struct Job {
-  std::string key, src;
+  std::string key;
   JitPassSpec spec;
+  MicroPass mp;  // the source is generated on the worker (off the caller's path)
   int device;
 };
 // heap-allocated and never destroyed: the detached workers may still wait on
@@ -630,7 +631,7 @@ void worker() {
     }
     const auto t0 = std::chrono::steady_clock::now();
     try {
-      const std::vector<char> bin = compile_cubin(j.src);
+      const std::vector<char> bin = compile_cubin(jit_source(j.spec, j.mp));
       cudaSetDevice(j.device);
       CacheEntry e = load_entry(bin, j.spec);
       std::lock_guard<std::mutex> lk(g_mu);
@@ -733,7 +734,7 @@ bool jit_lookup(const std::string& key, JitKernel* out) {
   return true;
 }
 
-void jit_compile_async(const std::string& key, const std::string& src, const JitPassSpec& spec,
+void jit_compile_async(const std::string& key, const JitPassSpec& spec, const MicroPass& mp,
                        int device) {
   static std::once_flag first;
   std::call_once(first, [&] {
@@ -744,7 +745,7 @@ void jit_compile_async(const std::string& key, const std::string& src, const Jit
     // state is torn down.
     const auto t0 = std::chrono::steady_clock::now();
     try {
-      const std::vector<char> bin = compile_cubin(src);
+      const std::vector<char> bin = compile_cubin(jit_source(spec, mp));
       CacheEntry e = load_entry(bin, spec);
       std::lock_guard<std::mutex> lk(g_mu);
       cache().emplace(key, e);
@@ -769,7 +770,7 @@ void jit_compile_async(const std::string& key, const std::string& src, const Jit
   if (g_exiting) return;
   if (g_queued->count(key)) return;
   (*g_queued)[key] = 1;
-  g_queue->push_back(Job{key, src, spec, device});
+  g_queue->push_back(Job{key, spec, mp, device});
   if (g_workers < kJitBackgroundThreads) {
     ++g_workers;
     // NVRTC recurses deeply on long straight-line kernels: give the

@@ -74,7 +74,7 @@ std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
 bool jit_lookup(const std::string& key, JitKernel* out);
 // Compiles a pass on a background thread into the cache (no-op when it is
 // queued or compiling already).
-void jit_compile_async(const std::string& key, const std::string& src, const JitPassSpec& spec,
+void jit_compile_async(const std::string& key, const JitPassSpec& spec, const MicroPass& mp,
                        int device);
 // Passes queued or compiling in the background.
 size_t jit_pending();

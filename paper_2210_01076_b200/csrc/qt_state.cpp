@@ -76,6 +76,9 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
       else fail(QT_ERR_ARG, "compiled passes unavailable: " + why);
     }
   }
+  // hybrid pays off where passes stream enough amplitudes to amortise the
+  // cache lookups (small states are launch-bound)
+  if (jit_mode_ == 2 && nlocal_ < kHybridMinQubits) jit_mode_ = 0;
   // geometry: compiled R = 4 / 2^12 tiles / 128-B runs; hybrid R = 3 (its
   // misses run on the interpreter, whose R = 4 variant is slow) with 2^12
   // tiles / 128-B runs; interpreter R = 3 / 2^10 tiles / 256-B runs
@@ -417,7 +420,7 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       if (jit_mode_ == 2) {
         // hybrid: cached passes run compiled, the others on the interpreter
         // while they compile in the background for the next update
-        if (!jit_lookup(key, &jk[pi])) jit_compile_async(key, jit_source(sp, micro[pi]), sp, device_);
+        if (!jit_lookup(key, &jk[pi])) jit_compile_async(key, sp, micro[pi], device_);
         continue;
       }
       keys.push_back(std::move(key));
