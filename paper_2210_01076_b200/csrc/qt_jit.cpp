@@ -116,6 +116,18 @@ uint64_t raw_bits(double d) {
 // instruction fetch, two uniform moves per non-encodable double.)
 struct Consts {
   std::string operator()(double d) const { return hexd(d); }
+  // table entries (a, b) may instead come from a per-pass __constant__ array
+  // read as double2 (one 16-B uniform load per entry instead of four
+  // uniform moves): QTB_JIT_TABCONST=1
+  bool tab_array = false;
+  std::vector<double> tab;
+  std::string pair(double a, double b) {
+    if (!tab_array) return hexd(a) + ", " + hexd(b);
+    const size_t i = tab.size() / 2;
+    tab.push_back(a);
+    tab.push_back(b);
+    return "KT[" + std::to_string(i) + "].x, KT[" + std::to_string(i) + "].y";
+  }
 };
 
 // Code of one layer word.
@@ -151,10 +163,10 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
       const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
       if (x & M_STAB) {
         if (a == 0.0 && b == 0.0) continue;  // identity entry
-        os << " pshear(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
+        os << " pshear(v" << s << ", " << kc.pair(a, b) << ");";
       } else {
         if (a == 1.0 && b == 0.0) continue;
-        os << " cscale(v" << s << ", " << kc(a) << ", " << kc(b) << ");";
+        os << " cscale(v" << s << ", " << kc.pair(a, b) << ");";
       }
     }
     os << "\n";
@@ -393,6 +405,7 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   const size_t nr = sp.rounds.size();
   std::ostringstream os;
   Consts kc;
+  kc.tab_array = sp.tab_const;
   // first / last round straight from / to HBM (no staging through smem)
   const Direct d0 = (!sp.pipe && nr) ? direct_round(sp, sp.rounds.front()) : Direct{};
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
@@ -536,7 +549,14 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   os << "  }\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && t == 0) atomicOr(flag, 1);\n";
   os << "}\n";
-  return kPrelude + os.str();
+  std::string head = kPrelude;
+  if (!kc.tab.empty()) {
+    head += "__constant__ double2 KT[" + std::to_string(kc.tab.size() / 2) + "] = {";
+    for (size_t i = 0; i < kc.tab.size(); i += 2)
+      head += (i ? ", {" : "{") + hexd(kc.tab[i]) + ", " + hexd(kc.tab[i + 1]) + "}";
+    head += "};\n";
+  }
+  return head + os.str();
 }
 
 std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
@@ -544,7 +564,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
   const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks,
-                          sp.coalesce_bits, sp.stagger_ns,
+                          sp.coalesce_bits, sp.stagger_ns, sp.tab_const,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
                           static_cast<int32_t>(mp.words.size()),

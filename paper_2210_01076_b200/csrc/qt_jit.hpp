@@ -44,6 +44,7 @@ struct JitPassSpec {
   // leave physical bits [0, coalesce_bits) to the threads (0 = never)
   int coalesce_bits = 0;
   int stagger_ns = 0;   // > 0: every second CTA of an SM starts this late
+  bool tab_const = false;  // table entries from a __constant__ array (else literals)
 };
 
 struct JitKernel {

@@ -22,15 +22,21 @@ for compiled in [int(x) for x in args.modes.split(',')]:
     t0 = time.perf_counter(); ok = jit_wait(300) if compiled >= 0 else True; wait = time.perf_counter() - t0
     lat = {"uniform": [], "tail": []}
     passes = []
+    plan_ms = []
+    from paper_2210_01076_b200 import _ffi, lib
+    import ctypes
     for m, mod in enumerate(w.modifiers[:args.mods]):
         cls = "tail" if (m // 2) % 2 == 1 else "uniform"
         t0 = time.perf_counter(); drv.modify(mod); sim.update_state()
         lat[cls].append((time.perf_counter() - t0) * 1e3)
         passes.append(sim.last_update().passes)
+        rs = _ffi.QtRunStats()
+        lib().qt_sim_last_update(sim._h, ctypes.byref(rs))
+        plan_ms.append(rs.plan_ms)
     nrm = sim.norm_squared()
     amps = sim.amplitudes(0, 1 << 10)
     sim.close()
-    print(json.dumps({"compiled": compiled, "seg": args.seg, "mean_passes": sum(passes) / len(passes), "full_ms": full, "bg_wait_s": wait, "bg_done": ok,
+    print(json.dumps({"compiled": compiled, "seg": args.seg, "mean_passes": sum(passes) / len(passes), "mean_plan_ms": sum(plan_ms) / len(plan_ms), "full_ms": full, "bg_wait_s": wait, "bg_done": ok,
                       "uniform": latency_stats(lat["uniform"]), "tail": latency_stats(lat["tail"]),
                       "norm_error": abs(nrm - 1), "amp0": [amps[0].real, amps[0].imag],
                       "jit": jit_stats()}), flush=True)
