@@ -190,7 +190,8 @@ int qt_plan_probe(int num_qubits, int global_qubits, int tile_qubits,
  * every tile pass and generates its compiled kernel; compile != 0 also runs
  * NVRTC on each. JSON {"passes","lowered","source_bytes","compiled",
  * "compile_ms","cubin_bytes"}; source_pass >= 0 returns that pass's CUDA
- * source instead. */
+ * source instead, source_pass == -2 the lowered layer words of every pass
+ * (JSON; tests/emulator.py replays them). */
 int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits,
                  int compile, int source_pass, const qt_gate* gates,
                  size_t count, char* buf, size_t cap, size_t* needed);

@@ -564,6 +564,45 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
     size_t last_tile = p.passes.size();
     for (size_t i = 0; i < p.passes.size(); ++i)
       if (p.passes[i].kind == qtb::PlanPass::Tile) last_tile = i;
+    if (source_pass == -2) {
+      // the lowered layer words of every pass (tests/emulator.py replays them)
+      std::string js = "{\"nqubits\":" + std::to_string(num_qubits) + ",\"passes\":[";
+      char hx[32];
+      for (size_t i = 0; i < p.passes.size(); ++i) {
+        const qtb::PlanPass& ps = p.passes[i];
+        if (i) js += ",";
+        if (!mp[i].ok) {
+          js += "{\"kind\":\"generic\"}";
+          continue;
+        }
+        const int R = std::min<int>(opt.reg_bits, static_cast<int>(ps.tile_phys.size()));
+        js += "{\"kind\":\"lowered\",\"R\":" + std::to_string(R) + ",\"tile_phys\":[";
+        for (size_t t = 0; t < ps.tile_phys.size(); ++t)
+          js += (t ? "," : "") + std::to_string(ps.tile_phys[t]);
+        js += "],\"rounds\":[";
+        for (size_t r = 0; r < ps.rounds.size(); ++r) {
+          js += std::string(r ? "," : "") + "{\"reg\":[";
+          for (size_t q = 0; q < ps.rounds[r].reg.size(); ++q)
+            js += (q ? "," : "") + std::to_string(ps.rounds[r].reg[q]);
+          js += "],\"first\":" + std::to_string(mp[i].round_first[r]) +
+                ",\"count\":" + std::to_string(mp[i].round_count[r]) + "}";
+        }
+        js += "],\"words\":[";
+        for (size_t w = 0; w < mp[i].size(); ++w)
+          js += std::string(w ? "," : "") + "[" + std::to_string(mp[i].words[2 * w]) + "," +
+                std::to_string(mp[i].words[2 * w + 1]) + "]";
+        js += "],\"pool\":[";
+        for (size_t k = 0; k < mp[i].pool.size(); ++k) {
+          uint64_t b;
+          std::memcpy(&b, &mp[i].pool[k], 8);
+          std::snprintf(hx, sizeof(hx), "\"%016llx\"", static_cast<unsigned long long>(b));
+          js += std::string(k ? "," : "") + hx;
+        }
+        js += "]}";
+      }
+      copy_out(js + "]}", buf, cap, needed);
+      return;
+    }
     size_t lowered = 0, bytes = 0, compiled = 0, cubin = 0;
     double ms = 0.0, fp = 0.0;
     std::string per = "[", rounds = "[";

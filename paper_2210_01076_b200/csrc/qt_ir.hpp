@@ -93,6 +93,15 @@ constexpr uint32_t M_SIGN = 1u << 26;    // sign flips (mask / terms in y)
 constexpr uint32_t M_PERM = 1u << 27;    // X / CX register permutation
 constexpr uint32_t M_NV_SHIFT = 28;      // tile-uniform sign terms of the table (2 bits)
 constexpr uint32_t M_LAST = 1u << 30;    // the round's last word (every round has one)
+// A lone diagonal gate the round compiler could not merge into a table (its
+// target or a control is a non-register tile bit or a global bit): per slot s
+// in the slot mask, multiply by d1 where the target bit is set, else d0.
+//   y = slot mask (16 bits) | (target slot + 1) << 16 (0: thread / tile bit)
+//       | M_TD_PHASE1 (d0 == 1: only set bits change)
+//   pool: [lmask (tile-local control bits), dl (tile-local target bit),
+//          gmask (global control bits), dg (global target bit), d0, d1]
+constexpr uint32_t M_TDIAG = 1u << 31;
+constexpr uint32_t M_TD_PHASE1 = 1u << 24;
 constexpr int kMaxTableVariantTerms = 3;
 
 // Variant id of a device op: the kernel dispatches on it to a fully

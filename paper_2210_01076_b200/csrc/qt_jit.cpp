@@ -155,6 +155,43 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
     os << " } }\n";
     return;
   }
+  if (x & M_TDIAG) {
+    const uint64_t lm = raw_bits(P[off]) & 0xffffffffull, dl = raw_bits(P[off + 1]) & 0xffffffffull;
+    const uint64_t gm = raw_bits(P[off + 2]), dg = raw_bits(P[off + 3]);
+    const int ds = static_cast<int>((y >> 16) & 15u) - 1;
+    const bool ph1 = (y & M_TD_PHASE1) != 0;
+    const std::string d0 = kc(P[off + 4]) + ", " + kc(P[off + 5]), d1 = kc(P[off + 6]) + ", " + kc(P[off + 7]);
+    os << "  {";
+    std::string cond;
+    if (lm) cond += "(jb & " + std::to_string(lm) + "u) == " + std::to_string(lm) + "u";
+    if (gm) cond += std::string(cond.empty() ? "" : " && ") + "(g & " + hexu(gm) + ") == " + hexu(gm);
+    if (!cond.empty()) os << " if (" << cond << ")";
+    os << " {";
+    if (ds < 0) {
+      std::string tb;
+      if (dl) tb += "(jb & " + std::to_string(dl) + "u) != 0";
+      if (dg) tb += std::string(tb.empty() ? "" : " || ") + "(g & " + hexu(dg) + ") != 0";
+      if (tb.empty()) tb = "false";
+      os << " const bool tb = " << tb << ";";
+      if (ph1) os << " if (tb) {";
+      for (int s = 0; s < NS; ++s) {
+        if (!((y >> s) & 1u)) continue;
+        if (ph1) os << " cscale(v" << s << ", " << d1 << ");";
+        else os << " cscale(v" << s << ", tb ? " << kc(P[off + 6]) << " : " << kc(P[off + 4]) << ", tb ? "
+                << kc(P[off + 7]) << " : " << kc(P[off + 5]) << ");";
+      }
+      if (ph1) os << " }";
+    } else {
+      for (int s = 0; s < NS; ++s) {
+        if (!((y >> s) & 1u)) continue;
+        const bool b = ((s >> ds) & 1) != 0;
+        if (ph1 && !b) continue;
+        os << " cscale(v" << s << ", " << (b ? d1 : d0) << ");";
+      }
+    }
+    os << " } }\n";
+    return;
+  }
   if (x & (M_STAB | M_CTAB)) {
     const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
     const uint32_t toff = off + 2 * nv;  // after nv (condition, slots) pairs

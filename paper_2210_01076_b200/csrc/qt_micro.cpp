@@ -17,6 +17,7 @@ constexpr double kMaxShear = 12.0;
 bool is_layer_lean(const DOp& d) {
   const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
   if (type == D_XPERM) return (d.hdr & (kOpDl | kOpDg)) == 0;
+  if (type == D_DIAG || type == D_PHASE1) return true;  // lowered to M_TDIAG words
   return type == D_LAYER && (d.hdr & kOpFlagMask) == 0;
 }
 
@@ -115,6 +116,27 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
           P.push_back(bits_as_double(d.gmask));
           mp.words.push_back(off | M_PERM);
           mp.words.push_back(d.hdr);
+          continue;
+        }
+        if (type == D_DIAG || type == D_PHASE1) {
+          const uint32_t v = d.hdr & kOpVariantMask;
+          const int cs = static_cast<int>((v >> 3) & 7u) - 1;
+          const int ds = static_cast<int>(v & 7u) - 1;
+          uint32_t smask = 0;
+          for (int sl = 0; sl < NS; ++sl)
+            if (cs < 0 || ((sl >> cs) & 1)) smask |= 1u << sl;
+          P.push_back(bits_as_double(d.lmask));
+          P.push_back(bits_as_double(d.dl));
+          P.push_back(bits_as_double(d.gmask));
+          P.push_back(bits_as_double(d.dg));
+          const size_t o = d.arg;
+          P.push_back(src[o]);      // d0 = m00
+          P.push_back(src[o + 1]);
+          P.push_back(src[o + 6]);  // d1 = m11
+          P.push_back(src[o + 7]);
+          mp.words.push_back(off | M_TDIAG);
+          mp.words.push_back(smask | (static_cast<uint32_t>(ds + 1) << 16) |
+                             (type == D_PHASE1 ? M_TD_PHASE1 : 0u));
           continue;
         }
         // D_LAYER pool: [table 2 NS][terms 2 nt][rotations 2 each][2x2s 8 each]
@@ -285,8 +307,11 @@ double micro_fp64_per_amp(const MicroPass& mp, int R) {
   double fp = 0.0;
   for (size_t w = 0; w < mp.size(); ++w) {
     const uint32_t x = mp.words[2 * w], y = mp.words[2 * w + 1];
-    (void)y;
     if (x & M_PERM) continue;
+    if (x & M_TDIAG) {
+      fp += 4.0 * __builtin_popcount(y & 0xffffu) / NS;
+      continue;
+    }
     uint32_t off = x & 0xffffu;
     if (x & (M_STAB | M_CTAB)) {
       const uint32_t nv = (x >> M_NV_SHIFT) & 3u;

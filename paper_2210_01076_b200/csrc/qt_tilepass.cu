@@ -471,6 +471,28 @@ __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uin
       k_perm<R>(v, w.y, d, jb, sg);
       continue;
     }
+    if (x & M_TDIAG) {
+      // a lone diagonal on a thread / tile bit (or a register slot under a
+      // thread / tile control): per-thread predicates, uniform slot loop
+      const uint32_t lm = static_cast<uint32_t>(__double_as_longlong(p.pool[off]));
+      const uint32_t dl = static_cast<uint32_t>(__double_as_longlong(p.pool[off + 1]));
+      const uint64_t gm = static_cast<uint64_t>(__double_as_longlong(p.pool[off + 2]));
+      const uint64_t dg = static_cast<uint64_t>(__double_as_longlong(p.pool[off + 3]));
+      const uint64_t g = *sg;
+      if ((jb & lm) != lm || (g & gm) != gm) continue;
+      const bool tb = (jb & dl) != 0 || (g & dg) != 0;
+      const int ds = static_cast<int>((w.y >> 16) & 15u) - 1;
+      const bool ph1 = (w.y & M_TD_PHASE1) != 0;
+      const double2 d0 = pl[(off >> 1) + 2], d1 = pl[(off >> 1) + 3];
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (!((w.y >> s) & 1u)) continue;
+        const bool b = ds >= 0 ? ((s >> ds) & 1) != 0 : tb;
+        if (ph1 && !b) continue;
+        cscale(v[s], b ? d1.x : d0.x, b ? d1.y : d0.y);
+      }
+      continue;
+    }
     if (x & (M_STAB | M_CTAB)) {
       const uint32_t nv = (x >> M_NV_SHIFT) & 3u;
       const double2* t = pl + (off >> 1) + nv;  // after nv (condition, slots) pairs

@@ -1,0 +1,83 @@
+"""Host-only parity of the lowered layer words (csrc/qt_micro.cpp) -- the
+instruction stream both device kernels execute: shear-form diagonal tables
+centred by a common phase (the removed scalars carried through the plan and
+folded into its last table), tile-uniform sign terms as slot flips, sign-only
+tables as integer flips, rotations as shears, X / CX permutations. The words
+of every pass are replayed by tests/emulator_lowered.py (an independent
+decoder of the documented layout) and compared with the dense oracle
+(oracle/, pinned to the reference oracle.cpp:15-50)."""
+import json
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2210_01076_b200 import jit_probe, workloads as W
+from paper_2210_01076_b200.gates import GateKind as K
+from paper_2210_01076_b200.gates import gate, gate_array, lower_to_reference
+from tests.emulator_lowered import apply_lowered
+from tests.test_planner import random_circuit, random_state
+
+# kinds whose passes lower completely (SWAP and off-register diagonal
+# variants keep generic passes)
+LEAN = [K.H, K.X, K.Y, K.Z, K.S, K.Sdg, K.T, K.Tdg, K.Rx, K.Ry, K.Rz, K.Cnot, K.Cz, K.U3]
+GEOMETRIES = [dict(), dict(tile_qubits=6, reg_bits=3, low_bits=2),
+              dict(tile_qubits=7, reg_bits=4, low_bits=3), dict(tile_qubits=5, reg_bits=2, low_bits=1)]
+
+
+def replay(n, gates, psi0=None, **geom):
+    plan = json.loads(jit_probe(n, gates, source_pass=-2, **geom))
+    if any(p["kind"] != "lowered" for p in plan["passes"]):
+        pytest.skip("plan has generic passes")
+    if psi0 is None:
+        psi0 = np.zeros(1 << n, dtype=np.complex128)
+        psi0[0] = 1.0
+    return apply_lowered(psi0, plan)
+
+
+@pytest.mark.parametrize("geom", range(len(GEOMETRIES)))
+def test_layered_u3_cz(geom):
+    w = W.config3(n=11, layers=6)
+    got = replay(w.n, w.gates, **GEOMETRIES[geom])
+    want = oracle.simulate(w.n, lower_to_reference(w.gates))
+    assert np.abs(got - want).max() <= 1e-12
+
+
+@pytest.mark.parametrize("geom", range(len(GEOMETRIES)))
+def test_config5_family(geom):
+    w = W.config5(n=11, ngates=250, nmods=0)
+    got = replay(w.n, w.gates, **GEOMETRIES[geom])
+    want = oracle.simulate(w.n, lower_to_reference(w.gates))
+    assert np.abs(got - want).max() <= 1e-12
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_lean_circuits(seed):
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.integers(3, 11))
+    g = random_circuit(rng, n, int(rng.integers(20, 200)), kinds=LEAN)
+    psi0 = random_state(rng, n)
+    geom = GEOMETRIES[seed % len(GEOMETRIES)]
+    if geom and geom["tile_qubits"] > n:
+        geom = dict(geom, tile_qubits=n)
+    plan = json.loads(jit_probe(n, g, source_pass=-2, **geom))
+    if any(p["kind"] != "lowered" for p in plan["passes"]):
+        pytest.skip("plan has generic passes")
+    got = apply_lowered(psi0, plan)
+    want = oracle.simulate(n, g, state=psi0.copy())
+    assert np.abs(got - want).max() <= 1e-12
+
+
+def test_sign_only_tables_are_flips_and_scalars_fold():
+    """RY with cos(theta/2) < 0 makes -1 factors (sign terms / tables of
+    +-1): they lower to integer flips, and a plan whose only table factors
+    are scalars still leaves the exact global phase (the carried scalar)."""
+    n = 6
+    rows = [gate(K.Ry, q, -1, 4.0 + q) for q in range(n)]
+    rows += [gate(K.Rz, q, -1, 0.7 * q) for q in range(n)]
+    g = gate_array(rows)
+    got = replay(n, g)
+    want = oracle.simulate(n, lower_to_reference(g))
+    assert np.abs(got - want).max() <= 1e-12
+    plan = json.loads(jit_probe(n, g, source_pass=-2))
+    assert all(p["kind"] == "lowered" for p in plan["passes"])
