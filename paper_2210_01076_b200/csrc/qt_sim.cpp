@@ -20,8 +20,11 @@
 // place into free chain buffers (the first pass of a segment reads the
 // previous checkpoint, so saving a checkpoint costs no extra HBM traffic).
 #include "qt_sim.hpp"
+#include "qt_jit.hpp"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 
@@ -52,6 +55,7 @@ Sim::Sim(int nqubits, const qt_config* cfg) : n_(nqubits) {
   const int want = cfg_.max_checkpoints > 0 ? cfg_.max_checkpoints + 1 : 48;
   const double frac = cfg_.checkpoint_fraction > 0 ? cfg_.checkpoint_fraction : 0.85;
   nbuf_ = st_->grow_pool(want, frac);
+  if (const char* e = std::getenv("QTB_SIM_TRACE")) trace_ = std::atoi(e) != 0;
 }
 
 // ---- circuit model (circuit.cpp) -------------------------------------------
@@ -287,6 +291,17 @@ void Sim::update_state() {
         st_->apply_ops(ops, b - a, st_->buffer(src.buf), &src.perm);
         chain_.push_back(Ckpt{b, dst, st_->perm()});
       }
+      if (trace_) {
+        const JitStats js = jit_stats();
+        std::fprintf(stderr, "qtask-b200 sim: segment [%llu, %llu) passes %llu hits %llu misses %llu host %.2f ms\n",
+                     static_cast<unsigned long long>(a), static_cast<unsigned long long>(b),
+                     static_cast<unsigned long long>(st_->stats.passes),
+                     static_cast<unsigned long long>(js.cache_hits - trace_hits_),
+                     static_cast<unsigned long long>(js.misses - trace_misses_),
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        trace_hits_ = js.cache_hits;
+        trace_misses_ = js.misses;
+      }
       stats.passes += st_->stats.passes;
       stats.kernel_launches += st_->stats.kernel_launches;
       stats.hbm_bytes += st_->stats.hbm_bytes;
@@ -296,7 +311,12 @@ void Sim::update_state() {
       a = b;
     }
     st_->bind(chain_.back().buf, chain_.back().perm);
+    const auto ts = std::chrono::steady_clock::now();
     st_->sync();  // raises QT_ERR_NUMERIC on a non-finite amplitude
+    if (trace_)
+      std::fprintf(stderr, "qtask-b200 sim: launched at %.2f ms, synced after %.2f ms more\n",
+                   std::chrono::duration<double, std::milli>(ts - t0).count(),
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count());
     bound_ids_.clear();
     for (const Ckpt& c : chain_)
       if (c.pos > 0 && c.pos < N) bound_ids_.push_back(ids[c.pos]);

@@ -71,6 +71,8 @@ class Sim {
   std::vector<uint32_t> bound_ids_;  // first gate of each segment of the last run (pos > 0)
   int nbuf_ = 1;
   qt_run_stats last_{};
+  bool trace_ = false;  // QTB_SIM_TRACE=1: per-segment timing / cache lines on stderr
+  uint64_t trace_hits_ = 0, trace_misses_ = 0;
 };
 
 }  // namespace qtb
