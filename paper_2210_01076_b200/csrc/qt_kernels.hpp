@@ -55,18 +55,22 @@ constexpr int micro_capacity() { return static_cast<int>(sizeof(P::ops) / 8); }
 // Fused tile pass over a state of 2^nlocal amplitudes. generic = false
 // selects the lean instantiation that only handles the fused layer ops
 // (MULTI, MULTIR, DTAB, STAB).
-// pipe = true: the double-buffered instantiation (the next tile is copied
-// into a second smem buffer with cp.async while the current one is worked
-// on; 2x the dynamic shared memory).
-cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool generic,
+// kmode: kKernelLean (layer words), kKernelLeanTdiag (layer words incl.
+// M_TDIAG: its handler costs the lean loop registers, so it has its own
+// instantiation) or kKernelGeneric (device ops). pipe = true: the
+// double-buffered instantiation (the next tile is copied into a second smem
+// buffer with cp.async while the current one is worked on; 2x the dynamic
+// shared memory).
+constexpr int kKernelLean = 0, kKernelGeneric = 1, kKernelLeanTdiag = 2;
+cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, int kmode,
                              bool pipe, cudaStream_t s);
-cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
+cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, int kmode,
                              bool pipe, cudaStream_t s);
 // Max threads per CTA of the tile-pass kernel for R register bits (its
 // launch bounds): a pass's tile has at most R + log2(this) bits.
 constexpr int tile_max_threads(int R) { return R >= 4 ? 256 : 512; }
 // Max resident CTAs per SM of the tile-pass kernel for (k, R).
-int tile_pass_occupancy(int k, int R, bool large, bool generic, bool pipe);
+int tile_pass_occupancy(int k, int R, bool large, int kmode, bool pipe);
 
 // Sets every amplitude to 0 and amplitude `index` to 1.
 cudaError_t launch_set_basis(double2* psi, uint64_t n, uint64_t index,

@@ -512,9 +512,13 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
               npool > static_cast<size_t>(kSmallPool) ||
               ps.rounds.size() > static_cast<size_t>(kSmallRounds);
     }
-    int occ_pipe = pipe_ ? tile_pass_occupancy(k, R, large, generic, true) : 0;
+    int kmode = generic ? kKernelGeneric : kKernelLean;
+    if (!generic)
+      for (size_t w = 0; w < mp.size(); ++w)
+        if (mp.words[2 * w] & M_TDIAG) kmode = kKernelLeanTdiag;
+    int occ_pipe = pipe_ ? tile_pass_occupancy(k, R, large, kmode, true) : 0;
     const bool pipe = occ_pipe > 0;
-    const int occ = std::max(1, pipe ? occ_pipe : tile_pass_occupancy(k, R, large, generic, false));
+    const int occ = std::max(1, pipe ? occ_pipe : tile_pass_occupancy(k, R, large, kmode, false));
     const uint64_t cap = static_cast<uint64_t>(occ) * sms_;
     const int grid = static_cast<int>(std::min<uint64_t>(h.ntiles, cap));
     tstart(0);
@@ -522,12 +526,12 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
       kp_large_->h = h;
       if (generic) fill_pass(*kp_large_, ps);
       else fill_pass_micro(*kp_large_, ps, mp);
-      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, generic, pipe, stream_), "tile pass launch");
+      cuda_check(launch_tile_pass(psi_, *kp_large_, grid, kmode, pipe, stream_), "tile pass launch");
     } else {
       kp_small_->h = h;
       if (generic) fill_pass(*kp_small_, ps);
       else fill_pass_micro(*kp_small_, ps, mp);
-      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, generic, pipe, stream_), "tile pass launch");
+      cuda_check(launch_tile_pass(psi_, *kp_small_, grid, kmode, pipe, stream_), "tile pass launch");
     }
     tstop();
     stats.passes += 1;

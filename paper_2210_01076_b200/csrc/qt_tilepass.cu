@@ -452,7 +452,7 @@ __device__ __forceinline__ void m_denses(double2 (&v)[1 << R], const double2*& q
 // Runs the layer words [o, o1) of a round. Each word's flag bits select the
 // compiled bodies: [table (variant chosen by tile-uniform conditions)]
 // [sign flips][rotation per slot][complex 2x2 per slot] (qt_ir.hpp).
-template <int R, typename P>
+template <int R, bool TD, typename P>
 __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uint32_t o,
                                            uint32_t jb, const uint64_t* sg) {
   constexpr int NS = 1 << R;
@@ -471,9 +471,10 @@ __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uin
       k_perm<R>(v, w.y, d, jb, sg);
       continue;
     }
-    if (x & M_TDIAG) {
+    if (TD && (x & M_TDIAG)) {
       // a lone diagonal on a thread / tile bit (or a register slot under a
       // thread / tile control): per-thread predicates, uniform slot loop
+      // (its own instantiation: the handler costs the lean loop registers)
       const uint32_t lm = static_cast<uint32_t>(__double_as_longlong(p.pool[off]));
       const uint32_t dl = static_cast<uint32_t>(__double_as_longlong(p.pool[off + 1]));
       const uint64_t gm = static_cast<uint64_t>(__double_as_longlong(p.pool[off + 2]));
@@ -568,9 +569,10 @@ __device__ __forceinline__ uint64_t next_tile_base(uint64_t base, uint64_t outer
 // PIPE = true: two smem tile buffers; tile i+1 streams in with cp.async
 // (no register staging) while tile i runs its register rounds, so every CTA
 // keeps a tile of loads in flight through its compute phase.
-template <int R, bool GENERIC, bool PIPE, typename P>
+template <int R, int KM, bool PIPE, typename P>
 __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
     tile_pass_kernel(double2* psi, const __grid_constant__ P p) {
+  constexpr bool GENERIC = KM == kKernelGeneric;
   extern __shared__ double2 sm[];
   constexpr int NS = 1 << R;
   const KPassHead& h = p.h;
@@ -663,7 +665,7 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
       }
       const uint32_t o1 = uint32_t(rd.op_first) + rd.op_count;
       if constexpr (!GENERIC) {
-        run_layers<R>(v, p, rd.op_first, jb, &s_tile[1]);
+        run_layers<R, KM == kKernelLeanTdiag>(v, p, rd.op_first, jb, &s_tile[1]);
       } else {
         // the next op's header is loaded while the current op runs (the
         // dispatch chain of an op starts from it; the op array always has a
@@ -716,56 +718,68 @@ __global__ void __launch_bounds__(kMaxThreads<R>, kMinBlocks<R>)
   if (__syncthreads_or(bad) && t == 0) atomicOr(h.flag, 1);
 }
 
-template <typename P, bool G, bool PIPE>
+template <typename P, int KM, bool PIPE>
 void* kernel_ptr(int R) {
   switch (R) {
-    case 1: return reinterpret_cast<void*>(&tile_pass_kernel<1, G, PIPE, P>);
-    case 2: return reinterpret_cast<void*>(&tile_pass_kernel<2, G, PIPE, P>);
-    case 3: return reinterpret_cast<void*>(&tile_pass_kernel<3, G, PIPE, P>);
-    default: return reinterpret_cast<void*>(&tile_pass_kernel<4, G, PIPE, P>);
+    case 1: return reinterpret_cast<void*>(&tile_pass_kernel<1, KM, PIPE, P>);
+    case 2: return reinterpret_cast<void*>(&tile_pass_kernel<2, KM, PIPE, P>);
+    case 3: return reinterpret_cast<void*>(&tile_pass_kernel<3, KM, PIPE, P>);
+    default: return reinterpret_cast<void*>(&tile_pass_kernel<4, KM, PIPE, P>);
   }
 }
 
-template <typename P>
-void* kernel_ptr(int R, bool generic, bool pipe) {
-  if (generic) return pipe ? kernel_ptr<P, true, true>(R) : kernel_ptr<P, true, false>(R);
-  return pipe ? kernel_ptr<P, false, true>(R) : kernel_ptr<P, false, false>(R);
+template <typename P, int KM>
+void* kernel_ptr(int R, bool pipe) {
+  return pipe ? kernel_ptr<P, KM, true>(R) : kernel_ptr<P, KM, false>(R);
 }
 
-template <typename P, bool G, bool PIPE>
+template <typename P>
+void* kernel_ptr(int R, int kmode, bool pipe) {
+  if (kmode == kKernelGeneric) return kernel_ptr<P, kKernelGeneric>(R, pipe);
+  if (kmode == kKernelLeanTdiag) return kernel_ptr<P, kKernelLeanTdiag>(R, pipe);
+  return kernel_ptr<P, kKernelLean>(R, pipe);
+}
+
+template <typename P, int KM, bool PIPE>
 cudaError_t launch(double2* psi, const P& p, int grid, cudaStream_t s) {
   const size_t smem = (PIPE ? 2 : 1) * (sizeof(double2) << p.h.k);
   const int threads = 1 << (p.h.k - p.h.reg_bits);
   switch (p.h.reg_bits) {
     case 1:
-      tile_pass_kernel<1, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<1, KM, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     case 2:
-      tile_pass_kernel<2, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<2, KM, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     case 3:
-      tile_pass_kernel<3, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<3, KM, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
     default:
-      tile_pass_kernel<4, G, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
+      tile_pass_kernel<4, KM, PIPE, P><<<grid, threads, smem, s>>>(psi, p);
       break;
   }
   return cudaGetLastError();
 }
 
+template <typename P, int KM>
+cudaError_t launch_pipe(double2* psi, const P& p, int grid, bool pipe, cudaStream_t s) {
+  return pipe ? launch<P, KM, true>(psi, p, grid, s) : launch<P, KM, false>(psi, p, grid, s);
+}
+
 template <typename P>
-cudaError_t launch_any(double2* psi, const P& p, int grid, bool generic, bool pipe,
+cudaError_t launch_any(double2* psi, const P& p, int grid, int kmode, bool pipe,
                        cudaStream_t s) {
-  if (generic) return pipe ? launch<P, true, true>(psi, p, grid, s) : launch<P, true, false>(psi, p, grid, s);
-  return pipe ? launch<P, false, true>(psi, p, grid, s) : launch<P, false, false>(psi, p, grid, s);
+  if (kmode == kKernelGeneric) return launch_pipe<P, kKernelGeneric>(psi, p, grid, pipe, s);
+  if (kmode == kKernelLeanTdiag) return launch_pipe<P, kKernelLeanTdiag>(psi, p, grid, pipe, s);
+  return launch_pipe<P, kKernelLean>(psi, p, grid, pipe, s);
 }
 
 }  // namespace
 
-int tile_pass_occupancy(int k, int R, bool large, bool generic, bool pipe) {
-  // per-device cache: (pipe, generic, large, k, R) -> resident CTAs per SM
+int tile_pass_occupancy(int k, int R, bool large, int kmode, bool pipe) {
+  // per-device cache: (pipe, kmode, large, k, R) -> resident CTAs per SM
   static thread_local int cache_dev = -1;
-  static thread_local int cache[8][kMaxTileBits + 1][kMaxRegBits + 1];
+  static thread_local int cache[12][kMaxTileBits + 1][kMaxRegBits + 1];
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev != cache_dev) {
@@ -774,12 +788,12 @@ int tile_pass_occupancy(int k, int R, bool large, bool generic, bool pipe) {
         for (int& v : row) v = -1;
     cache_dev = dev;
   }
-  int& slot = cache[(large ? 1 : 0) + (generic ? 2 : 0) + (pipe ? 4 : 0)][k][R];
+  int& slot = cache[(large ? 1 : 0) + 2 * kmode + (pipe ? 6 : 0)][k][R];
   if (slot >= 0) return slot;
   const size_t smem = (pipe ? 2 : 1) * (sizeof(double2) << k);
   const int threads = 1 << (k - R);
-  void* fn = large ? kernel_ptr<KPassLarge>(R, generic, pipe)
-                   : kernel_ptr<KPassSmall>(R, generic, pipe);
+  void* fn = large ? kernel_ptr<KPassLarge>(R, kmode, pipe)
+                   : kernel_ptr<KPassSmall>(R, kmode, pipe);
   int occ = 0;
   // the attribute is per function: always allow the largest tile (2^13
   // single-buffered, 2^12 double-buffered)
@@ -795,14 +809,14 @@ int tile_pass_occupancy(int k, int R, bool large, bool generic, bool pipe) {
   return occ;
 }
 
-cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, bool generic,
+cudaError_t launch_tile_pass(double2* psi, const KPassSmall& p, int grid, int kmode,
                              bool pipe, cudaStream_t s) {
-  return launch_any(psi, p, grid, generic, pipe, s);
+  return launch_any(psi, p, grid, kmode, pipe, s);
 }
 
-cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, bool generic,
+cudaError_t launch_tile_pass(double2* psi, const KPassLarge& p, int grid, int kmode,
                              bool pipe, cudaStream_t s) {
-  return launch_any(psi, p, grid, generic, pipe, s);
+  return launch_any(psi, p, grid, kmode, pipe, s);
 }
 
 }  // namespace qtb
