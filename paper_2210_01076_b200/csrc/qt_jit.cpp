@@ -827,7 +827,14 @@ void jit_compile_async(const std::string& key, const JitPassSpec& spec, const Mi
   if (g_exiting) return;
   if (g_queued->count(key)) return;
   (*g_queued)[key] = 1;
-  g_queue->push_back(Job{key, spec, mp, device});
+  // newest first (the latest edits' passes are the likeliest to recur), and a
+  // bounded backlog: under a stream of edits the oldest queued passes are
+  // dropped rather than compiled late
+  g_queue->push_front(Job{key, spec, mp, device});
+  while (g_queue->size() > kJitMaxBacklog) {
+    g_queued->erase(g_queue->back().key);
+    g_queue->pop_back();
+  }
   if (g_workers < kJitBackgroundThreads) {
     ++g_workers;
     // NVRTC recurses deeply on long straight-line kernels: give the

@@ -80,6 +80,7 @@ void jit_compile_async(const std::string& key, const JitPassSpec& spec, const Mi
 // Passes queued or compiling in the background.
 size_t jit_pending();
 constexpr int kJitBackgroundThreads = 4;
+constexpr size_t kJitMaxBacklog = 96;  // queued background compiles (newest kept)
 constexpr size_t kJitStackBytes = size_t(256) << 20;  // per compile thread (reserved, not touched)
 
 // Launches a compiled pass (grid = occupancy x SMs, capped by the tiles).
