@@ -233,6 +233,24 @@ Plan State::plan(const std::vector<LOp>& ops) const {
 }
 
 void State::apply(const qt_gate* gates, size_t count) {
+  // re-applying the gate list of the previous call from the same qubit map
+  // reuses its plan, lowering and compiled passes (no host planning)
+  std::string key(reinterpret_cast<const char*>(gates), count * sizeof(qt_gate));
+  key.append(reinterpret_cast<const char*>(perm_.data()), perm_.size() * sizeof(int));
+  if (last_.valid && last_.key == key) {
+    cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+    stats = qt_run_stats{};
+    stats.gates = count;
+    if (jit_mode_ == 2) {
+      // hybrid: passes compiled since the last call are picked up
+      Prepared pr = prepare(last_.plan);
+      launch_prepared(last_.plan, pr, nullptr);
+    } else {
+      launch_prepared(last_.plan, last_.prep, nullptr);
+    }
+    perm_ = last_.plan.perm_after;
+    return;
+  }
   std::vector<LOp> ops;
   ops.reserve(count);
   std::string err;
@@ -241,7 +259,19 @@ void State::apply(const qt_gate* gates, size_t count) {
     if (rc != QT_OK) fail(rc, err);
   }
   fuse_ops(ops, n_);
-  apply_ops(ops, count);
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  const auto t0 = std::chrono::steady_clock::now();
+  last_.valid = false;
+  last_.plan = plan(ops);
+  const auto t1 = std::chrono::steady_clock::now();
+  stats = qt_run_stats{};
+  stats.gates = count;
+  stats.plan_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  last_.prep = prepare(last_.plan);
+  last_.key = std::move(key);
+  last_.valid = true;
+  launch_prepared(last_.plan, last_.prep, nullptr);
+  perm_ = last_.plan.perm_after;
 }
 
 int State::grow_pool(int count, double max_fraction_of_free) {
@@ -355,38 +385,9 @@ bool micro_fits(const PlanPass& ps, const MicroPass& mp) {
 
 }  // namespace
 
-void State::upload_and_launch(const Plan& plan, const double2* src) {
-  cuda_check(cudaEventRecord(ev0_, stream_), "event");
-  size_t timing_idx = timings_used_;  // events accumulate until collected
-  auto tstart = [&](int kind) {
-    if (!timing_) return;
-    if (timing_idx >= timings_.size()) {
-      PassTiming t;
-      cudaEventCreate(&t.start);
-      cudaEventCreate(&t.stop);
-      timings_.push_back(t);
-    }
-    timings_[timing_idx].kind = kind;
-    cudaEventRecord(timings_[timing_idx].start, stream_);
-  };
-  auto tstop = [&]() {
-    if (!timing_) return;
-    cudaEventRecord(timings_[timing_idx].stop, stream_);
-    ++timing_idx;
-  };
-  const uint64_t buf_mask = buffer_amps() - 1;
-  // out-of-place start: the first tile pass reads src; otherwise copy
-  if (src && (plan.passes.empty() || plan.passes[0].kind != PlanPass::Tile)) {
-    cuda_check(cudaMemcpyAsync(psi_, src, sizeof(double2) * buffer_amps(),
-                               cudaMemcpyDeviceToDevice, stream_),
-               "state copy");
-    stats.kernel_launches += 1;
-    stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
-    src = nullptr;
-  }
-  if (!kp_small_) kp_small_.reset(new KPassSmall);
-  if (!kp_large_) kp_large_.reset(new KPassLarge);
-  const std::vector<MicroPass> micro = lower_plan_micro(
+State::Prepared State::prepare(const Plan& plan) {
+  Prepared pr;
+  pr.micro = lower_plan_micro(
       plan, opt_.reg_bits,
       MicroLimits{static_cast<size_t>(micro_capacity<KPassLarge>()),
                   sizeof(KPassLarge::pool) / sizeof(double),
@@ -394,7 +395,9 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
   size_t last_tile = plan.passes.size();
   for (size_t pi = 0; pi < plan.passes.size(); ++pi)
     if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
-  std::vector<JitKernel> jk(plan.passes.size());
+  pr.jk.assign(plan.passes.size(), JitKernel{});
+  const std::vector<MicroPass>& micro = pr.micro;
+  std::vector<JitKernel>& jk = pr.jk;
   if (jit_mode_) {
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<JitPassSpec> specs(plan.passes.size());
@@ -438,6 +441,47 @@ void State::upload_and_launch(const Plan& plan, const double2* src) {
     }
     stats.plan_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
+  return pr;
+}
+
+void State::upload_and_launch(const Plan& plan, const double2* src) { launch_prepared(plan, prepare(plan), src); }
+
+void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2* src) {
+  cuda_check(cudaEventRecord(ev0_, stream_), "event");
+  size_t timing_idx = timings_used_;  // events accumulate until collected
+  auto tstart = [&](int kind) {
+    if (!timing_) return;
+    if (timing_idx >= timings_.size()) {
+      PassTiming t;
+      cudaEventCreate(&t.start);
+      cudaEventCreate(&t.stop);
+      timings_.push_back(t);
+    }
+    timings_[timing_idx].kind = kind;
+    cudaEventRecord(timings_[timing_idx].start, stream_);
+  };
+  auto tstop = [&]() {
+    if (!timing_) return;
+    cudaEventRecord(timings_[timing_idx].stop, stream_);
+    ++timing_idx;
+  };
+  const uint64_t buf_mask = buffer_amps() - 1;
+  // out-of-place start: the first tile pass reads src; otherwise copy
+  if (src && (plan.passes.empty() || plan.passes[0].kind != PlanPass::Tile)) {
+    cuda_check(cudaMemcpyAsync(psi_, src, sizeof(double2) * buffer_amps(),
+                               cudaMemcpyDeviceToDevice, stream_),
+               "state copy");
+    stats.kernel_launches += 1;
+    stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
+    src = nullptr;
+  }
+  if (!kp_small_) kp_small_.reset(new KPassSmall);
+  if (!kp_large_) kp_large_.reset(new KPassLarge);
+  const std::vector<MicroPass>& micro = pr.micro;
+  const std::vector<JitKernel>& jk = pr.jk;
+  size_t last_tile = plan.passes.size();
+  for (size_t pi = 0; pi < plan.passes.size(); ++pi)
+    if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
   for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
     const PlanPass& ps = plan.passes[pi];
     if (ps.kind == PlanPass::Exchange) {

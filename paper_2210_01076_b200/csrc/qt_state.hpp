@@ -13,6 +13,7 @@
 #include "qt_kernels.hpp"
 #include "qt_plan.hpp"
 #include "qt_jit.hpp"
+#include "qt_micro.hpp"
 #include "qtask_c.h"
 
 namespace qtb {
@@ -105,7 +106,23 @@ class State {
   qt_run_stats stats{};
 
  private:
+  // the per-plan host work before launching: lowering + compiled passes
+  struct Prepared {
+    std::vector<MicroPass> micro;
+    std::vector<JitKernel> jk;
+  };
+  Prepared prepare(const Plan& plan);
+  void launch_prepared(const Plan& plan, const Prepared& pr, const double2* src);
   void upload_and_launch(const Plan& plan, const double2* src);
+  // apply(): the previous call's plan, reused when the same gate list is
+  // applied again from the same qubit map
+  struct LastApply {
+    bool valid = false;
+    std::string key;
+    Plan plan;
+    Prepared prep;
+  };
+  LastApply last_;
   void exchange(const PlanPass& pass);
 
   int n_ = 0, nlocal_ = 0, buf_bits_ = 0;

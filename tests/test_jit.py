@@ -177,3 +177,23 @@ def test_hybrid_compiled_bitwise_equals_interpreter(gpu):
     assert after["cache_hits"] > before["cache_hits"]
     assert first.tobytes() == second.tobytes()
     assert np.abs(first - oracle.simulate(20, w.gates)).max() <= TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("compiled", [0, 1])
+def test_repeated_apply_reuses_plan(gpu, compiled):
+    """apply() of the previous gate list reuses its plan (and compiled passes);
+    a different list, or a changed state, is planned afresh -- results stay
+    those of the oracle either way."""
+    rng = np.random.default_rng(77)
+    n = 14
+    a = random_circuit(rng, n, 120, kinds=[K.H, K.Rx, K.Ry, K.Rz, K.Cnot, K.Cz, K.T])
+    b = random_circuit(rng, n, 90, kinds=[K.H, K.Ry, K.Cnot, K.S])
+    st = StateVector(n, compiled=compiled)
+    psi = np.zeros(1 << n, dtype=np.complex128)
+    psi[0] = 1
+    for g in (a, a, b, a, b, b):
+        st.apply(g)
+        psi = oracle.simulate(n, g, state=psi)
+        assert np.abs(st.read() - psi).max() <= TOL
+    st.close()
