@@ -488,6 +488,13 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
     cp_tile("base", "sm0");
     os << "  }\n";
   }
+  // register prefetch of the next tile's first round-0 slots (direct round 0)
+  const int npf = (d0.ok && !sp.pipe) ? std::min(sp.pf_regs, NS) : 0;
+  if (npf > 0) {
+    os << " ";
+    for (int s0 = 0; s0 < npf; ++s0) os << " double2 n" << s0 << " = make_double2(0.0, 0.0);";
+    os << "\n";
+  }
   os << "  for (u64 tile = t0; tile < t1; ++tile) {\n";
   if (sp.pipe) {
     os << "    char* const smb = sm0 + cur;\n"
@@ -529,7 +536,17 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
     for (int s = 0; s < NS; ++s)
       for (int i = 0; i < R; ++i)
         if (s & (1 << i)) sb[s] ^= rd.sbit[i];
-    if (first_direct) {
+    if (first_direct && npf > 0) {
+      // slots [0, npf) were loaded during the previous tile's last round
+      os << " const char* gs = reinterpret_cast<const char*>(src + base + off_d0);\n     ";
+      for (int s = 0; s < NS; ++s) {
+        if (s < npf)
+          os << " double2 v" << s << " = (tile == t0) ? __ldcs(reinterpret_cast<const double2*>(gs + "
+             << d0.off[s] << "ull)) : n" << s << ";";
+        else
+          os << " double2 v" << s << " = __ldcs(reinterpret_cast<const double2*>(gs + " << d0.off[s] << "ull));";
+      }
+    } else if (first_direct) {
       os << " const char* gs = reinterpret_cast<const char*>(src + base + off_d0);\n     ";
       for (int s = 0; s < NS; ++s)
         os << " double2 v" << s << " = __ldcs(reinterpret_cast<const double2*>(gs + " << d0.off[s] << "ull));";
@@ -552,6 +569,13 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
         os << " double2 v" << s << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s] << "u));";
     }
     os << "\n";
+    if (npf > 0 && r + 1 == nr) {
+      os << "      if (tile + 1 < t1) { const char* gn = reinterpret_cast<const char*>(src + (((base | ~"
+         << outer << ") + 1) & " << outer << ") + off_d0);";
+      for (int s = 0; s < npf; ++s)
+        os << " n" << s << " = __ldcs(reinterpret_cast<const double2*>(gn + " << d0.off[s] << "ull));";
+      os << " }\n";
+    }
     const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
     for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
     if (last_direct) {
@@ -601,7 +625,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
   const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks,
-                          sp.coalesce_bits, sp.stagger_ns, sp.tab_const,
+                          sp.coalesce_bits, sp.stagger_ns, sp.tab_const, sp.pf_regs,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
                           static_cast<int32_t>(mp.words.size()),

@@ -45,6 +45,7 @@ struct JitPassSpec {
   int coalesce_bits = 0;
   int stagger_ns = 0;   // > 0: every second CTA of an SM starts this late
   bool tab_const = false;  // table entries from a __constant__ array (else literals)
+  int pf_regs = 0;  // round-0 slots of the next tile loaded into registers during the last round
 };
 
 struct JitKernel {

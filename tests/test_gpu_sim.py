@@ -307,3 +307,48 @@ def test_cpp_dropin_program(gpu):
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "[FAIL]" not in out.stdout
+
+
+def test_config5_shape_hybrid_compiled(gpu):
+    """The incremental engine's default at >= 20 qubits: hybrid compiled
+    passes (segments found in the compile cache run compiled, the others on
+    the interpreter while they compile). C5 shape at n=20, 1200 gates, 24
+    modifiers. Engine A's first update runs cold (every pass on the
+    interpreter); engine B, built after the background compiles drained,
+    runs the same plans compiled: bit-identical states. Then the same edits
+    on both, the oracle after every 4th update, and an interpreter-only
+    engine (its own tile geometry) within 1e-12."""
+    from paper_2210_01076_b200 import jit_stats, jit_wait
+    n = 20
+    w = W.config5(n=n, ngates=1200, nmods=24, seed=55)
+    cfg = Config(256, 0, max_checkpoints=8)
+    a = Simulator(n, cfg)
+    da = W.NetDriver(a)
+    da.build(w.gates)
+    a.update_state()
+    cold = a.amplitudes(0, (1 << n) - 1)
+    assert jit_wait(300)
+    hits0 = jit_stats()["cache_hits"]
+    b = Simulator(n, cfg)
+    db = W.NetDriver(b)
+    db.build(w.gates)
+    b.update_state()
+    assert jit_stats()["cache_hits"] > hits0
+    assert b.amplitudes(0, (1 << n) - 1).tobytes() == cold.tobytes()
+    c = Simulator(n, Config(256, 0, max_checkpoints=8, compiled=-1))
+    dc = W.NetDriver(c)
+    dc.build(w.gates)
+    c.update_state()
+    gates = w.gates
+    for m, mod in enumerate(w.modifiers):
+        for s, d in ((a, da), (b, db), (c, dc)):
+            d.modify(mod)
+            s.update_state()
+        gates = W.apply_modifier(gates, mod)
+        va = a.amplitudes(0, (1 << n) - 1)
+        assert va.tobytes() == b.amplitudes(0, (1 << n) - 1).tobytes()
+        assert np.abs(va - c.amplitudes(0, (1 << n) - 1)).max() <= 1e-12
+        if m % 4 == 0:
+            assert np.abs(va - oracle.simulate(n, gates)).max() <= 1e-10
+    for s in (a, b, c):
+        s.close()
