@@ -67,6 +67,9 @@ FI void shear(double2& x, double2& y, double a, double b) {
 FI void pshear(double2& v, double a, double b) {
   v.x = fma(a, v.y, v.x); v.y = fma(b, v.x, v.y); v.x = fma(a, v.y, v.x);
 }
+FI void pshear2(double2& v, const double2 ab) { pshear(v, ab.x, ab.y); }
+FI void cscale(double2& x, double br, double bi);
+FI void cscale2(double2& x, const double2 c) { cscale(x, c.x, c.y); }
 FI void cscale(double2& x, double br, double bi) {
   const double p0 = -bi * x.y, p1 = bi * x.x;
   x.x = fma(br, x.x, p0); x.y = fma(br, x.y, p1);
@@ -120,15 +123,24 @@ struct Consts {
   // read as double2 (one 16-B uniform load per entry instead of four
   // uniform moves): QTB_JIT_TABCONST=1
   bool tab_array = false;
+  bool tab_smem = false;  // ... copied once per CTA into shared memory (KS)
   std::vector<double> tab;
   std::string pair(double a, double b) {
-    if (!tab_array) return hexd(a) + ", " + hexd(b);
+    if (!tab_array && !tab_smem) return hexd(a) + ", " + hexd(b);
     const size_t i = tab.size() / 2;
     tab.push_back(a);
     tab.push_back(b);
+    if (tab_smem) return "KS[" + std::to_string(i) + "]";
     return "KT[" + std::to_string(i) + "].x, KT[" + std::to_string(i) + "].y";
   }
 };
+
+// QTB_JIT_STEPMAJOR=1: rotations emitted shear step by shear step across
+// the pairs (an instruction-order experiment; the arithmetic is identical)
+const bool g_step_major = [] {
+  const char* e = std::getenv("QTB_JIT_STEPMAJOR");
+  return e && std::atoi(e) != 0;
+}();
 
 // Code of one layer word.
 void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y,
@@ -200,10 +212,10 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
       const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
       if (x & M_STAB) {
         if (a == 0.0 && b == 0.0) continue;  // identity entry
-        os << " pshear(v" << s << ", " << kc.pair(a, b) << ");";
+        os << (kc.tab_smem ? " pshear2(v" : " pshear(v") << s << ", " << kc.pair(a, b) << ");";
       } else {
         if (a == 1.0 && b == 0.0) continue;
-        os << " cscale(v" << s << ", " << kc.pair(a, b) << ");";
+        os << (kc.tab_smem ? " cscale2(v" : " cscale(v") << s << ", " << kc.pair(a, b) << ");";
       }
     }
     os << "\n";
@@ -250,9 +262,25 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
     const double ca = P[off], cb = P[off + 1];
     off += 2;
     os << " ";
-    for (int s = 0; s < NS; ++s) {
-      if (s & (1 << a)) continue;
-      os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << kc(ca) << ", " << kc(cb) << ");";
+    if (g_step_major) {
+      // step-major: each of the three shears across all pairs before the next
+      const std::string A = kc(ca), B = kc(cb);
+      for (int step = 0; step < 3; ++step)
+        for (int s = 0; s < NS; ++s) {
+          if (s & (1 << a)) continue;
+          const int s1 = s | (1 << a);
+          if (step == 1)
+            os << " v" << s1 << ".x = fma(" << B << ", v" << s << ".x, v" << s1 << ".x); v" << s1
+               << ".y = fma(" << B << ", v" << s << ".y, v" << s1 << ".y);";
+          else
+            os << " v" << s << ".x = fma(" << A << ", v" << s1 << ".x, v" << s << ".x); v" << s
+               << ".y = fma(" << A << ", v" << s1 << ".y, v" << s << ".y);";
+        }
+    } else {
+      for (int s = 0; s < NS; ++s) {
+        if (s & (1 << a)) continue;
+        os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << kc(ca) << ", " << kc(cb) << ");";
+      }
     }
     os << "\n";
   }
@@ -443,6 +471,7 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   std::ostringstream os;
   Consts kc;
   kc.tab_array = sp.tab_const;
+  kc.tab_smem = sp.tab_smem && !sp.tab_const;
   // first / last round straight from / to HBM (no staging through smem)
   const Direct d0 = (!sp.pipe && nr) ? direct_round(sp, sp.rounds.front()) : Direct{};
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
@@ -487,6 +516,14 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
        << "  if (t0 < t1) {\n";
     cp_tile("base", "sm0");
     os << "  }\n";
+  }
+  if (kc.tab_smem && sp.tab_entries > 0) {
+    // the pass's table constants, copied once per CTA behind the tile
+    // buffer(s): one 16-B shared load per entry instead of four uniform moves
+    os << "  double2* const KS = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + "
+       << (sp.pipe ? 2 : 1) * (16u << k) << "u);\n"
+       << "  for (u32 i = t; i < @@NTAB@@u; i += blockDim.x) KS[i] = KT[i];\n"
+       << "  __syncthreads();\n";
   }
   // register prefetch of the next tile's first round-0 slots (direct round 0)
   const int npf = (d0.ok && !sp.pipe) ? std::min(sp.pf_regs, NS) : 0;
@@ -610,14 +647,25 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   os << "  }\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && t == 0) atomicOr(flag, 1);\n";
   os << "}\n";
+  std::string body = os.str();
+  const size_t ph = body.find("@@NTAB@@");
+  if (ph != std::string::npos) body.replace(ph, 8, std::to_string(kc.tab.size() / 2));
   std::string head = kPrelude;
-  if (!kc.tab.empty()) {
-    head += "__constant__ double2 KT[" + std::to_string(kc.tab.size() / 2) + "] = {";
+  if (!kc.tab.empty() || ph != std::string::npos) {
+    head += "__constant__ double2 KT[" + std::to_string(std::max<size_t>(1, kc.tab.size() / 2)) + "] = {";
     for (size_t i = 0; i < kc.tab.size(); i += 2)
       head += (i ? ", {" : "{") + hexd(kc.tab[i]) + ", " + hexd(kc.tab[i + 1]) + "}";
+    if (kc.tab.empty()) head += "{0.0, 0.0}";
     head += "};\n";
   }
-  return head + os.str();
+  return head + body;
+}
+
+int count_table_entries(const MicroPass& mp, int R) {
+  int n = 0;
+  for (size_t w = 0; w < mp.size(); ++w)
+    if (mp.words[2 * w] & (M_STAB | M_CTAB)) n += 1 << R;
+  return n;
 }
 
 std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
@@ -625,7 +673,8 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
   const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks,
-                          sp.coalesce_bits, sp.stagger_ns, sp.tab_const, sp.pf_regs,
+                          sp.coalesce_bits, sp.stagger_ns, sp.tab_const, sp.pf_regs, sp.tab_smem,
+                          sp.tab_entries,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
                           static_cast<int32_t>(mp.words.size()),
@@ -656,7 +705,8 @@ CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp) {
     throw std::runtime_error("loading a compiled pass failed");
   }
   e.k.threads = 1 << (sp.k - sp.R);
-  e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
+  e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k) +
+             (sp.tab_smem && !sp.tab_const ? sizeof(double2) * sp.tab_entries : 0);
   const void* fn = reinterpret_cast<const void*>(e.k.fn);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(e.k.smem)) != cudaSuccess ||

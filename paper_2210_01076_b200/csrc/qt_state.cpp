@@ -102,6 +102,7 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   if (const char* e = std::getenv("QTB_JIT_STAGGER")) stagger_ns_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_JIT_TABCONST")) tab_const_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_JIT_PFREGS")) pf_regs_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("QTB_JIT_TABSMEM")) tab_smem_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_PIPE")) pipe_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_PIPE_MAXFP")) pipe_max_fp64_ = std::atof(e);
   if (const char* e = std::getenv("QTB_PF")) {
@@ -418,6 +419,8 @@ State::Prepared State::prepare(const Plan& plan) {
       sp.stagger_ns = stagger_ns_;
       sp.tab_const = tab_const_;
       sp.pf_regs = pf_regs_;
+      sp.tab_smem = tab_smem_;
+      sp.tab_entries = count_table_entries(micro[pi], sp.R);
       if (pf_ && !sp.pipe) {
         int run = 0;
         while (run < sp.k - sp.R && ps.tile_phys[run] == run) ++run;

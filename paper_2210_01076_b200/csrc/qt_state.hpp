@@ -164,6 +164,7 @@ class State {
   int stagger_ns_ = 0;  // compiled passes: start delay of every 2nd CTA per SM
   bool tab_const_ = false;  // compiled passes: table entries from __constant__
   int pf_regs_ = 0;  // compiled passes: next-tile round-0 slots prefetched into registers
+  bool tab_smem_ = false;  // compiled passes: table entries from shared memory
   int occupancy_ = 1, sms_ = 148;
   bool timing_ = false;
   std::vector<PassTiming> timings_;
