@@ -618,9 +618,6 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
       if (const char* e = std::getenv("QTB_PIPE")) sp.pipe = std::atoi(e) != 0 && 2 * (16u << sp.k) <= 200u * 1024u;
       if (const char* e = std::getenv("QTB_JIT_MINB")) sp.min_blocks = std::atoi(e);
       sp.coalesce_bits = qtb::kJitDirectBits;
-      if (const char* e = std::getenv("QTB_JIT_PFREGS")) sp.pf_regs = std::atoi(e);
-      if (const char* e = std::getenv("QTB_JIT_TABSMEM")) sp.tab_smem = std::atoi(e) != 0;
-      sp.tab_entries = qtb::count_table_entries(mp[i], sp.R);
       if (const char* e = std::getenv("QTB_DIRECT_BITS")) sp.coalesce_bits = std::atoi(e);
       const std::string src = qtb::jit_source(sp, mp[i]);
       if (source_pass >= 0) {

@@ -67,9 +67,6 @@ FI void shear(double2& x, double2& y, double a, double b) {
 FI void pshear(double2& v, double a, double b) {
   v.x = fma(a, v.y, v.x); v.y = fma(b, v.x, v.y); v.x = fma(a, v.y, v.x);
 }
-FI void pshear2(double2& v, const double2 ab) { pshear(v, ab.x, ab.y); }
-FI void cscale(double2& x, double br, double bi);
-FI void cscale2(double2& x, const double2 c) { cscale(x, c.x, c.y); }
 FI void cscale(double2& x, double br, double bi) {
   const double p0 = -bi * x.y, p1 = bi * x.x;
   x.x = fma(br, x.x, p0); x.y = fma(br, x.y, p1);
@@ -114,33 +111,14 @@ uint64_t raw_bits(double d) {
 }
 
 // FP64 constants of a pass, as hex-float literals in the instruction stream.
-// (A __constant__ array read with LDCU measured slower on C3: the pass's
-// constants overflow the per-SM constant cache; literals ride the
-// instruction fetch, two uniform moves per non-encodable double.)
+// (Measured slower on C3 and removed: the constants in a __constant__ array
+// read with uniform loads -- the pass's constants overflow the per-SM
+// constant cache -- or copied once per CTA into shared memory. Literals ride
+// the instruction fetch, two uniform moves per non-encodable double.)
 struct Consts {
   std::string operator()(double d) const { return hexd(d); }
-  // table entries (a, b) may instead come from a per-pass __constant__ array
-  // read as double2 (one 16-B uniform load per entry instead of four
-  // uniform moves): QTB_JIT_TABCONST=1
-  bool tab_array = false;
-  bool tab_smem = false;  // ... copied once per CTA into shared memory (KS)
-  std::vector<double> tab;
-  std::string pair(double a, double b) {
-    if (!tab_array && !tab_smem) return hexd(a) + ", " + hexd(b);
-    const size_t i = tab.size() / 2;
-    tab.push_back(a);
-    tab.push_back(b);
-    if (tab_smem) return "KS[" + std::to_string(i) + "]";
-    return "KT[" + std::to_string(i) + "].x, KT[" + std::to_string(i) + "].y";
-  }
+  std::string pair(double a, double b) const { return hexd(a) + ", " + hexd(b); }
 };
-
-// QTB_JIT_STEPMAJOR=1: rotations emitted shear step by shear step across
-// the pairs (an instruction-order experiment; the arithmetic is identical)
-const bool g_step_major = [] {
-  const char* e = std::getenv("QTB_JIT_STEPMAJOR");
-  return e && std::atoi(e) != 0;
-}();
 
 // Code of one layer word.
 void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y,
@@ -212,10 +190,10 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
       const double a = P[toff + 2 * s], b = P[toff + 2 * s + 1];
       if (x & M_STAB) {
         if (a == 0.0 && b == 0.0) continue;  // identity entry
-        os << (kc.tab_smem ? " pshear2(v" : " pshear(v") << s << ", " << kc.pair(a, b) << ");";
+        os << " pshear(v" << s << ", " << kc.pair(a, b) << ");";
       } else {
         if (a == 1.0 && b == 0.0) continue;
-        os << (kc.tab_smem ? " cscale2(v" : " cscale(v") << s << ", " << kc.pair(a, b) << ");";
+        os << " cscale(v" << s << ", " << kc.pair(a, b) << ");";
       }
     }
     os << "\n";
@@ -262,25 +240,9 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
     const double ca = P[off], cb = P[off + 1];
     off += 2;
     os << " ";
-    if (g_step_major) {
-      // step-major: each of the three shears across all pairs before the next
-      const std::string A = kc(ca), B = kc(cb);
-      for (int step = 0; step < 3; ++step)
-        for (int s = 0; s < NS; ++s) {
-          if (s & (1 << a)) continue;
-          const int s1 = s | (1 << a);
-          if (step == 1)
-            os << " v" << s1 << ".x = fma(" << B << ", v" << s << ".x, v" << s1 << ".x); v" << s1
-               << ".y = fma(" << B << ", v" << s << ".y, v" << s1 << ".y);";
-          else
-            os << " v" << s << ".x = fma(" << A << ", v" << s1 << ".x, v" << s << ".x); v" << s
-               << ".y = fma(" << A << ", v" << s1 << ".y, v" << s << ".y);";
-        }
-    } else {
-      for (int s = 0; s < NS; ++s) {
-        if (s & (1 << a)) continue;
-        os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << kc(ca) << ", " << kc(cb) << ");";
-      }
+    for (int s = 0; s < NS; ++s) {
+      if (s & (1 << a)) continue;
+      os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << kc(ca) << ", " << kc(cb) << ");";
     }
     os << "\n";
   }
@@ -470,14 +432,11 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   const size_t nr = sp.rounds.size();
   std::ostringstream os;
   Consts kc;
-  kc.tab_array = sp.tab_const;
-  kc.tab_smem = sp.tab_smem && !sp.tab_const;
   // first / last round straight from / to HBM (no staging through smem)
   const Direct d0 = (!sp.pipe && nr) ? direct_round(sp, sp.rounds.front()) : Direct{};
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
   // launch bounds: <= 64 registers for R <= 3, <= 128 for R = 4
   const int minb = sp.min_blocks > 0 ? sp.min_blocks : std::max(1, (R >= 4 ? 512 : 1024) / threads);
-  if (sp.stagger_ns > 0) os << "__device__ u32 qt_smctr[256];\n";
   os << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << minb << ")\n"
      << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per) {\n"
      << "  extern __shared__ double2 sm[];\n"
@@ -487,15 +446,6 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
      << "  const u32 st4 = swz(t) << 4;\n";
   if (d0.ok) os << "  const u64 off_d0 = pdep64(t, " << hexu(d0.tmask) << ");\n";
   if (dl.ok) os << "  const u64 off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
-  if (sp.stagger_ns > 0) {
-    // the second CTA of each SM starts late, so the two CTAs' load and
-    // compute phases interleave instead of running in lock step
-    os << "  { __shared__ u32 s_rank;\n"
-       << "    if (t == 0) { u32 smid; asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(smid));\n"
-       << "      s_rank = atomicAdd(&qt_smctr[smid & 255u], 1u) & 1u; }\n"
-       << "    __syncthreads();\n"
-       << "    if (s_rank) __nanosleep(" << sp.stagger_ns << "u); }\n";
-  }
   os << "  const u64 t0 = u64(blockIdx.x) * per;\n"
      << "  const u64 t1 = t0 + per < " << hexu(sp.ntiles) << " ? t0 + per : " << hexu(sp.ntiles) << ";\n"
      << "  u64 base = pdep64(t0, " << hexu(sp.outer_mask) << ");\n"
@@ -516,21 +466,6 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
        << "  if (t0 < t1) {\n";
     cp_tile("base", "sm0");
     os << "  }\n";
-  }
-  if (kc.tab_smem && sp.tab_entries > 0) {
-    // the pass's table constants, copied once per CTA behind the tile
-    // buffer(s): one 16-B shared load per entry instead of four uniform moves
-    os << "  double2* const KS = reinterpret_cast<double2*>(reinterpret_cast<char*>(sm) + "
-       << (sp.pipe ? 2 : 1) * (16u << k) << "u);\n"
-       << "  for (u32 i = t; i < @@NTAB@@u; i += blockDim.x) KS[i] = KT[i];\n"
-       << "  __syncthreads();\n";
-  }
-  // register prefetch of the next tile's first round-0 slots (direct round 0)
-  const int npf = (d0.ok && !sp.pipe) ? std::min(sp.pf_regs, NS) : 0;
-  if (npf > 0) {
-    os << " ";
-    for (int s0 = 0; s0 < npf; ++s0) os << " double2 n" << s0 << " = make_double2(0.0, 0.0);";
-    os << "\n";
   }
   os << "  for (u64 tile = t0; tile < t1; ++tile) {\n";
   if (sp.pipe) {
@@ -573,17 +508,7 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
     for (int s = 0; s < NS; ++s)
       for (int i = 0; i < R; ++i)
         if (s & (1 << i)) sb[s] ^= rd.sbit[i];
-    if (first_direct && npf > 0) {
-      // slots [0, npf) were loaded during the previous tile's last round
-      os << " const char* gs = reinterpret_cast<const char*>(src + base + off_d0);\n     ";
-      for (int s = 0; s < NS; ++s) {
-        if (s < npf)
-          os << " double2 v" << s << " = (tile == t0) ? __ldcs(reinterpret_cast<const double2*>(gs + "
-             << d0.off[s] << "ull)) : n" << s << ";";
-        else
-          os << " double2 v" << s << " = __ldcs(reinterpret_cast<const double2*>(gs + " << d0.off[s] << "ull));";
-      }
-    } else if (first_direct) {
+    if (first_direct) {
       os << " const char* gs = reinterpret_cast<const char*>(src + base + off_d0);\n     ";
       for (int s = 0; s < NS; ++s)
         os << " double2 v" << s << " = __ldcs(reinterpret_cast<const double2*>(gs + " << d0.off[s] << "ull));";
@@ -606,13 +531,6 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
         os << " double2 v" << s << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s] << "u));";
     }
     os << "\n";
-    if (npf > 0 && r + 1 == nr) {
-      os << "      if (tile + 1 < t1) { const char* gn = reinterpret_cast<const char*>(src + (((base | ~"
-         << outer << ") + 1) & " << outer << ") + off_d0);";
-      for (int s = 0; s < npf; ++s)
-        os << " n" << s << " = __ldcs(reinterpret_cast<const double2*>(gn + " << d0.off[s] << "ull));";
-      os << " }\n";
-    }
     const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
     for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
     if (last_direct) {
@@ -647,25 +565,7 @@ std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   os << "  }\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && t == 0) atomicOr(flag, 1);\n";
   os << "}\n";
-  std::string body = os.str();
-  const size_t ph = body.find("@@NTAB@@");
-  if (ph != std::string::npos) body.replace(ph, 8, std::to_string(kc.tab.size() / 2));
-  std::string head = kPrelude;
-  if (!kc.tab.empty() || ph != std::string::npos) {
-    head += "__constant__ double2 KT[" + std::to_string(std::max<size_t>(1, kc.tab.size() / 2)) + "] = {";
-    for (size_t i = 0; i < kc.tab.size(); i += 2)
-      head += (i ? ", {" : "{") + hexd(kc.tab[i]) + ", " + hexd(kc.tab[i + 1]) + "}";
-    if (kc.tab.empty()) head += "{0.0, 0.0}";
-    head += "};\n";
-  }
-  return head + body;
-}
-
-int count_table_entries(const MicroPass& mp, int R) {
-  int n = 0;
-  for (size_t w = 0; w < mp.size(); ++w)
-    if (mp.words[2 * w] & (M_STAB | M_CTAB)) n += 1 << R;
-  return n;
+  return kPrelude + os.str();
 }
 
 std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
@@ -673,8 +573,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
   const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks,
-                          sp.coalesce_bits, sp.stagger_ns, sp.tab_const, sp.pf_regs, sp.tab_smem,
-                          sp.tab_entries,
+                          sp.coalesce_bits,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
                           static_cast<int32_t>(mp.words.size()),
@@ -705,8 +604,7 @@ CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp) {
     throw std::runtime_error("loading a compiled pass failed");
   }
   e.k.threads = 1 << (sp.k - sp.R);
-  e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k) +
-             (sp.tab_smem && !sp.tab_const ? sizeof(double2) * sp.tab_entries : 0);
+  e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
   const void* fn = reinterpret_cast<const void*>(e.k.fn);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(e.k.smem)) != cudaSuccess ||

@@ -43,11 +43,6 @@ struct JitPassSpec {
   // first / last round read / write HBM directly when their register bits
   // leave physical bits [0, coalesce_bits) to the threads (0 = never)
   int coalesce_bits = 0;
-  int stagger_ns = 0;   // > 0: every second CTA of an SM starts this late
-  bool tab_const = false;  // table entries from a __constant__ array (else literals)
-  int pf_regs = 0;  // round-0 slots of the next tile loaded into registers during the last round
-  bool tab_smem = false;  // table entries from shared memory (copied once per CTA)
-  int tab_entries = 0;    // table entries of the pass (count_table_entries)
 };
 
 struct JitKernel {
@@ -56,9 +51,6 @@ struct JitKernel {
   size_t smem = 0;
   int occupancy = 0;  // resident CTAs per SM
 };
-
-// Diagonal-table entries of a lowered pass (2^R per table word).
-int count_table_entries(const MicroPass& mp, int R);
 
 // Tile geometry of a planned pass (buf_bits = log2 of the local buffer).
 JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool check);

@@ -99,10 +99,6 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_JIT_MINB")) jit_min_blocks_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_DIRECT_BITS")) direct_bits_ = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("QTB_JIT_STAGGER")) stagger_ns_ = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("QTB_JIT_TABCONST")) tab_const_ = std::atoi(e) != 0;
-  if (const char* e = std::getenv("QTB_JIT_PFREGS")) pf_regs_ = std::max(0, std::atoi(e));
-  if (const char* e = std::getenv("QTB_JIT_TABSMEM")) tab_smem_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_PIPE")) pipe_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_PIPE_MAXFP")) pipe_max_fp64_ = std::atof(e);
   if (const char* e = std::getenv("QTB_PF")) {
@@ -416,11 +412,6 @@ State::Prepared State::prepare(const Plan& plan) {
                 (pipe_max_fp64_ <= 0.0 || micro_fp64_per_amp(micro[pi], sp.R) <= pipe_max_fp64_);
       sp.min_blocks = jit_min_blocks_;
       sp.coalesce_bits = direct_bits_;
-      sp.stagger_ns = stagger_ns_;
-      sp.tab_const = tab_const_;
-      sp.pf_regs = pf_regs_;
-      sp.tab_smem = tab_smem_;
-      sp.tab_entries = count_table_entries(micro[pi], sp.R);
       if (pf_ && !sp.pipe) {
         int run = 0;
         while (run < sp.k - sp.R && ps.tile_phys[run] == run) ++run;

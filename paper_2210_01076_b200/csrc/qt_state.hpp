@@ -161,10 +161,6 @@ class State {
   // compiled passes: first / last round straight from / to HBM when physical
   // bits [0, direct_bits_) stay thread bits (128-B runs); 0 = always stage
   int direct_bits_ = kJitDirectBits;
-  int stagger_ns_ = 0;  // compiled passes: start delay of every 2nd CTA per SM
-  bool tab_const_ = false;  // compiled passes: table entries from __constant__
-  int pf_regs_ = 0;  // compiled passes: next-tile round-0 slots prefetched into registers
-  bool tab_smem_ = false;  // compiled passes: table entries from shared memory
   int occupancy_ = 1, sms_ = 148;
   bool timing_ = false;
   std::vector<PassTiming> timings_;
