@@ -229,11 +229,12 @@ void Sim::update_state() {
   // segment length: the chain has nbuf_ buffers for N gates
   uint64_t seg = cfg_.segment_gates > 0 ? static_cast<uint64_t>(cfg_.segment_gates) : 0;
   if (seg == 0) {
-    // >= 256 gates per segment: shorter segments break pass fusion more than
-    // they save in restart distance (C5: 139 -> 300 gates per segment cut
-    // the uniform-position update from 191 to 140 ms)
+    // >= 256 gates per segment from 20 qubits up: shorter segments break pass
+    // fusion more than they save in restart distance (C5: 139 -> 300 gates
+    // per segment cut the uniform-position update from 191 to 140 ms)
     seg = (N + static_cast<uint64_t>(nbuf_) - 1) / static_cast<uint64_t>(nbuf_);
-    seg = std::max<uint64_t>(seg, kMinSegmentGates);
+    // small states are launch-bound: fine checkpoints (short restarts) win there
+    seg = std::max<uint64_t>(seg, n_ >= kHybridMinQubits ? kMinSegmentGates : 64);
   }
 
   std::vector<char> used(nbuf_, 0);
