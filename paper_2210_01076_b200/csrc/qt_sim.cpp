@@ -33,6 +33,7 @@
 namespace qtb {
 
 constexpr uint64_t kMinSegmentGates = 256;
+constexpr size_t kSegmentPlanCache = 512;  // cached segment plans (cleared when full)
 
 Sim::Sim(int nqubits, const qt_config* cfg) : n_(nqubits) {
   if (nqubits < 1 || nqubits > 40)
@@ -274,22 +275,35 @@ void Sim::update_state() {
         in_place = true;
         if (chain_.size() <= chain_keep) clobbered = true;
       }
-      std::vector<LOp> ops;
-      ops.reserve(static_cast<size_t>(b - a));
-      for (uint64_t i = a; i < b; ++i) {
-        const int rc = lower_gate(gates[i], n_, static_cast<uint32_t>(i), ops, &err);
-        if (rc != QT_OK) fail(rc, err);
-      }
-      fuse_ops(ops, n_);
       const Ckpt src = chain_.back();
+      // a segment's gates (by identity) from the same qubit map plan the
+      // same way: the plan and its lowering are cached across updates
+      std::string key(reinterpret_cast<const char*>(ids.data() + a), (b - a) * sizeof(uint32_t));
+      key.append(reinterpret_cast<const char*>(src.perm.data()), src.perm.size() * sizeof(int));
+      std::shared_ptr<State::PreparedPlan> pp;
+      auto hit = seg_plans_.find(key);
+      if (hit != seg_plans_.end()) {
+        pp = hit->second;
+      } else {
+        std::vector<LOp> ops;
+        ops.reserve(static_cast<size_t>(b - a));
+        for (uint64_t i = a; i < b; ++i) {
+          const int rc = lower_gate(gates[i], n_, static_cast<uint32_t>(i), ops, &err);
+          if (rc != QT_OK) fail(rc, err);
+        }
+        fuse_ops(ops, n_);
+        pp = st_->prepare_ops(ops, &src.perm);
+        if (seg_plans_.size() >= kSegmentPlanCache) seg_plans_.clear();
+        seg_plans_.emplace(std::move(key), pp);
+      }
       if (in_place) {
         st_->bind(dst, src.perm);
-        st_->apply_ops(ops, b - a);
+        st_->apply_prepared(*pp, b - a);
         chain_.back().pos = b;
         chain_.back().perm = st_->perm();
       } else {
         st_->bind(dst, src.perm);
-        st_->apply_ops(ops, b - a, st_->buffer(src.buf), &src.perm);
+        st_->apply_prepared(*pp, b - a, st_->buffer(src.buf), &src.perm);
         chain_.push_back(Ckpt{b, dst, st_->perm()});
       }
       if (trace_) {

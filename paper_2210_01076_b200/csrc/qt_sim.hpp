@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <string>
 #include <unordered_map>
 #include <vector>
 
@@ -69,6 +70,9 @@ class Sim {
   std::unique_ptr<State> st_;
   std::vector<Ckpt> chain_;  // valid checkpoints, increasing pos
   std::vector<uint32_t> bound_ids_;  // first gate of each segment of the last run (pos > 0)
+  // plans of segments by (gate ids, input qubit map): segments re-simulated
+  // unchanged after an edit skip planning
+  std::unordered_map<std::string, std::shared_ptr<State::PreparedPlan>> seg_plans_;
   int nbuf_ = 1;
   qt_run_stats last_{};
   bool trace_ = false;  // QTB_SIM_TRACE=1: per-segment timing / cache lines on stderr

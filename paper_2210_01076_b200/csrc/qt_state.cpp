@@ -299,6 +299,35 @@ void State::bind(int i, const std::vector<int>& perm) {
   perm_ = perm;
 }
 
+std::shared_ptr<State::PreparedPlan> State::prepare_ops(const std::vector<LOp>& ops,
+                                                        const std::vector<int>* perm) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  auto pp = std::make_shared<PreparedPlan>();
+  const auto t0 = std::chrono::steady_clock::now();
+  pp->plan = make_plan(ops, n_, nlocal_, perm ? *perm : perm_, opt_);
+  pp->prep = prepare(pp->plan);
+  pp->plan_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return pp;
+}
+
+void State::apply_prepared(const PreparedPlan& pp, uint64_t ngates, const double2* src,
+                           const std::vector<int>* src_perm) {
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  if (src == psi_) src = nullptr;
+  if (src && src_perm) perm_ = *src_perm;
+  stats = qt_run_stats{};
+  stats.gates = ngates;
+  stats.plan_ms = pp.plan_ms;
+  if (jit_mode_ == 2) {
+    // hybrid: passes compiled since the plan was prepared are picked up
+    const Prepared fresh = prepare(pp.plan);
+    launch_prepared(pp.plan, fresh, src);
+  } else {
+    launch_prepared(pp.plan, pp.prep, src);
+  }
+  perm_ = pp.plan.perm_after;
+}
+
 void State::apply_ops(const std::vector<LOp>& ops, uint64_t ngates,
                       const double2* src, const std::vector<int>* src_perm) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");

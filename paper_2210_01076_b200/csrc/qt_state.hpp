@@ -99,6 +99,16 @@ class State {
 
   Plan plan(const std::vector<LOp>& ops) const;
   const PlanOptions& options() const { return opt_; }
+
+  // A plan with its host-side preparation (lowering, compiled passes), for
+  // callers that re-run the same ops (the incremental engine's segments).
+  struct PreparedPlan;
+  // Plans `ops` from qubit map `perm` (nullptr: the current one).
+  std::shared_ptr<PreparedPlan> prepare_ops(const std::vector<LOp>& ops,
+                                            const std::vector<int>* perm);
+  // apply_ops with the planning already done.
+  void apply_prepared(const PreparedPlan& pp, uint64_t ngates, const double2* src = nullptr,
+                      const std::vector<int>* src_perm = nullptr);
   void set_timing(bool on) { timing_ = on; }
   // Device ms of every launch of the last apply (timing enabled).
   std::vector<std::pair<int, float>> last_timings(bool consume = true);
@@ -112,6 +122,15 @@ class State {
     std::vector<JitKernel> jk;
   };
   Prepared prepare(const Plan& plan);
+
+ public:
+  struct PreparedPlan {
+    Plan plan;
+    Prepared prep;
+    double plan_ms = 0.0;
+  };
+
+ private:
   void launch_prepared(const Plan& plan, const Prepared& pr, const double2* src);
   void upload_and_launch(const Plan& plan, const double2* src);
   // apply(): the previous call's plan, reused when the same gate list is
