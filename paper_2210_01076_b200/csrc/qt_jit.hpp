@@ -5,13 +5,14 @@
 // circuit that is simulated more than once can instead be compiled: each
 // lowered pass becomes one straight-line sm_100a kernel (NVRTC, loaded with
 // cudaLibraryLoadData) whose register rounds, slot addresses and FP64
-// constants are literals -- the DFMAs read their constants straight from the
-// constant bank and no dispatch instruction is left in the hot loop. Compiled
-// passes are cached process-wide by their generated source, so re-running a
-// circuit (or the same pass in another circuit) skips compilation.
+// constants are literals (hex-float immediates) and no dispatch instruction
+// is left in the hot loop. Compiled passes are cached process-wide by an
+// exact binary key of the pass (jit_key: layer words, pool, tile geometry),
+// so re-running a circuit (or the same pass in another circuit) skips
+// compilation; hybrid mode compiles misses on background threads.
 //
 // NVRTC is loaded at run time (dlopen libnvrtc.so.12); without it compiled
-// mode reports an error and the interpreter kernel runs instead.
+// mode (1) fails at state creation and hybrid mode (2) is the interpreter.
 #pragma once
 
 #include <cuda_runtime.h>

@@ -17,7 +17,9 @@ class StateVector:
     GPU, exchanges by device copies) or "sharded" (one rank of a
     ``world``-GPU state, NCCL exchanges; pass ``rank``, ``world``, ``nccl_id``).
     compiled=True runs every tile pass as its own NVRTC-compiled straight-line
-    kernel (cached by source: for circuits applied more than once).
+    kernel (cached process-wide by the pass's content: for circuits applied more
+    than once); compiled=2: hybrid (cached passes compiled, the others on the
+    interpreter while they compile in the background).
     """
 
     def __init__(self, num_qubits: int, mode: str = "single", shards: int = 1,
