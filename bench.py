@@ -395,8 +395,8 @@ def main():
                      "kernel": ("qtjit: compiled tile passes (qt_jit.cpp)" if compiled
                                 else "tile_pass_kernel (qt_tilepass.cu)"), "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms,
-                     "note": "the C3 passes are FP64-bound, not HBM-bound (2398 FP64 ops per "
-                             "amplitude over 20 passes): see roofline_fp64 and DESIGN.md section 4"},
+                     "note": "the C3 passes are FP64-bound, not HBM-bound (2338 FP64 ops per "
+                             "amplitude over 22 passes): see roofline_fp64 and DESIGN.md section 4"},
         "roofline_fp64": {"achieved_dfma_per_s": fp64_achieved, "peak_dfma_per_s": fp64_peak,
                           "frac": fp64_achieved / fp64_peak if fp64_peak else None,
                           "note": "DFMA-pipe instructions of the lowered ops (complex 2x2 = 8/amp, "

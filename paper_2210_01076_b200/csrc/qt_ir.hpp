@@ -152,11 +152,14 @@ constexpr int kMaxRegBits = 4;
 // C3 on B200 (the pass is latency-bound, so resident warps win over R = 4).
 constexpr int kDefaultTileBits = 10;
 constexpr int kDefaultRegBits = 3;
-// compiled passes (qt_jit.cpp): R = 4, 2^12-amplitude tiles whose lowest 3
-// physical bits are always in the tile (128-B runs) -- measured best on C3
+// compiled passes (qt_jit.cpp): R = 4, 2^12-amplitude tiles whose lowest 4
+// physical bits are always in the tile (256-B runs) -- measured best on C3
+// (221 ms vs 226 ms with 128-B runs); hybrid mode (the incremental engine)
+// keeps 128-B runs (tuned on C5)
 constexpr int kJitTileBits = 12;
 constexpr int kJitRegBits = 4;
-constexpr int kJitLowBits = 3;
+constexpr int kJitLowBits = 4;
+constexpr int kHybridLowBits = 3;
 constexpr int kJitDirectBits = 3;
 // hybrid compiled passes (incremental engine) from this many local qubits up
 constexpr int kHybridMinQubits = 20;

@@ -84,7 +84,7 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   // tiles / 128-B runs; interpreter R = 3 / 2^10 tiles / 256-B runs
   opt_.reg_bits = jit_mode_ == 1 ? kJitRegBits : kDefaultRegBits;
   opt_.tile_bits = jit_mode_ ? kJitTileBits : kDefaultTileBits;
-  if (jit_mode_) opt_.low_bits = kJitLowBits;
+  if (jit_mode_) opt_.low_bits = jit_mode_ == 1 ? kJitLowBits : kHybridLowBits;
   if (cfg && cfg->tile_qubits > 0)
     opt_.tile_bits = std::min(cfg->tile_qubits, kMaxTileBits);
   // tuning overrides (benchmark sweeps only)
