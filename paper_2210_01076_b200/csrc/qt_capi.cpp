@@ -616,6 +616,7 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
       qtb::JitPassSpec sp = qtb::make_jit_spec(p.passes[i], opt.reg_bits, num_qubits, i == last_tile);
       // the state's tuning overrides (QTB_PIPE / QTB_JIT_MINB), as qt_state.cpp applies them
       if (const char* e = std::getenv("QTB_PIPE")) sp.pipe = std::atoi(e) != 0 && 2 * (16u << sp.k) <= 200u * 1024u;
+      if (sp.pipe) sp.ring = false;
       if (const char* e = std::getenv("QTB_JIT_MINB")) sp.min_blocks = std::atoi(e);
       sp.coalesce_bits = qtb::kJitDirectBits;
       if (const char* e = std::getenv("QTB_DIRECT_BITS")) sp.coalesce_bits = std::atoi(e);

@@ -80,7 +80,8 @@ enum DType : uint32_t {
 // Pool data of a layer, in order: [nv tile-uniform sign terms (global-bit
 // condition, slot mask: 2 words each)][diagonal table of 2^R entries]
 // [sign terms (2 words each)]
-// [(a, b) per rotation slot][8 doubles per 2x2 slot].
+// [scaled rotation (t, 0) or (u, 1) per rotation slot: qt_micro.cpp
+// push_rotation][8 doubles per 2x2 slot].
 // Tile-uniform sign terms (condition on global bits only) negate the
 // table's output slots with one uniform test per term instead of flipping signs
 // per amplitude.

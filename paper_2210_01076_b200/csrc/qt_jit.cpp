@@ -63,6 +63,19 @@ FI void shear(double2& x, double2& y, double a, double b) {
   y.x = fma(b, x.x, y.x); y.y = fma(b, x.y, y.y);
   x.x = fma(a, y.x, x.x); x.y = fma(a, y.y, x.y);
 }
+// scaled rotations (qt_micro.cpp push_rotation): c [[1, -t], [t, 1]] and
+// s [[u, -1], [1, u]], two FMAs per real pair (same operations as the
+// interpreter's pair_srot)
+FI void trot(double2& x, double2& y, double k) {
+  const double2 a = x, b = y;
+  x.x = fma(-k, b.x, a.x); x.y = fma(-k, b.y, a.y);
+  y.x = fma(k, a.x, b.x); y.y = fma(k, a.y, b.y);
+}
+FI void urot(double2& x, double2& y, double k) {
+  const double2 a = x, b = y;
+  x.x = fma(k, a.x, -b.x); x.y = fma(k, a.y, -b.y);
+  y.x = fma(k, b.x, a.x); y.y = fma(k, b.y, a.y);
+}
 // e^{i phi} on one amplitude as shears of (re, im)
 FI void pshear(double2& v, double a, double b) {
   v.x = fma(a, v.y, v.x); v.y = fma(b, v.x, v.y); v.x = fma(a, v.y, v.x);
@@ -90,12 +103,24 @@ FI void flip2(double2& v, u32 sg) { v.x = flipd(v.x, sg); v.y = flipd(v.y, sg); 
 FI void neg2(double2& v) { flip2(v, 0x80000000u); }
 )PRE";
 
+// Exact hexadecimal-float literal of d, formatted from its bits (not with
+// printf's %a, whose radix character follows the process locale).
 std::string hexd(double d) {
+  uint64_t w;
+  std::memcpy(&w, &d, 8);
+  const bool neg = (w >> 63) != 0;
+  const int e = static_cast<int>((w >> 52) & 0x7ffu);
+  const uint64_t m = w & ((1ull << 52) - 1);
+  if (e == 0x7ff) throw std::runtime_error("non-finite literal");
   char b[48];
-  std::snprintf(b, sizeof(b), "%a", d);
-  std::string s(b);
-  if (s == "inf" || s == "-inf" || s == "nan" || s == "-nan") throw std::runtime_error("non-finite literal");
-  return s;
+  if (e == 0 && m == 0) {
+    std::snprintf(b, sizeof(b), "%s0x0p+0", neg ? "-" : "");
+  } else {
+    const int ex = e == 0 ? -1022 : e - 1023;
+    std::snprintf(b, sizeof(b), "%s0x%d.%013llxp%+d", neg ? "-" : "", e == 0 ? 0 : 1,
+                  static_cast<unsigned long long>(m), ex);
+  }
+  return b;
 }
 
 std::string hexu(uint64_t x) {
@@ -237,12 +262,12 @@ void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y
   const uint32_t rmask = (x >> M_ROT_SHIFT) & 15u, dmask = (x >> M_DENSE_SHIFT) & 15u;
   for (int a = 0; a < R; ++a) {
     if (!(rmask & (1u << a))) continue;
-    const double ca = P[off], cb = P[off + 1];
+    const double ck = P[off], form = P[off + 1];
     off += 2;
     os << " ";
     for (int s = 0; s < NS; ++s) {
       if (s & (1 << a)) continue;
-      os << " shear(v" << s << ", v" << (s | (1 << a)) << ", " << kc(ca) << ", " << kc(cb) << ");";
+      os << (form != 0.0 ? " urot(v" : " trot(v") << s << ", v" << (s | (1 << a)) << ", " << kc(ck) << ");";
     }
     os << "\n";
   }
@@ -370,6 +395,14 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     sp.slot_sb[s] = swz_host(s << (k - R)) << 4;
   }
   sp.tile_phys = ps.tile_phys;
+  // the ring kernel (jit_source_ring): 3 tile buffers must fit one CTA's
+  // shared memory and 2 groups one CTA (QTB_JIT_RING=0: the direct kernel)
+  static const bool ring_env = [] {
+    const char* e = std::getenv("QTB_JIT_RING");
+    return !e || std::atoi(e) != 0;
+  }();
+  sp.ring = ring_env && 3 * (sizeof(double2) << k) + 64 <= 227 * 1024 && (2 << (k - R)) <= 1024 &&
+            (1 << (k - R)) >= 32 && buf_bits - k >= 1;
   sp.rounds.resize(ps.rounds.size());
   for (size_t r = 0; r < ps.rounds.size(); ++r) {
     const PlanRound& pr = ps.rounds[r];
@@ -426,8 +459,127 @@ Direct direct_round(const JitPassSpec& sp, const DRound& rd) {
 
 }  // namespace
 
+// Ring variant (the default for compiled passes): a persistent CTA per SM
+// with TWO consumer groups of 2^(k-R) threads, each group running the
+// register rounds of its own tile, and a ring of three tile buffers in shared
+// memory. When a group has finished reading its tile's buffer it streams the
+// tile three ahead into that buffer (cp.async 16-B copies, swizzled like every
+// round's accesses) and arms the buffer's mbarrier with
+// cp.async.mbarrier.arrive; the other group waits on that barrier. So the HBM
+// reads of a tile are in flight while both groups compute: no round-0 load
+// stalls the FP64 rounds. The last round stores straight to HBM when its
+// register bits leave the coalescing bits to the threads.
+//   tile j (of the CTA's range) -> group j & 1, buffer j % 3, mbarrier j % 6
+//   with phase parity (j / 6) & 1. Six barriers, not three: tiles j and j + 3
+// share a buffer but belong to different groups, and the group waiting for
+// j + 3 may get there while the load of tile j is still in flight -- with one
+// barrier per buffer its parity test would then see tile j's pending phase as
+// the "preceding" phase of j + 3's and pass. Barrier j % 6 was last used by
+// tile j - 6 of the same group, which that group has consumed.
+std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp) {
+  const int R = sp.R, NS = 1 << R, k = sp.k;
+  const int T = 1 << (k - R);
+  const size_t nr = sp.rounds.size();
+  const uint32_t TB = 16u << k;
+  std::ostringstream os;
+  Consts kc;
+  const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
+  const std::string outer = hexu(sp.outer_mask);
+  os << "FI void mbar_wait(u32 a, u32 ph) {\n"
+     << "  asm volatile(\"{\\n .reg .pred p;\\n W:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n"
+        " @!p bra W;\\n }\" :: \"r\"(a), \"r\"(ph) : \"memory\");\n}\n"
+     << "FI void gbar(u32 id) { asm volatile(\"bar.sync %0, " << T << ";\" :: \"r\"(id) : \"memory\"); }\n"
+     << "extern \"C\" __global__ void __launch_bounds__(" << 2 * T << ", 1)\n"
+     << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per) {\n"
+     << "  extern __shared__ __align__(16) double2 sm[];\n"
+     << "  char* const sm0 = reinterpret_cast<char*>(sm);\n"
+     << "  const u32 smbase = static_cast<u32>(__cvta_generic_to_shared(sm0));\n"
+     << "  const u32 fb = smbase + " << 3 * TB << "u;  // 6 mbarriers (8 B each)\n"
+     << "  const u32 grp = threadIdx.x >> " << (k - R) << ";\n"
+     << "  const u32 t = threadIdx.x & " << (T - 1) << "u;\n"
+     << "  const u64 off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
+     << "  const u32 st4 = swz(t) << 4;\n";
+  if (dl.ok) os << "  const u64 off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
+  os << "  const u64 t0 = u64(blockIdx.x) * per;\n"
+     << "  const u64 t1 = t0 + per < " << hexu(sp.ntiles) << " ? t0 + per : " << hexu(sp.ntiles) << ";\n"
+     << "  const u64 cnt = t1 > t0 ? t1 - t0 : 0;\n"
+     << "  if (threadIdx.x == 0) {\n"
+     << "    for (u32 b = 0; b < 6; ++b)\n"
+     << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], %1;\" :: \"r\"(fb + 8 * b), \"r\"(" << T
+     << ") : \"memory\");\n"
+     << "  }\n"
+     << "  __syncthreads();\n"
+     << "  auto load = [&](u64 i) {\n"
+     << "    const char* s = reinterpret_cast<const char*>(src + pdep64(t0 + i, " << outer << ") + off_t);\n"
+     << "    const u32 b = static_cast<u32>(i % 3);\n"
+     << "    const u32 d = smbase + b * " << TB << "u;\n";
+  for (int s2 = 0; s2 < NS; ++s2)
+    os << "    asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(d + (st4 ^ " << sp.slot_sb[s2]
+       << "u)), \"l\"(s + " << sp.slot_gb[s2] << "ull) : \"memory\");\n";
+  os << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(fb + 8 * static_cast<u32>(i % 6)) : \"memory\");\n"
+     << "  };\n"
+     << "  if (grp == 0) { if (cnt > 0) load(0); if (cnt > 2) load(2); }\n"
+     << "  else if (cnt > 1) load(1);\n"
+     << "  bool bad = false;\n"
+     << "  for (u64 j = grp; j < cnt; j += 2) {\n"
+     << "    const u32 bi = static_cast<u32>(j % 3);\n"
+     << "    char* const smb = sm0 + bi * " << TB << "u;\n"
+     << "    mbar_wait(fb + 8 * static_cast<u32>(j % 6), static_cast<u32>((j / 6) & 1));\n"
+     << "    const u64 base = pdep64(t0 + j, " << outer << ");\n"
+     << "    const u64 g = gbase_hi | base;\n";
+  for (size_t r = 0; r < nr; ++r) {
+    const DRound& rd = sp.rounds[r];
+    const bool last_direct = r + 1 == nr && dl.ok;
+    os << "    { // round " << r << "\n      u32 jb = t;";
+    for (int i = 0; i < R; ++i) os << " jb = insert_zero(jb, " << int(rd.sreg[i]) << "u);";
+    os << "\n      const u32 a = swz(jb) << 4;\n     ";
+    std::vector<uint32_t> sb(NS, 0);
+    for (int s2 = 0; s2 < NS; ++s2)
+      for (int i = 0; i < R; ++i)
+        if (s2 & (1 << i)) sb[s2] ^= rd.sbit[i];
+    for (int s2 = 0; s2 < NS; ++s2)
+      os << " double2 v" << s2 << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s2] << "u));";
+    os << "\n";
+    const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
+    for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
+    if (last_direct) {
+      // the group's buffer is free once every thread has read it
+      os << "      gbar(1 + grp);\n"
+         << "      if (j + 3 < cnt) load(j + 3);\n"
+         << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
+      for (int s2 = 0; s2 < NS; ++s2) {
+        if (sp.check) os << " bad = bad || !finite2(v" << s2 << ");";
+        os << " __stcs(reinterpret_cast<double2*>(gd + " << dl.off[s2] << "ull), v" << s2 << ");";
+      }
+      os << " }\n    }\n";
+    } else {
+      os << "     ";
+      for (int s2 = 0; s2 < NS; ++s2)
+        os << " *reinterpret_cast<double2*>(smb + (a ^ " << sb[s2] << "u)) = v" << s2 << ";";
+      os << "\n      gbar(1 + grp);\n    }\n";
+    }
+  }
+  if (!dl.ok) {
+    os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
+    for (int s2 = 0; s2 < NS; ++s2) {
+      os << "      { const double2 x = *reinterpret_cast<const double2*>(smb + (st4 ^ " << sp.slot_sb[s2]
+         << "u));";
+      if (sp.check) os << " bad = bad || !finite2(x);";
+      os << " __stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s2] << "ull), x); }\n";
+    }
+    os << "    }\n"
+       << "    gbar(1 + grp);\n"
+       << "    if (j + 3 < cnt) load(j + 3);\n";
+  }
+  os << "  }\n";
+  if (sp.check) os << "  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);\n";
+  os << "}\n";
+  return kPrelude + os.str();
+}
+
 std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
   const int R = sp.R, NS = 1 << R, k = sp.k;
+  if (sp.ring) return jit_source_ring(sp, mp);
   const int threads = 1 << (k - R);
   const size_t nr = sp.rounds.size();
   std::ostringstream os;
@@ -572,7 +724,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   // every input of jit_source, as bytes (exact: no hash collisions)
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
-  const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks,
+  const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring,
                           sp.coalesce_bits,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
@@ -603,8 +755,8 @@ CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp) {
     cudaGetLastError();
     throw std::runtime_error("loading a compiled pass failed");
   }
-  e.k.threads = 1 << (sp.k - sp.R);
-  e.k.smem = (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
+  e.k.threads = (sp.ring ? 2 : 1) << (sp.k - sp.R);
+  e.k.smem = sp.ring ? 3 * (sizeof(double2) << sp.k) + 64 : (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
   const void* fn = reinterpret_cast<const void*>(e.k.fn);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(e.k.smem)) != cudaSuccess ||

@@ -38,6 +38,7 @@ struct JitPassSpec {
   bool check = false;
   bool pipe = false;    // double-buffered tiles: the next tile streams in (cp.async) during the rounds
   int pf_bits = 0;      // > 0: L2 prefetch of the next tile in runs of 2^pf_bits amplitudes
+  bool ring = false;    // persistent CTA, two consumer groups, 3-buffer cp.async + mbarrier ring (jit_source_ring)
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
   std::vector<DRound> rounds;  // reg / sreg / sbit per round
   std::vector<int> tile_phys;  // physical bit of each tile bit (ascending)

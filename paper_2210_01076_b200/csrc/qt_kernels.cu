@@ -171,7 +171,9 @@ __global__ void topk_hist_kernel(const double2* __restrict__ psi, uint64_t count
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
     const uint64_t k = norm_key(__ldcs(psi + i));
-    if ((k & pmask) == prefix) atomicAdd(&h[(k >> shift) & (kTopkBins - 1)], 1u);
+    // the digit below the chosen prefix (pmask covers every higher bit; the
+    // last digit can be narrower than kTopkBits)
+    if ((k & pmask) == prefix) atomicAdd(&h[((k & ~pmask) >> shift) & (kTopkBins - 1)], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kTopkBins; i += blockDim.x)

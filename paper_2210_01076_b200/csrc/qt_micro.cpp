@@ -13,6 +13,9 @@ constexpr double kPi = 3.14159265358979323846;
 // largest shear factor |tan(phi/2)| accepted for a table entry (|phi| <=
 // ~0.94 pi); beyond it the table stays complex multiplies
 constexpr double kMaxShear = 12.0;
+// carried-scalar magnitude below which the stored state is renormalised
+// (the state then holds amplitudes up to 2^300: far from FP64 overflow)
+constexpr double kRescaleBelow = 0x1p-300;
 
 bool is_layer_lean(const DOp& d) {
   const uint32_t type = (d.hdr & kOpVariantMask) >> 10;
@@ -68,6 +71,25 @@ void push_shear(std::vector<double>& pool, const cplx& t) {
   const double phi = std::atan2(t.im, t.re);
   pool.push_back(-std::tan(0.5 * phi));
   pool.push_back(std::sin(phi));
+}
+
+// A rotation [[c, -s], [s, c]] (the round compiler's (c, s), c >= 0),
+// lowered to two FMAs per real pair instead of three shears:
+//   c >= |s|: c [[1, -t], [t, 1]], t = s / c:  x' = x - t y,  y' = y + t x
+//   else:     s [[u, -1], [1, u]], u = c / s:  x' = u x - y,  y' = x + u y
+// (|t|, |u| <= 1: each output is one FMA of a perfectly conditioned step).
+// The scale factor is uniform over the state, so it is carried like the
+// table phases and folded into the plan's last table. Pool: (t, 0) or (u, 1).
+void push_rotation(std::vector<double>& pool, double c, double s, cplx& carried) {
+  if (c >= std::fabs(s)) {
+    pool.push_back(s / c);
+    pool.push_back(0.0);
+    carried = cplx{carried.re * c, carried.im * c};
+  } else {
+    pool.push_back(c / s);
+    pool.push_back(1.0);
+    carried = cplx{carried.re * s, carried.im * s};
+  }
 }
 
 void pad_even(std::vector<double>& pool) {
@@ -232,8 +254,10 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
         const uint32_t rmask = (d.hdr >> 6) & 15u;
         for (int a = 0; a < R; ++a) {
           if (!(rmask & (1u << a))) continue;
-          P.push_back(src[o]);
-          P.push_back(src[o + 1]);
+          // the round compiler's rotation (c, s), |theta| <= pi/2, becomes a
+          // scaled rotation of two FMAs per real pair; its scale (c or s)
+          // joins the carried scalar (see push_rotation)
+          push_rotation(P, src[o], src[o + 1], pass_carried);
           o += 2;
         }
         for (int a = 0; a < R; ++a) {
@@ -248,6 +272,22 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
         }
         mp.words.push_back(x);
         mp.words.push_back(y);
+        // the scaled rotations grow the stored state by up to sqrt(2) each:
+        // long before it could overflow, an exact power-of-two scale word
+        // (a complex table of 2^-m) renormalises it
+        const double mag = std::hypot(pass_carried.re, pass_carried.im);
+        if (mag > 0.0 && mag < kRescaleBelow) {
+          const double f = std::ldexp(1.0, std::ilogb(mag));
+          pad_even(P);
+          const uint32_t so = static_cast<uint32_t>(P.size());
+          for (int s = 0; s < NS; ++s) {
+            P.push_back(f);
+            P.push_back(0.0);
+          }
+          pass_carried = cplx{pass_carried.re / f, pass_carried.im / f};
+          mp.words.push_back(so | M_CTAB);
+          mp.words.push_back(0);
+        }
       }
       if (!ok) break;
       if (mp.size() == mp.round_first.back()) {  // an empty round: one no-op word
@@ -324,7 +364,7 @@ double micro_fp64_per_amp(const MicroPass& mp, int R) {
       }
       fp += ((x & M_STAB) ? 3.0 : 4.0) * live / NS;
     }
-    fp += 3.0 * __builtin_popcount((x >> M_ROT_SHIFT) & 15u) +
+    fp += 2.0 * __builtin_popcount((x >> M_ROT_SHIFT) & 15u) +
           8.0 * __builtin_popcount((x >> M_DENSE_SHIFT) & 15u);
   }
   return fp;

@@ -48,7 +48,7 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
 
 // FP64-pipe instructions per amplitude of a lowered pass (roofline
 // accounting): shear table 3 per non-identity entry / 2^R, complex table 4,
-// rotation 3, complex 2x2 8 (per amplitude of the slot pairs).
+// rotation 2 (scaled form), complex 2x2 8 (per amplitude of the slot pairs).
 double micro_fp64_per_amp(const MicroPass& mp, int reg_bits);
 
 }  // namespace qtb

@@ -478,13 +478,12 @@ void emit_layer(LayerState& L, EncRound& out) {
   }
   for (int i = 0; i < L.R; ++i) {
     if (!(L.mmask & (1u << i))) continue;
-    // rotation [[c, -s], [s, c]] (c >= 0, to_rotations) as three in-place
-    // shears (kernel pair_shear): x += a y; y += b x; x += a y with
-    // a = -tan(theta/2) = -s / (1 + c) in [-1, 1] and b = sin(theta) = s
+    // rotation [[c, -s], [s, c]] (c >= 0, to_rotations) as (c, s): the
+    // generic kernel applies it as three in-place shears (pair_shear), the
+    // lean layer words as a scaled two-FMA rotation (qt_micro.cpp)
     if (rmask & (1u << i)) {
-      const double c = L.M[i][0].re, sn = L.M[i][2].re;
-      out.pool.push_back(-sn / (1.0 + c));
-      out.pool.push_back(sn);
+      out.pool.push_back(L.M[i][0].re);
+      out.pool.push_back(L.M[i][2].re);
     }
   }
   for (int i = 0; i < L.R; ++i)

@@ -439,6 +439,7 @@ State::Prepared State::prepare(const Plan& plan) {
       sp = make_jit_spec(ps, opt_.reg_bits, buf_bits_, pi == last_tile);
       sp.pipe = pipe_ && (2 * (sizeof(double2) << sp.k)) <= 200 * 1024 &&
                 (pipe_max_fp64_ <= 0.0 || micro_fp64_per_amp(micro[pi], sp.R) <= pipe_max_fp64_);
+      if (sp.pipe) sp.ring = false;
       sp.min_blocks = jit_min_blocks_;
       sp.coalesce_bits = direct_bits_;
       if (pf_ && !sp.pipe) {

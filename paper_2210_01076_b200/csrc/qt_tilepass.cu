@@ -270,8 +270,10 @@ __device__ __forceinline__ void layer_rot(double2 (&v)[1 << R], const P& p, uint
                                           int& o) {
   if constexpr (A < R) {
     if (mask & (1u << A)) {
-      // rotation as three in-place shears (a, b): see pair_shear
-      pair_shear<R, A>(v, p.pool[o], p.pool[o + 1]);
+      // rotation (c, s) as three in-place shears a = -s / (1 + c), b = s
+      // (pair_shear; the division is correctly rounded, as on the host)
+      const double c = p.pool[o], sn = p.pool[o + 1];
+      pair_shear<R, A>(v, -sn / (1.0 + c), sn);
       o += 2;
     }
     layer_rot<R, A + 1>(v, p, mask, o);
@@ -426,12 +428,43 @@ __device__ __forceinline__ void m_ctab(double2 (&v)[1 << R], const double2* t) {
   }
 }
 
+// Scaled rotation of the lean layer words (qt_micro.cpp push_rotation): two
+// FMAs per real pair, the scale carried by the plan.
+//   (t, 0):  x' = x - t y,  y' = y + t x        (c [[1, -t], [t, 1]])
+//   (u, 1):  x' = u x - y,  y' = x + u y        (s [[u, -1], [1, u]])
+template <int R, int A>
+__device__ __forceinline__ void pair_srot(double2 (&v)[1 << R], double k, bool uform) {
+  if (uform) {
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+      if (s & (1 << A)) continue;
+      const int s1 = s | (1 << A);
+      const double2 x = v[s], y = v[s1];
+      v[s].x = fma(k, x.x, -y.x);
+      v[s].y = fma(k, x.y, -y.y);
+      v[s1].x = fma(k, y.x, x.x);
+      v[s1].y = fma(k, y.y, x.y);
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < (1 << R); ++s) {
+      if (s & (1 << A)) continue;
+      const int s1 = s | (1 << A);
+      const double2 x = v[s], y = v[s1];
+      v[s].x = fma(-k, y.x, x.x);
+      v[s].y = fma(-k, y.y, x.y);
+      v[s1].x = fma(k, x.x, y.x);
+      v[s1].y = fma(k, x.y, y.y);
+    }
+  }
+}
+
 template <int R, int A>
 __device__ __forceinline__ void m_rots(double2 (&v)[1 << R], const double2*& q, uint32_t x) {
   if constexpr (A < R) {
     if (x & (1u << (M_ROT_SHIFT + A))) {
       const double2 ab = *q++;
-      pair_shear<R, A>(v, ab.x, ab.y);
+      pair_srot<R, A>(v, ab.x, ab.y != 0.0);
     }
     m_rots<R, A + 1>(v, q, x);
   }

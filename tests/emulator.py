@@ -76,16 +76,14 @@ def apply_plan(state: np.ndarray, plan_json: str, base: int = 0, exchange=None) 
                         tab = np.array(op[10][0::2]) + 1j * np.array(op[10][1::2])
                         psi = psi * tab[slot]
                     psi = _signs(psi, op[11], slot, idx, tile)
-                    # rotations (shear form) on the slots in a, then complex 2x2s
+                    # rotations (c, s) on the slots in a, then complex 2x2s
                     # on the slots in lmask (op[4])
                     mats = []
                     k = 0
                     for sl in range(len(reg)):
-                        if (a >> sl) & 1:  # rotation as shears (a, b): Sx(a) Sy(b) Sx(a)
-                            sa, sb = data[k], data[k + 1]
-                            sx = np.array([[1.0, sa], [0.0, 1.0]])
-                            sy = np.array([[1.0, 0.0], [sb, 1.0]])
-                            mats.append((sl, (sx @ sy @ sx).astype(np.complex128).ravel()))
+                        if (a >> sl) & 1:  # rotation [[c, -s], [s, c]]
+                            c, sn = data[k], data[k + 1]
+                            mats.append((sl, np.array([c, -sn, sn, c], dtype=np.complex128)))
                             k += 2
                     for sl in range(len(reg)):
                         if (lmask >> sl) & 1:

@@ -50,6 +50,24 @@ def test_uniform_superposition_ties(gpu):
     st.close()
 
 
+def test_near_ties_across_a_binade(gpu):
+    """Keys one or two ulps apart on both sides of a power of two (a nearly
+    uniform state): the radix digits split high up and the last, narrower
+    digit must still be read below the chosen prefix."""
+    rng = np.random.default_rng(11)
+    n = 20
+    base = 2.0 ** -10
+    lo = np.nextafter(base, 0.0)
+    hi = np.nextafter(base, 1.0)
+    vals = rng.choice([lo, base, hi, np.nextafter(hi, 1.0)], size=1 << n, p=[0.45, 0.45, 0.0998, 0.0002])
+    psi = vals.astype(np.complex128)
+    st = StateVector(n)
+    st.write(psi)
+    for k in (1, 100, 5000, 300000):
+        check(st, psi, k)
+    st.close()
+
+
 def test_quantised_amplitudes_many_ties(gpu):
     rng = np.random.default_rng(5)
     n = 18

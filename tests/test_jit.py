@@ -58,12 +58,13 @@ def test_source_is_deterministic_and_literal():
 
 
 def test_fp64_accounting_layered():
-    """A layer of RY rotations on every qubit of a 12-qubit state: one
-    rotation (3 FP64 / amplitude) per qubit, no tables."""
+    """A layer of RY rotations on every qubit of a 12-qubit state: one scaled
+    rotation (2 FP64 / amplitude) per qubit, no tables; the product of the
+    rotations' scales is folded into one complex table at the end (4)."""
     n = 12
     g = gate_array([gate(K.Ry, q, -1, 0.1 + q) for q in range(n)])
     js = json.loads(jit_probe(n, g, tile_qubits=12, reg_bits=3, low_bits=3))
-    assert js["fp64_per_amp"] == pytest.approx(3.0 * n)
+    assert js["fp64_per_amp"] == pytest.approx(2.0 * n + 4.0)
 
 
 # ---------------------------------------------------------------- GPU ------

@@ -81,3 +81,30 @@ def test_sign_only_tables_are_flips_and_scalars_fold():
     assert np.abs(got - want).max() <= 1e-12
     plan = json.loads(jit_probe(n, g, source_pass=-2))
     assert all(p["kind"] == "lowered" for p in plan["passes"])
+
+
+def test_scaled_rotations_renormalise_long_plans():
+    """Rotations lower to two-FMA scaled forms (c[[1,-t],[t,1]] or
+    s[[u,-1],[1,u]]) whose scales the plan carries; H / RY(pi/2) grow the
+    stored state by sqrt(2) each, so a 2400-rotation plan would overflow FP64
+    without the power-of-two renormalising words (qt_micro.cpp
+    kRescaleBelow). The replay must still match the oracle exactly."""
+    n = 6
+    rows = []
+    for layer in range(400):
+        for q in range(n):
+            rows.append(gate(K.H, q, -1) if (layer + q) % 2 else gate(K.Ry, q, -1, 1.5707963267948966))
+        for q in range(layer % 2, n - 1, 2):      # brick-wall CZ: no fusion
+            rows.append(gate(K.Cz, q, q + 1))
+    g = gate_array(rows)
+    plan = json.loads(jit_probe(n, g, source_pass=-2))
+    assert all(p["kind"] == "lowered" for p in plan["passes"])
+    from tests.emulator_lowered import _f
+    tiny = [v for ps in plan["passes"] for v in map(_f, ps["pool"]) if 0.0 < abs(v) < 2.0 ** -200]
+    assert tiny, "no renormalising scale word was emitted"
+
+    got = replay(n, g)
+    want = oracle.simulate(n, lower_to_reference(g))
+    assert np.isfinite(got).all()
+    assert np.abs(got - want).max() <= 1e-10
+    assert abs(float(np.vdot(got, got).real) - 1.0) <= 1e-12
