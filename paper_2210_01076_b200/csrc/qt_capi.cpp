@@ -553,6 +553,7 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
     if (reg_bits > 0) opt.reg_bits = std::min(reg_bits, qtb::kMaxRegBits);
     if (tile_qubits > 0) opt.tile_bits = std::min(tile_qubits, qtb::kMaxTileBits);
     if (low_bits > 0) opt.low_bits = low_bits;
+    if (const char* e = std::getenv("QTB_PASS_FP64")) opt.max_pass_fp64 = std::atof(e);
     std::vector<int> perm(num_qubits);
     for (int q = 0; q < num_qubits; ++q) perm[q] = q;
     const qtb::Plan p = qtb::make_plan(ops, num_qubits, num_qubits, perm, opt);

@@ -140,10 +140,27 @@ uint64_t raw_bits(double d) {
 // read with uniform loads -- the pass's constants overflow the per-SM
 // constant cache -- or copied once per CTA into shared memory. Literals ride
 // the instruction fetch, two uniform moves per non-encodable double.)
+// With a kernel-parameter block (JitPassSpec::kparam) the distinct
+// constants go to `K.k[i]` instead: DFMA reads them through uniform loads of
+// the parameter bank (one LDCU.128 per two doubles instead of four UMOVs).
 struct Consts {
-  std::string operator()(double d) const { return hexd(d); }
-  std::string pair(double a, double b) const { return hexd(a) + ", " + hexd(b); }
+  bool param = false;
+  std::vector<double> vals;
+  std::unordered_map<uint64_t, int> index;
+  std::string operator()(double d) {
+    if (!param) return hexd(d);
+    uint64_t w;
+    std::memcpy(&w, &d, 8);
+    auto it = index.find(w);
+    if (it == index.end()) {
+      it = index.emplace(w, static_cast<int>(vals.size())).first;
+      vals.push_back(d);
+    }
+    return "K.k[" + std::to_string(it->second) + "]";
+  }
+  std::string pair(double a, double b) { std::string x = (*this)(a); return x + ", " + (*this)(b); }
 };
+constexpr size_t kMaxKParams = 3800;  // doubles (kernel parameters <= 32764 bytes)
 
 // Code of one layer word.
 void emit_word(std::ostringstream& os, Consts& kc, int R, uint32_t x, uint32_t y,
@@ -403,6 +420,13 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
   }();
   sp.ring = ring_env && 3 * (sizeof(double2) << k) + 64 <= 227 * 1024 && (2 << (k - R)) <= 1024 &&
             (1 << (k - R)) >= 32 && buf_bits - k >= 1;
+  // measured slower on C3 (247 vs 195 ms: the parameter-bank loads spill
+  // registers), so off unless QTB_JIT_KPARAM=1
+  static const bool kparam_env = [] {
+    const char* e = std::getenv("QTB_JIT_KPARAM");
+    return e && std::atoi(e) != 0;
+  }();
+  sp.kparam = sp.ring && kparam_env;
   sp.rounds.resize(ps.rounds.size());
   for (size_t r = 0; r < ps.rounds.size(); ++r) {
     const PlanRound& pr = ps.rounds[r];
@@ -476,13 +500,14 @@ Direct direct_round(const JitPassSpec& sp, const DRound& rd) {
 // barrier per buffer its parity test would then see tile j's pending phase as
 // the "preceding" phase of j + 3's and pass. Barrier j % 6 was last used by
 // tile j - 6 of the same group, which that group has consumed.
-std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp) {
+std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vector<double>* kparams) {
   const int R = sp.R, NS = 1 << R, k = sp.k;
   const int T = 1 << (k - R);
   const size_t nr = sp.rounds.size();
   const uint32_t TB = 16u << k;
   std::ostringstream os;
   Consts kc;
+  kc.param = sp.kparam;
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
   const std::string outer = hexu(sp.outer_mask);
   os << "FI void mbar_wait(u32 a, u32 ph) {\n"
@@ -490,7 +515,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp) {
         " @!p bra W;\\n }\" :: \"r\"(a), \"r\"(ph) : \"memory\");\n}\n"
      << "FI void gbar(u32 id) { asm volatile(\"bar.sync %0, " << T << ";\" :: \"r\"(id) : \"memory\"); }\n"
      << "extern \"C\" __global__ void __launch_bounds__(" << 2 * T << ", 1)\n"
-     << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per) {\n"
+     << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per"
+     << (sp.kparam ? ", const __grid_constant__ KP K" : "") << ") {\n"
      << "  extern __shared__ __align__(16) double2 sm[];\n"
      << "  char* const sm0 = reinterpret_cast<char*>(sm);\n"
      << "  const u32 smbase = static_cast<u32>(__cvta_generic_to_shared(sm0));\n"
@@ -574,12 +600,25 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp) {
   os << "  }\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);\n";
   os << "}\n";
-  return kPrelude + os.str();
+  std::string head = kPrelude;
+  if (sp.kparam) {
+    if (kc.vals.size() > kMaxKParams) {
+      // too many constants for one parameter block: literals instead
+      JitPassSpec lit = sp;
+      lit.kparam = false;
+      if (kparams) kparams->clear();
+      return jit_source_ring(lit, mp, kparams);
+    }
+    if (kc.vals.empty()) kc.vals.push_back(0.0);
+    head += "struct KP { double k[" + std::to_string(kc.vals.size()) + "]; };\n";
+    if (kparams) *kparams = kc.vals;
+  }
+  return head + os.str();
 }
 
-std::string jit_source(const JitPassSpec& sp, const MicroPass& mp) {
+std::string jit_source(const JitPassSpec& sp, const MicroPass& mp, std::vector<double>* kparams) {
   const int R = sp.R, NS = 1 << R, k = sp.k;
-  if (sp.ring) return jit_source_ring(sp, mp);
+  if (sp.ring) return jit_source_ring(sp, mp, kparams);
   const int threads = 1 << (k - R);
   const size_t nr = sp.rounds.size();
   std::ostringstream os;
@@ -724,7 +763,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   // every input of jit_source, as bytes (exact: no hash collisions)
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
-  const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring,
+  const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam,
                           sp.coalesce_bits,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
@@ -748,8 +787,10 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
 namespace {
 
 // Loads a CUBIN and fills the launch facts; caller holds no lock.
-CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp) {
+CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp,
+                      const std::vector<double>& kparams) {
   CacheEntry e;
+  if (!kparams.empty()) e.k.kp = std::make_shared<const std::vector<double>>(kparams);
   if (cudaLibraryLoadData(&e.lib, bin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
       cudaLibraryGetKernel(&e.k.fn, e.lib, "qtjit") != cudaSuccess) {
     cudaGetLastError();
@@ -812,9 +853,10 @@ void worker() {
     }
     const auto t0 = std::chrono::steady_clock::now();
     try {
-      const std::vector<char> bin = compile_cubin(jit_source(j.spec, j.mp));
+      std::vector<double> kp;
+      const std::vector<char> bin = compile_cubin(jit_source(j.spec, j.mp, &kp));
       cudaSetDevice(j.device);
-      CacheEntry e = load_entry(bin, j.spec);
+      CacheEntry e = load_entry(bin, j.spec, kp);
       std::lock_guard<std::mutex> lk(g_mu);
       cache().emplace(j.key, e);
       ++g_stats.compiled;
@@ -840,7 +882,7 @@ void worker() {
 }  // namespace
 
 std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
-                                   const std::vector<std::function<std::string()>>& sources,
+                                   const std::vector<std::function<std::string(std::vector<double>*)>>& sources,
                                    const std::vector<JitPassSpec*>& specs) {
   std::vector<JitKernel> out(keys.size());
   std::vector<size_t> todo;
@@ -860,6 +902,7 @@ std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
   const auto t0 = std::chrono::steady_clock::now();
   // parallel NVRTC compiles (independent programs)
   std::vector<std::vector<char>> bins(keys.size());
+  std::vector<std::vector<double>> kps(keys.size());
   const size_t nthr = std::max<size_t>(1, std::min<size_t>(todo.size(), std::thread::hardware_concurrency()));
   std::atomic<size_t> next{0};
   std::mutex err_mu;
@@ -869,7 +912,7 @@ std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
   } ctx{[&] {
     for (size_t j; (j = next.fetch_add(1)) < todo.size();) {
       try {
-        bins[todo[j]] = compile_cubin(sources[todo[j]]());
+        bins[todo[j]] = compile_cubin(sources[todo[j]](&kps[todo[j]]));
       } catch (const std::exception& e) {
         std::lock_guard<std::mutex> lk(err_mu);
         if (err.empty()) err = e.what();
@@ -891,7 +934,7 @@ std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
   for (pthread_t th : ths) pthread_join(th, nullptr);
   if (!err.empty()) throw std::runtime_error(err);
   for (size_t i : todo) {
-    CacheEntry e = load_entry(bins[i], *specs[i]);
+    CacheEntry e = load_entry(bins[i], *specs[i], kps[i]);
     out[i] = e.k;
     std::lock_guard<std::mutex> lk(g_mu);
     cache().emplace(keys[i], e);
@@ -926,8 +969,9 @@ void jit_compile_async(const std::string& key, const JitPassSpec& spec, const Mi
     // state is torn down.
     const auto t0 = std::chrono::steady_clock::now();
     try {
-      const std::vector<char> bin = compile_cubin(jit_source(spec, mp));
-      CacheEntry e = load_entry(bin, spec);
+      std::vector<double> kp;
+      const std::vector<char> bin = compile_cubin(jit_source(spec, mp, &kp));
+      CacheEntry e = load_entry(bin, spec, kp);
       std::lock_guard<std::mutex> lk(g_mu);
       cache().emplace(key, e);
       ++g_stats.compiled;
@@ -985,7 +1029,8 @@ cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* ps
   const uint64_t cap = static_cast<uint64_t>(k.occupancy) * static_cast<uint64_t>(sms);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, cap));
   uint64_t per = (ntiles + grid - 1) / grid;
-  void* args[] = {&psi, &src, &flag, &gbase_hi, &per};
+  void* args[] = {&psi, &src, &flag, &gbase_hi, &per,
+                  k.kp ? const_cast<double*>(k.kp->data()) : nullptr};
   return cudaLaunchKernel(reinterpret_cast<const void*>(k.fn), dim3(grid), dim3(k.threads), args,
                           k.smem, s);
 }

@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -38,6 +39,7 @@ struct JitPassSpec {
   bool check = false;
   bool pipe = false;    // double-buffered tiles: the next tile streams in (cp.async) during the rounds
   int pf_bits = 0;      // > 0: L2 prefetch of the next tile in runs of 2^pf_bits amplitudes
+  bool kparam = false;  // FP64 constants in a kernel-parameter block (ring kernel), not literals
   bool ring = false;    // persistent CTA, two consumer groups, 3-buffer cp.async + mbarrier ring (jit_source_ring)
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
   std::vector<DRound> rounds;  // reg / sreg / sbit per round
@@ -52,13 +54,17 @@ struct JitKernel {
   int threads = 0;
   size_t smem = 0;
   int occupancy = 0;  // resident CTAs per SM
+  std::shared_ptr<const std::vector<double>> kp;  // the kernel-parameter constants (kparam passes)
 };
 
 // Tile geometry of a planned pass (buf_bits = log2 of the local buffer).
 JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool check);
 
 // CUDA C++ source of one compiled pass.
-std::string jit_source(const JitPassSpec& spec, const MicroPass& mp);
+// With spec.kparam the pass's distinct FP64 constants are returned in
+// *kparams (the launch passes them as the kernel-parameter block).
+std::string jit_source(const JitPassSpec& spec, const MicroPass& mp,
+                       std::vector<double>* kparams = nullptr);
 
 // Exact cache key of a compiled pass: the bytes of every input of
 // jit_source (looking a pass up costs no source generation).
@@ -67,7 +73,7 @@ std::string jit_key(const JitPassSpec& spec, const MicroPass& mp);
 // Compiles (or finds in the cache) the kernels of `keys` (sources generated
 // on a miss only), in parallel. Throws on compile / load failure.
 std::vector<JitKernel> jit_kernels(const std::vector<std::string>& keys,
-                                   const std::vector<std::function<std::string()>>& sources,
+                                   const std::vector<std::function<std::string(std::vector<double>*)>>& sources,
                                    const std::vector<JitPassSpec*>& specs);
 
 // Hybrid mode: a cached kernel, or false (the caller runs the interpreter

@@ -909,12 +909,15 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
     int nblocked = 0;
     PlanPass pass;
     size_t scanned = 0;
+    double fp64 = 0.0;
     for (size_t i = first; i < nops && scanned < static_cast<size_t>(opt.lookahead); ++i) {
       if (done[i]) continue;
       ++scanned;
       const LOp& op = ops[i];
       const int nr = roles(op, rl);
       bool can = true;
+      const double cost = (op.kind == LKind::Dense) ? 3.0 : 0.0;
+      if (opt.max_pass_fp64 > 0.0 && !pass.ops.empty() && fp64 + cost > opt.max_pass_fp64) can = false;
       for (int t = 0; t < nr; ++t) {
         if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
       }
@@ -942,6 +945,7 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
       }
       if (can) {
         done[i] = 1;
+        fp64 += cost;
         pass.ops.push_back(to_phys(op, cur));
       } else {
         for (int t = 0; t < nr; ++t) {

@@ -19,7 +19,18 @@ struct PlanOptions {
   // local qubits up: it costs host time per round and pays off only where a
   // pass streams enough amplitudes (small states are launch/host-bound)
   int round_search_min_bits = 22;
+  // estimated FP64 ops per amplitude a tile pass may carry (0 = no cap): a
+  // non-diagonal op counts ~3 (scaled rotation + its share of a table).
+  // Balances FP64-heavy passes against HBM-bound ones (QTB_PASS_FP64).
+  double max_pass_fp64 = 0.0;
 };
+
+// Cost model of the compiled-mode plan search (qt_state.cpp State::plan):
+// FP64 pipe rate (DFMA/s, B200 probe at load clocks) and the ring kernel's
+// measured streaming rate (B/s, tools/tilebits_bench.py: ~5.9 TB/s).
+constexpr double kPlanFp64PerS = 1.75e13;
+constexpr double kPlanHbmBytesPerS = 5.9e12;
+constexpr int kPlanSearchMinBits = 24;
 
 // Merges runs of uncontrolled single-qubit ops on the same qubit into one
 // 2x2 (matrix product) and drops exact identities. Order-preserving:

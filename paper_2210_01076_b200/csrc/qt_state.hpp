@@ -176,6 +176,7 @@ class State {
   // use); 2 = hybrid: passes found in the compile cache run compiled, the
   // others on the interpreter while they compile in the background
   int jit_mode_ = 0;
+  bool plan_search_ = true;  // compiled mode: search the per-pass FP64 cap (QTB_PLAN_SEARCH=0: off)
   int jit_min_blocks_ = 0;  // compiled passes' launch-bound override (QTB_JIT_MINB)
   // compiled passes: first / last round straight from / to HBM when physical
   // bits [0, direct_bits_) stay thread bits (128-B runs); 0 = always stage
