@@ -136,6 +136,18 @@ int qt_state_create(int num_qubits, const qt_config* cfg, qt_state** out);
 int qt_state_create_sharded(int num_qubits, int rank, int world,
                             const void* nccl_id, const qt_config* cfg,
                             qt_state** out);
+/* An in-process group of `world` emulated ranks (power of two): each rank
+ * is a qt_state made by qt_state_create_group and driven by its own host
+ * thread; the ranks' exchanges are rendezvous of those threads with the data
+ * moved by device-to-device copies ordered by CUDA events (qt_comm.hpp
+ * LocalComm). Same kernels, rank offsets, exchange schedule and norm combine
+ * as qt_state_create_sharded, on one GPU (or several GPUs of one process).
+ * The group must outlive its states. */
+typedef struct qt_group qt_group;
+int qt_group_create(int world, qt_group** out);
+int qt_group_destroy(qt_group* g);
+int qt_state_create_group(int num_qubits, qt_group* group, int rank,
+                          const qt_config* cfg, qt_state** out);
 /* `shards` emulated ranks held as slices of one GPU's memory, exchanged
  * with device copies -- exercises the sharded scheduler bit-exactly on
  * one GPU ("loopback comm backend"). */

@@ -12,6 +12,6 @@ from .errors import (BadQubitError, Error, InvalidPositionError,  # noqa: F401
                      SuperpositionGateError, UnknownGateError, UnknownNetError)
 from .gates import GateKind, gate, gate_array, lower_to_reference  # noqa: F401
 from .simulator import Config, Simulator, UpdateStats  # noqa: F401
-from .state import StateVector, nccl_unique_id, probe_fp64  # noqa: F401
+from .state import RankGroup, StateVector, nccl_unique_id, probe_fp64  # noqa: F401
 
 __all__ = ["GateKind", "Simulator", "Config", "StateVector", "gate", "gate_array"]

@@ -53,6 +53,7 @@ class QtRunStats(ctypes.Structure):
 HEADER_SYMBOLS = [
     "qt_last_error", "qt_device_count", "qt_version",
     "qt_state_create", "qt_state_create_sharded", "qt_state_create_loopback",
+    "qt_group_create", "qt_group_destroy", "qt_state_create_group",
     "qt_nccl_unique_id", "qt_state_destroy", "qt_state_num_qubits", "qt_set_basis",
     "qt_write", "qt_read", "qt_apply", "qt_norm_squared", "qt_sync", "qt_last_stats",
     "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe", "qt_jit_probe", "qt_jit_stats", "qt_jit_pending",
@@ -78,6 +79,9 @@ _SIGS = {
     "qt_state_create_sharded": ([_c.c_int, _c.c_int, _c.c_int, _vp, _vp,
                                  _c.POINTER(_vp)], _c.c_int),
     "qt_state_create_loopback": ([_c.c_int, _c.c_int, _vp, _c.POINTER(_vp)], _c.c_int),
+    "qt_group_create": ([_c.c_int, _c.POINTER(_vp)], _c.c_int),
+    "qt_group_destroy": ([_vp], _c.c_int),
+    "qt_state_create_group": ([_c.c_int, _vp, _c.c_int, _vp, _c.POINTER(_vp)], _c.c_int),
     "qt_nccl_unique_id": ([_vp], _c.c_int),
     "qt_state_destroy": ([_vp], _c.c_int),
     "qt_state_num_qubits": ([_vp], _c.c_int),

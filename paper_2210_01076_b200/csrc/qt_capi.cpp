@@ -104,7 +104,33 @@ int qt_state_create_sharded(int num_qubits, int rank, int world,
                             qt_state** out) {
   if (!out || !nccl_id) return null_arg();
   return guard([&] {
-    *out = new qt_state{new qtb::State(num_qubits, qtb::Mode::Nccl, world, rank, nccl_id, cfg)};
+    *out = new qt_state{new qtb::State(num_qubits, qtb::Mode::Sharded, world, rank, nccl_id, cfg)};
+  });
+}
+
+struct qt_group {
+  std::shared_ptr<qtb::LocalGroup> g;
+};
+
+int qt_group_create(int world, qt_group** out) {
+  if (!out) return null_arg();
+  return guard([&] {
+    if (world < 1 || (world & (world - 1)) != 0) qtb::fail(QT_ERR_ARG, "group size must be a power of two");
+    *out = new qt_group{std::make_shared<qtb::LocalGroup>(world)};
+  });
+}
+
+int qt_group_destroy(qt_group* g) {
+  if (!g) return QT_OK;
+  return guard([&] { delete g; });
+}
+
+int qt_state_create_group(int num_qubits, qt_group* group, int rank, const qt_config* cfg,
+                          qt_state** out) {
+  if (!out || !group) return null_arg();
+  return guard([&] {
+    *out = new qt_state{new qtb::State(num_qubits, qtb::Mode::Sharded, group->g->world(), rank,
+                                       nullptr, cfg, group->g)};
   });
 }
 
@@ -120,7 +146,7 @@ int qt_nccl_unique_id(void* out128) {
   if (!out128) return null_arg();
   return guard([&] {
     std::string err;
-    if (!qtb::Comm::unique_id(out128, &err)) qtb::fail(QT_ERR_NCCL, err);
+    if (!qtb::NcclComm::unique_id(out128, &err)) qtb::fail(QT_ERR_NCCL, err);
   });
 }
 

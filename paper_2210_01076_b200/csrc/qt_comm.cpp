@@ -1,4 +1,5 @@
-// qt_comm.cpp -- NCCL over NVLink for global<->local qubit exchanges.
+// qt_comm.cpp -- transports for global<->local qubit exchanges: NCCL over
+// NVLink, and an in-process group of emulated ranks (qt_comm.hpp).
 //
 // The reference is single-process (executor.hpp:40-47); sharding the state
 // on its top qubits across GPUs is new in this build.
@@ -8,6 +9,7 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstring>
 
 namespace qtb {
@@ -82,7 +84,7 @@ static bool nccl_ok(NcclApi* api, ncclResult_t r, const char* what,
   return false;
 }
 
-bool Comm::unique_id(void* out128, std::string* err) {
+bool NcclComm::unique_id(void* out128, std::string* err) {
   NcclApi* api = load_api(err);
   if (!api) return false;
   ncclUniqueId id;
@@ -91,8 +93,8 @@ bool Comm::unique_id(void* out128, std::string* err) {
   return true;
 }
 
-Comm* Comm::create(const void* unique_id, int rank, int world, int device,
-                   std::string* err) {
+NcclComm* NcclComm::create(const void* unique_id, int rank, int world, int device,
+                           std::string* err) {
   NcclApi* api = load_api(err);
   if (!api) return nullptr;
   if (cudaSetDevice(device) != cudaSuccess) {
@@ -105,7 +107,7 @@ Comm* Comm::create(const void* unique_id, int rank, int world, int device,
   if (!nccl_ok(api, api->CommInitRank(&c, world, id, rank), "ncclCommInitRank",
                err))
     return nullptr;
-  Comm* cm = new Comm();
+  NcclComm* cm = new NcclComm();
   cm->api_ = api;
   cm->comm_ = c;
   cm->rank_ = rank;
@@ -113,13 +115,13 @@ Comm* Comm::create(const void* unique_id, int rank, int world, int device,
   return cm;
 }
 
-Comm::~Comm() {
+NcclComm::~NcclComm() {
   if (api_ && comm_) api_->CommDestroy(comm_);
 }
 
-bool Comm::sendrecv(int npeers, const int* peers, const void* const* sends,
-                    void* const* recvs, size_t bytes, cudaStream_t s,
-                    std::string* err) {
+bool NcclComm::sendrecv(int npeers, const int* peers, const void* const* sends,
+                        void* const* recvs, size_t bytes, cudaStream_t s,
+                        std::string* err) {
   if (!nccl_ok(api_, api_->GroupStart(), "ncclGroupStart", err)) return false;
   for (int i = 0; i < npeers; ++i) {
     if (!nccl_ok(api_, api_->Send(sends[i], bytes, ncclUint8, peers[i], comm_, s),
@@ -133,16 +135,132 @@ bool Comm::sendrecv(int npeers, const int* peers, const void* const* sends,
   return nccl_ok(api_, api_->GroupEnd(), "ncclGroupEnd", err);
 }
 
-bool Comm::allgather_double(const double* in, double* out, cudaStream_t s,
-                            std::string* err) {
+bool NcclComm::allgather_double(const double* in, double* out, cudaStream_t s,
+                                std::string* err) {
   return nccl_ok(api_, api_->AllGather(in, out, 1, ncclFloat64, comm_, s),
                  "ncclAllGather", err);
 }
 
-bool Comm::check_async(std::string* err) {
+bool NcclComm::check_async(std::string* err) {
   ncclResult_t r = 0;
   api_->CommGetAsyncError(comm_, &r);
   return nccl_ok(api_, r, "NCCL async error", err);
+}
+
+// ---- in-process group ------------------------------------------------------
+
+namespace {
+constexpr auto kRendezvousTimeout = std::chrono::seconds(600);
+}
+
+LocalGroup::LocalGroup(int world) : world_(world), slots_(world) {}
+
+LocalGroup::~LocalGroup() {
+  for (Slot& sl : slots_) {
+    if (sl.device >= 0) cudaSetDevice(sl.device);
+    if (sl.ready) cudaEventDestroy(sl.ready);
+    if (sl.read) cudaEventDestroy(sl.read);
+  }
+}
+
+LocalComm::LocalComm(std::shared_ptr<LocalGroup> g, int rank, int device) : g_(std::move(g)) {
+  rank_ = rank;
+  world_ = g_->world();
+  LocalGroup::Slot& me = g_->slots_[rank];
+  me.device = device;
+  me.send_to.assign(world_, nullptr);
+  cudaEventCreateWithFlags(&me.ready, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&me.read, cudaEventDisableTiming);
+}
+
+LocalComm::~LocalComm() = default;
+
+template <typename Copy>
+bool LocalComm::rendezvous(const std::vector<int>& peers, cudaStream_t s, Copy copy,
+                           std::string* err) {
+  LocalGroup& g = *g_;
+  LocalGroup::Slot& me = g.slots_[rank_];
+  uint64_t seq = 0;
+  {
+    std::unique_lock<std::mutex> lk(g.mu_);
+    if (cudaEventRecord(me.ready, s) != cudaSuccess) {
+      if (err) *err = "local transport: event record failed";
+      return false;
+    }
+    seq = ++me.seq;
+    g.cv_.notify_all();
+    const bool ok = g.cv_.wait_for(lk, kRendezvousTimeout, [&] {
+      for (int p : peers)
+        if (g.slots_[p].seq < seq) return false;
+      return true;
+    });
+    if (!ok) {
+      if (err) *err = "local transport: a peer rank never reached the exchange";
+      return false;
+    }
+  }
+  // the peers' sends are ready (stream order) and stay untouched until they
+  // pass the read barrier below, which waits for this rank's reads
+  for (int p : peers)
+    if (p != rank_) cudaStreamWaitEvent(s, g.slots_[p].ready, 0);
+  if (!copy()) {
+    if (err) *err = "local transport: device copy failed";
+    return false;
+  }
+  {
+    std::unique_lock<std::mutex> lk(g.mu_);
+    cudaEventRecord(me.read, s);
+    me.read_seq = seq;
+    g.cv_.notify_all();
+    const bool ok = g.cv_.wait_for(lk, kRendezvousTimeout, [&] {
+      for (int p : peers)
+        if (g.slots_[p].read_seq < seq) return false;
+      return true;
+    });
+    if (!ok) {
+      if (err) *err = "local transport: a peer rank never finished the exchange";
+      return false;
+    }
+  }
+  for (int p : peers)
+    if (p != rank_) cudaStreamWaitEvent(s, g.slots_[p].read, 0);
+  return true;
+}
+
+bool LocalComm::sendrecv(int npeers, const int* peers, const void* const* sends,
+                         void* const* recvs, size_t bytes, cudaStream_t s, std::string* err) {
+  LocalGroup::Slot& me = g_->slots_[rank_];
+  std::vector<int> pv(peers, peers + npeers);
+  {
+    std::lock_guard<std::mutex> lk(g_->mu_);
+    for (int i = 0; i < npeers; ++i) me.send_to[peers[i]] = sends[i];
+  }
+  return rendezvous(pv, s, [&] {
+    for (int i = 0; i < npeers; ++i) {
+      const void* src = g_->slots_[peers[i]].send_to[rank_];
+      if (cudaMemcpyAsync(recvs[i], src, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return false;
+    }
+    return true;
+  }, err);
+}
+
+bool LocalComm::allgather_double(const double* in, double* out, cudaStream_t s,
+                                 std::string* err) {
+  LocalGroup::Slot& me = g_->slots_[rank_];
+  std::vector<int> all(world_);
+  for (int r = 0; r < world_; ++r) all[r] = r;
+  {
+    std::lock_guard<std::mutex> lk(g_->mu_);
+    me.gather_src = in;
+  }
+  return rendezvous(all, s, [&] {
+    for (int r = 0; r < world_; ++r)
+      if (cudaMemcpyAsync(out + r, g_->slots_[r].gather_src, sizeof(double),
+                          cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+        return false;
+    return true;
+  }, err);
 }
 
 }  // namespace qtb

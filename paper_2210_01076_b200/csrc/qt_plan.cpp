@@ -877,7 +877,9 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
         }
       }
       const int g = nqubits - nlocal;
-      if (static_cast<int>(need_g.size()) > g) need_g.resize(g);
+      // at most g globals per exchange, and no more than there are local
+      // victim bits (shards of fewer bits than the rank bits)
+      if (static_cast<int>(need_g.size()) > std::min(g, nlocal)) need_g.resize(std::min(g, nlocal));
       // victims: among the top local bits, the furthest next X use first
       const int ncand = std::min(nlocal, std::max(4, static_cast<int>(need_g.size())));
       std::vector<int> cand;

@@ -46,7 +46,7 @@ int ilog2(uint64_t x) {
 }  // namespace
 
 State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
-             const qt_config* cfg)
+             const qt_config* cfg, std::shared_ptr<LocalGroup> group)
     : n_(nqubits), mode_(mode), rank_(rank), world_(shards) {
   if (nqubits < 1 || nqubits > 40) fail(QT_ERR_BAD_QUBIT, "qubit count must be in [1, 40]");
   if (shards < 1 || (shards & (shards - 1)) != 0)
@@ -123,10 +123,16 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   perm_.resize(n_);
   for (int q = 0; q < n_; ++q) perm_[q] = q;
 
-  if (mode == Mode::Nccl) {
-    std::string err;
-    comm_.reset(Comm::create(nccl_id, rank, shards, device_, &err));
-    if (!comm_) fail(QT_ERR_NCCL, err);
+  if (mode == Mode::Sharded) {
+    if (rank < 0 || rank >= shards) fail(QT_ERR_ARG, "rank out of range");
+    if (group) {
+      if (group->world() != shards) fail(QT_ERR_ARG, "group size differs from the shard count");
+      comm_.reset(new LocalComm(group, rank, device_));
+    } else {
+      std::string err;
+      comm_.reset(NcclComm::create(nccl_id, rank, shards, device_, &err));
+      if (!comm_) fail(QT_ERR_NCCL, err);
+    }
   }
   set_basis(0);
 }
@@ -156,7 +162,7 @@ void State::set_basis(uint64_t index) {
   for (int q = 0; q < n_; ++q) perm_[q] = q;
   uint64_t local = index;
   uint64_t target = ~0ull;  // index within this buffer, or none
-  if (mode_ == Mode::Nccl) {
+  if (mode_ == Mode::Sharded) {
     const uint64_t owner = index >> nlocal_;
     local = index & ((1ull << nlocal_) - 1);
     if (owner == static_cast<uint64_t>(rank_)) target = local;
@@ -173,7 +179,7 @@ void State::write(uint64_t first, uint64_t count, const double* src) {
     if (perm_[q] != q) fail(QT_ERR_ARG, "write needs the canonical qubit order (call set_basis)");
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   uint64_t lo = first, hi = first + count;
-  if (mode_ == Mode::Nccl) {
+  if (mode_ == Mode::Sharded) {
     const uint64_t s0 = static_cast<uint64_t>(rank_) << nlocal_;
     const uint64_t s1 = s0 + (1ull << nlocal_);
     lo = std::max(lo, s0);
@@ -197,7 +203,7 @@ void State::read(uint64_t first, uint64_t count, double* dst) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   bool identity = true;
   for (int q = 0; q < n_; ++q) identity = identity && perm_[q] == q;
-  if (identity && mode_ != Mode::Nccl) {
+  if (identity && mode_ != Mode::Sharded) {
     cuda_check(cudaMemcpyAsync(dst, psi_ + first, count * sizeof(double2),
                                cudaMemcpyDeviceToHost, stream_),
                "read");
@@ -216,7 +222,7 @@ void State::read(uint64_t first, uint64_t count, double* dst) {
   for (int q = 0; q < n_; ++q) pm[q] = static_cast<uint8_t>(perm_[q]);
   for (uint64_t off = 0; off < count; off += chunk) {
     const uint64_t c = std::min(chunk, count - off);
-    if (mode_ == Mode::Nccl) {
+    if (mode_ == Mode::Sharded) {
       cuda_check(launch_gather_shard(psi_, d_tmp_, first + off, c, pm.data(), n_,
                                      nlocal_, static_cast<uint64_t>(rank_), stream_),
                  "gather");
@@ -581,7 +587,7 @@ void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2*
       tstart(0);
       cuda_check(jit_launch(jk[pi], 1ull << (buf_bits_ - static_cast<int>(ps.tile_phys.size())), sms_,
                             psi_, src ? src : psi_, d_flag_,
-                            mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0,
+                            mode_ == Mode::Sharded ? (static_cast<uint64_t>(rank_) << nlocal_) : 0,
                             stream_),
                  "compiled pass launch");
       src = nullptr;
@@ -623,7 +629,7 @@ void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2*
       h.slot_sb[s] = swz_host(s << (k - R)) << 4;
     }
     h.ntiles = 1ull << (buf_bits_ - k);
-    h.gbase_hi = mode_ == Mode::Nccl ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
+    h.gbase_hi = mode_ == Mode::Sharded ? (static_cast<uint64_t>(rank_) << nlocal_) : 0;
     // lean kernel (micro-ops) when the pass lowered and fits a launch;
     // otherwise the generic kernel decodes the device ops
     const MicroPass& mp = micro[pi];
@@ -754,11 +760,14 @@ void State::exchange(const PlanPass& pass) {
     stats.exchanged_bytes += pass.exchange.size() * (buffer_amps() / 2) * sizeof(double2);
     return;
   }
-  if (mode_ != Mode::Nccl) fail(QT_ERR_ARG, "exchange on an unsharded state");
+  if (mode_ != Mode::Sharded) fail(QT_ERR_ARG, "exchange on an unsharded state");
   const int k = static_cast<int>(pass.exchange.size());
   // receive buffer: at most 1/8 of the shard, split across the peers
   uint64_t want = std::max<uint64_t>(1, (1ull << nlocal_) / 8);
   want = std::min<uint64_t>(want, 1ull << 27);  // 2 GiB
+  // every step receives at least one amplitude from each of the 2^k - 1
+  // peers (small shards: 1/8 of the shard can be less than that)
+  want = std::max<uint64_t>(want, (1ull << k) - 1);
   if (d_tmp_amps_ < want) {
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     cudaFree(d_tmp_);
@@ -801,7 +810,7 @@ void State::exchange(const PlanPass& pass) {
 // logical index order (two more sweeps). Permuted (loopback) states are
 // streamed in logical-order chunks through the gather kernel.
 std::vector<TopkItem> State::top_k(uint64_t k) {
-  if (mode_ == Mode::Nccl) fail(QT_ERR_ARG, "top_k: sharded (NCCL) states are not supported");
+  if (mode_ == Mode::Sharded) fail(QT_ERR_ARG, "top_k: sharded (NCCL) states are not supported");
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   const uint64_t total = 1ull << n_;
   k = std::min(k, total);
@@ -938,7 +947,7 @@ double State::norm_squared() {
   double* out = d_scratch_ + kNormBlocks;
   cuda_check(launch_norm(psi_, buffer_amps(), d_scratch_, out, stream_), "norm");
   std::vector<double> parts(world_, 0.0);
-  if (mode_ == Mode::Nccl) {
+  if (mode_ == Mode::Sharded) {
     std::string err;
     double* gathered = d_scratch_ + kNormBlocks + 1;
     if (!comm_->allgather_double(out, gathered, stream_, &err)) fail(QT_ERR_NCCL, err);
@@ -952,7 +961,7 @@ double State::norm_squared() {
   }
   sync();
   double acc = 0.0;
-  for (int r = 0; r < (mode_ == Mode::Nccl ? world_ : 1); ++r) acc += parts[r];
+  for (int r = 0; r < (mode_ == Mode::Sharded ? world_ : 1); ++r) acc += parts[r];
   return acc;
 }
 

@@ -27,7 +27,7 @@ struct QtError {
 [[noreturn]] void fail(int code, const std::string& msg);
 void cuda_check(cudaError_t e, const char* what);
 
-enum class Mode { Single, Loopback, Nccl };
+enum class Mode { Single, Loopback, Sharded };
 
 // Per-pass timing record (when timing is enabled).
 struct PassTiming {
@@ -52,8 +52,10 @@ std::vector<ExchangeStep> exchange_schedule(int rank, int nlocal,
 
 class State {
  public:
+  // Sharded states exchange through NCCL (nccl_id) or, when `group` is
+  // given, through the in-process transport of that group (qt_comm.hpp).
   State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
-        const qt_config* cfg);
+        const qt_config* cfg, std::shared_ptr<LocalGroup> group = nullptr);
   ~State();
 
   int nqubits() const { return n_; }

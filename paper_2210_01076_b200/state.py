@@ -15,7 +15,9 @@ class StateVector:
 
     mode: "single" (one GPU), "loopback" (``shards`` emulated ranks on one
     GPU, exchanges by device copies) or "sharded" (one rank of a
-    ``world``-GPU state, NCCL exchanges; pass ``rank``, ``world``, ``nccl_id``).
+    ``world``-GPU state, NCCL exchanges; pass ``rank``, ``world``, ``nccl_id``)
+    or "group" (rank ``rank`` of an in-process RankGroup: the sharded kernels and
+    exchange schedule with an in-process transport; see RankGroup).
     compiled=True runs every tile pass as its own NVRTC-compiled straight-line
     kernel (cached process-wide by the pass's content: for circuits applied more
     than once); compiled=2: hybrid (cached passes compiled, the others on the
@@ -24,7 +26,8 @@ class StateVector:
 
     def __init__(self, num_qubits: int, mode: str = "single", shards: int = 1,
                  rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 device: int = -1, tile_qubits: int = 0, compiled: bool = False):
+                 device: int = -1, tile_qubits: int = 0, compiled: bool = False,
+                 group: "RankGroup | None" = None):
         self._h = ctypes.c_void_p()
         cfg = _ffi.make_config(device=device, tile_qubits=tile_qubits, compiled=compiled)
         if mode == "single":
@@ -32,6 +35,12 @@ class StateVector:
         elif mode == "loopback":
             check(lib().qt_state_create_loopback(num_qubits, shards, ctypes.byref(cfg),
                                                  ctypes.byref(self._h)))
+        elif mode == "group":
+            if group is None:
+                raise ValueError("group mode needs a RankGroup")
+            self._group = group  # keeps the group alive
+            check(lib().qt_state_create_group(num_qubits, group.handle, rank, ctypes.byref(cfg),
+                                              ctypes.byref(self._h)))
         elif mode == "sharded":
             if nccl_id is None or len(nccl_id) != 128:
                 raise ValueError("sharded mode needs the 128-byte NCCL unique id")
@@ -145,3 +154,90 @@ def probe_fp64(device: int = 0) -> float:
     v = ctypes.c_double(0.0)
     check(lib().qt_probe_fp64(device, ctypes.byref(v)))
     return v.value
+
+
+class RankGroup:
+    """An in-process group of ``world`` emulated ranks of one sharded state
+    (qt_group_create / qt_state_create_group): the same kernels, rank offsets,
+    exchange schedule and norm combine as one-process-per-GPU NCCL sharding,
+    with the exchanges as device-to-device copies between the ranks' buffers
+    (csrc/qt_comm.hpp LocalComm). Every collective call (apply with exchanges,
+    norm_squared) must be made by all ranks concurrently: ``run`` calls a
+    function on every rank, each on its own host thread (ctypes releases the
+    GIL during the native calls)."""
+
+    def __init__(self, num_qubits: int, world: int, device: int = -1, tile_qubits: int = 0,
+                 compiled: bool = False):
+        self._g = ctypes.c_void_p()
+        check(lib().qt_group_create(world, ctypes.byref(self._g)))
+        self.n = num_qubits
+        self.world = world
+        self.ranks = [StateVector(num_qubits, mode="group", rank=r, device=device,
+                                  tile_qubits=tile_qubits, compiled=compiled, group=self)
+                      for r in range(world)]
+
+    @property
+    def handle(self):
+        return self._g
+
+    def run(self, fn):
+        """[fn(rank_state) for every rank], concurrently; re-raises the first error."""
+        import threading
+        out = [None] * self.world
+        errs = [None] * self.world
+
+        def go(r):
+            try:
+                out[r] = fn(self.ranks[r])
+            except BaseException as e:  # reported to the caller
+                errs[r] = e
+
+        th = [threading.Thread(target=go, args=(r,)) for r in range(self.world)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return out
+
+    def set_basis(self, index: int = 0):
+        self.run(lambda st: st.set_basis(index))
+
+    def apply(self, gates: np.ndarray):
+        self.run(lambda st: st.apply(gates))
+
+    def norm_squared(self) -> float:
+        vals = self.run(lambda st: st.norm_squared())
+        assert all(v == vals[0] for v in vals), "ranks disagree on the norm"
+        return vals[0]
+
+    def read(self, first: int = 0, count: int | None = None) -> np.ndarray:
+        """Logical amplitudes [first, first+count): each rank fills the ones it
+        holds (zeros elsewhere), summed here."""
+        if count is None:
+            count = (1 << self.n) - first
+        acc = np.zeros(count, dtype=np.complex128)
+        buf = np.empty(count, dtype=np.complex128)
+        for st in self.ranks:
+            st.read(first, count, buf)
+            acc += buf
+        return acc
+
+    def stats(self):
+        return [st.stats() for st in self.ranks]
+
+    def close(self):
+        for st in getattr(self, "ranks", []):
+            st.close()
+        self.ranks = []
+        if getattr(self, "_g", None) and self._g.value:
+            lib().qt_group_destroy(self._g)
+            self._g = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
