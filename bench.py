@@ -322,15 +322,19 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
     # per-launch events recorded on the same stream inside the timed region
-    pass_ms = [ms for kind, ms in st.last_timings() if kind == 0]
+    timings = st.last_timings()
+    pass_ms = [ms for kind, ms in timings if kind == 0]
+    exch_ms = [ms for kind, ms in timings if kind == 1]
+    run_stats = st.stats()
     st.sync()
     ms = e0.elapsed_time(e1)
     st.set_timing(False)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, sum(exch_ms) / max(1, args.steps)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
-    ms = float(t.item())
+    ms = float(t[0].item())
+    exch_ms_step = float(t[1].item())
     sec = ms / 1e3
     value = args.steps * G * amps / sec
     launches = args.steps * (len(tiles) + 1 + sum(len(p.get("swap", []))
@@ -426,6 +430,21 @@ def main():
         "check": {"norm_error": abs(nrm - 1.0),
                   "note": "|<psi|psi> - 1| of the last e2e step's state (deterministic "
                           "two-level reduction)"},
+        "exchange": ({
+            "swaps_per_step": int(run_stats["swaps"]),
+            "sent_bytes_per_step_per_gpu": int(run_stats["exchanged_bytes"]),
+            "local_copy_bytes_per_step_per_gpu": int(run_stats["exchange_local_bytes"]),
+            "device_ms_per_step": exch_ms_step,
+            "ms_per_swap": exch_ms_step / max(1, run_stats["swaps"]),
+            "nvlink_gbs_per_gpu": (run_stats["exchanged_bytes"] / (exch_ms_step * 1e-3) / 1e9
+                                   if exch_ms_step > 0 else None),
+            "nvlink_frac": (run_stats["exchanged_bytes"] / (exch_ms_step * 1e-3) / 900e9
+                            if exch_ms_step > 0 else None),
+            "nvlink_peak_note": "900 GB/s per direction per GPU (nominal NVLink 5); the "
+                                "measured peer copy on this pool is ~770 GB/s",
+            "transport": "NCCL grouped send/recv, two-buffer exchange (received regions land "
+                         "in place; only this rank's own region is copied locally)",
+        } if world > 1 else None),
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

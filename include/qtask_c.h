@@ -114,6 +114,7 @@ typedef struct qt_run_stats {
   uint64_t segments;            /* checkpoint segments executed            */
   double device_ms;             /* device time of the call (CUDA events)   */
   double plan_ms;               /* host planning time                      */
+  uint64_t exchange_local_bytes;/* local HBM bytes the exchanges copied    */
 } qt_run_stats;
 
 const char* qt_last_error(void);

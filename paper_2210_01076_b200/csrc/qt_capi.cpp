@@ -53,6 +53,17 @@ int guard(F&& f) {
   }
 }
 
+// Collective calls of a sharded state: a failure on this rank releases the
+// rest of an in-process group (their rendezvous report it) instead of
+// leaving them waiting for this rank.
+template <typename F>
+int guard_collective(qt_state* st, F&& f) {
+  const int rc = guard(std::forward<F>(f));
+  if (rc != QT_OK) st->s->abort_comm(g_err);
+  return rc;
+}
+
+
 int null_arg() {
   g_err = "null argument";
   return QT_ERR_ARG;
@@ -177,12 +188,12 @@ int qt_read(qt_state* st, uint64_t first, uint64_t count, double* outp) {
 
 int qt_apply(qt_state* st, const qt_gate* gates, size_t count) {
   if (!st || (!gates && count)) return null_arg();
-  return guard([&] { st->s->apply(gates, count); });
+  return guard_collective(st, [&] { st->s->apply(gates, count); });
 }
 
 int qt_norm_squared(qt_state* st, double* outp) {
   if (!st || !outp) return null_arg();
-  return guard([&] { *outp = st->s->norm_squared(); });
+  return guard_collective(st, [&] { *outp = st->s->norm_squared(); });
 }
 
 int qt_sync(qt_state* st) {
@@ -259,6 +270,7 @@ int qt_plan_probe_ex(int num_qubits, int global_qubits, int tile_qubits, int det
     qtb::fuse_ops(ops, num_qubits);
     qtb::PlanOptions opt;
     if (tile_qubits > 0) opt.tile_bits = tile_qubits < qtb::kMaxTileBits ? tile_qubits : qtb::kMaxTileBits;
+    if (const char* e = std::getenv("QTB_VICTIM_SPAN")) opt.victim_span = std::atoi(e);
     std::vector<int> perm(num_qubits);
     for (int q = 0; q < num_qubits; ++q) perm[q] = q;
     const qtb::Plan p = qtb::make_plan(ops, num_qubits, num_qubits - global_qubits, perm, opt);
@@ -580,6 +592,7 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
     if (tile_qubits > 0) opt.tile_bits = std::min(tile_qubits, qtb::kMaxTileBits);
     if (low_bits > 0) opt.low_bits = low_bits;
     if (const char* e = std::getenv("QTB_PASS_FP64")) opt.max_pass_fp64 = std::atof(e);
+    if (const char* e = std::getenv("QTB_VICTIM_SPAN")) opt.victim_span = std::atoi(e);
     std::vector<int> perm(num_qubits);
     for (int q = 0; q < num_qubits; ++q) perm[q] = q;
     const qtb::Plan p = qtb::make_plan(ops, num_qubits, num_qubits, perm, opt);

@@ -9,6 +9,7 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 
@@ -168,7 +169,7 @@ LocalComm::LocalComm(std::shared_ptr<LocalGroup> g, int rank, int device) : g_(s
   world_ = g_->world();
   LocalGroup::Slot& me = g_->slots_[rank];
   me.device = device;
-  me.send_to.assign(world_, nullptr);
+  me.send_to.assign(world_, {});
   cudaEventCreateWithFlags(&me.ready, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&me.read, cudaEventDisableTiming);
 }
@@ -190,10 +191,15 @@ bool LocalComm::rendezvous(const std::vector<int>& peers, cudaStream_t s, Copy c
     seq = ++me.seq;
     g.cv_.notify_all();
     const bool ok = g.cv_.wait_for(lk, kRendezvousTimeout, [&] {
+      if (g.broken_) return true;
       for (int p : peers)
         if (g.slots_[p].seq < seq) return false;
       return true;
     });
+    if (g.broken_) {
+      if (err) *err = "local transport: a peer rank failed: " + g.why_;
+      return false;
+    }
     if (!ok) {
       if (err) *err = "local transport: a peer rank never reached the exchange";
       return false;
@@ -213,10 +219,15 @@ bool LocalComm::rendezvous(const std::vector<int>& peers, cudaStream_t s, Copy c
     me.read_seq = seq;
     g.cv_.notify_all();
     const bool ok = g.cv_.wait_for(lk, kRendezvousTimeout, [&] {
+      if (g.broken_) return true;
       for (int p : peers)
         if (g.slots_[p].read_seq < seq) return false;
       return true;
     });
+    if (g.broken_) {
+      if (err) *err = "local transport: a peer rank failed: " + g.why_;
+      return false;
+    }
     if (!ok) {
       if (err) *err = "local transport: a peer rank never finished the exchange";
       return false;
@@ -227,18 +238,34 @@ bool LocalComm::rendezvous(const std::vector<int>& peers, cudaStream_t s, Copy c
   return true;
 }
 
+void LocalComm::abort(const std::string& why) {
+  std::lock_guard<std::mutex> lk(g_->mu_);
+  if (!g_->broken_) {
+    g_->broken_ = true;
+    g_->why_ = "rank " + std::to_string(rank_) + ": " + why;
+  }
+  g_->cv_.notify_all();
+}
+
 bool LocalComm::sendrecv(int npeers, const int* peers, const void* const* sends,
                          void* const* recvs, size_t bytes, cudaStream_t s, std::string* err) {
   LocalGroup::Slot& me = g_->slots_[rank_];
-  std::vector<int> pv(peers, peers + npeers);
+  std::vector<int> pv;
   {
     std::lock_guard<std::mutex> lk(g_->mu_);
-    for (int i = 0; i < npeers; ++i) me.send_to[peers[i]] = sends[i];
+    for (auto& v : me.send_to) v.clear();
+    for (int i = 0; i < npeers; ++i) {
+      me.send_to[peers[i]].push_back(sends[i]);
+      if (std::find(pv.begin(), pv.end(), peers[i]) == pv.end()) pv.push_back(peers[i]);
+    }
   }
   return rendezvous(pv, s, [&] {
+    std::vector<size_t> next(world_, 0);
     for (int i = 0; i < npeers; ++i) {
-      const void* src = g_->slots_[peers[i]].send_to[rank_];
-      if (cudaMemcpyAsync(recvs[i], src, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+      const std::vector<const void*>& from = g_->slots_[peers[i]].send_to[rank_];
+      const size_t j = next[peers[i]]++;
+      if (j >= from.size()) return false;  // the peer sends fewer pieces
+      if (cudaMemcpyAsync(recvs[i], from[j], bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return false;
     }
     return true;

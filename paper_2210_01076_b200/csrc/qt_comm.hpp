@@ -31,7 +31,8 @@ class Comm {
   int rank() const { return rank_; }
   int world() const { return world_; }
   // Grouped point-to-point: sends[i] (bytes) to peers[i] and receives the
-  // same byte count from peers[i] into recvs[i], as one group: on return
+  // same byte count from peers[i] into recvs[i], as one group (a peer may
+  // appear several times: its sends and receives match in order): on return
   // (stream order) every receive has landed and every send buffer may be
   // overwritten.
   virtual bool sendrecv(int npeers, const int* peers, const void* const* sends,
@@ -42,6 +43,9 @@ class Comm {
                                 std::string* err) = 0;
   virtual bool check_async(std::string* err) = 0;
   virtual const char* kind() const = 0;
+  // This rank failed mid-call: release peers waiting on it (in-process
+  // group) instead of letting them time out.
+  virtual void abort(const std::string& why) {}
 
  protected:
   int rank_ = 0, world_ = 1;
@@ -81,13 +85,15 @@ class LocalGroup {
   struct Slot {
     uint64_t seq = 0;        // calls posted by this rank (sendrecv or allgather)
     uint64_t read_seq = 0;   // calls whose reads this rank has issued
-    std::vector<const void*> send_to;  // per destination rank (this call)
+    std::vector<std::vector<const void*>> send_to;  // per destination rank, in order (this call)
     const double* gather_src = nullptr;
     cudaEvent_t ready = nullptr;  // the rank's stream reached the call
     cudaEvent_t read = nullptr;   // the rank's reads of its peers are issued
     int device = -1;
   };
   int world_;
+  bool broken_ = false;
+  std::string why_;
   std::mutex mu_;
   std::condition_variable cv_;
   std::vector<Slot> slots_;
@@ -103,6 +109,7 @@ class LocalComm : public Comm {
                         std::string* err) override;
   bool check_async(std::string*) override { return true; }
   const char* kind() const override { return "local"; }
+  void abort(const std::string& why) override;
 
  private:
   // posts this rank's call, waits until `peers` posted the same call, makes

@@ -281,6 +281,30 @@ cudaError_t launch_norm(const double2* psi, uint64_t n, double* scratch,
   return cudaGetLastError();
 }
 
+// dst[off(r) + i] = src[off(r) + i] for the runs r of an exchange's own
+// region: off(r) = pdep(r, above) | vpat, run length 2^run_bits amplitudes
+// (16-B vector copies, one grid-stride loop over all amplitudes).
+__global__ void copy_runs_kernel(double2* __restrict__ dst, const double2* __restrict__ src,
+                                 uint64_t above, uint64_t vpat, int run_bits, uint64_t total) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t lo = (1ull << run_bits) - 1;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    uint64_t r = i >> run_bits, off = 0;
+    for (uint64_t m = above; m; m &= m - 1) {
+      if (r & 1) off |= m & (~m + 1);
+      r >>= 1;
+    }
+    const uint64_t j = off | vpat | (i & lo);
+    dst[j] = __ldcs(src + j);
+  }
+}
+
+cudaError_t launch_copy_runs(double2* dst, const double2* src, uint64_t above, uint64_t vpat,
+                             int run_bits, uint64_t total, cudaStream_t s) {
+  copy_runs_kernel<<<grid_for(total, 256), 256, 0, s>>>(dst, src, above, vpat, run_bits, total);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bitswap(double2* psi, int nbits, int b1, int b2,
                            cudaStream_t s) {
   if (b1 > b2) {

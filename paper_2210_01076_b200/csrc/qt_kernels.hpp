@@ -81,6 +81,10 @@ constexpr int kNormBlocks = 1184;  // 8 x 148 SMs
 cudaError_t launch_norm(const double2* psi, uint64_t n, double* scratch,
                         double* out, cudaStream_t s);
 // Swaps physical index bits b1 < b2 of a 2^nbits vector in place.
+// Copies the runs of an exchange's own region (State::exchange, two-buffer
+// scheme): offsets pdep(r, above) | vpat, 2^run_bits amplitudes each.
+cudaError_t launch_copy_runs(double2* dst, const double2* src, uint64_t above, uint64_t vpat,
+                             int run_bits, uint64_t total, cudaStream_t s);
 cudaError_t launch_bitswap(double2* psi, int nbits, int b1, int b2,
                            cudaStream_t s);
 // out[i] = psi[phys(first + i)] where phys permutes logical index bits by

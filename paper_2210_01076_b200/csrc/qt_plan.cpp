@@ -880,8 +880,14 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
       // at most g globals per exchange, and no more than there are local
       // victim bits (shards of fewer bits than the rank bits)
       if (static_cast<int>(need_g.size()) > std::min(g, nlocal)) need_g.resize(std::min(g, nlocal));
-      // victims: among the top local bits, the furthest next X use first
-      const int ncand = std::min(nlocal, std::max(4, static_cast<int>(need_g.size())));
+      // victims: among the top local bits, the furthest next X use first.
+      // The candidates reach down to kVictimSpan bits below the top (runs of
+      // >= 2^(nlocal - kVictimSpan) amplitudes per exchange step): with only
+      // the top few bits as candidates, the qubits swapped out are needed
+      // again soon and swapped straight back (C4 at 8 shards: 20 exchanges
+      // instead of 12).
+      const int ncand = std::min(nlocal, std::max({4, static_cast<int>(need_g.size()),
+                                                   std::min(nlocal, opt.victim_span)}));
       std::vector<int> cand;
       for (int p = nlocal - 1; p >= nlocal - ncand; --p) cand.push_back(p);
       std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) {

@@ -23,6 +23,9 @@ struct PlanOptions {
   // non-diagonal op counts ~3 (scaled rotation + its share of a table).
   // Balances FP64-heavy passes against HBM-bound ones (QTB_PASS_FP64).
   double max_pass_fp64 = 0.0;
+  // exchanges pick their local victim bits among the top victim_span local
+  // bits (QTB_VICTIM_SPAN)
+  int victim_span = 10;
 };
 
 // Cost model of the compiled-mode plan search (qt_state.cpp State::plan):

@@ -19,6 +19,7 @@
 #include <functional>
 #include <atomic>
 #include <cmath>
+#include <mutex>
 #include <thread>
 
 #include "qt_gates.hpp"
@@ -101,7 +102,9 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   }
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PASS_FP64")) opt_.max_pass_fp64 = std::atof(e);
+  if (const char* e = std::getenv("QTB_VICTIM_SPAN")) opt_.victim_span = std::atoi(e);
   if (const char* e = std::getenv("QTB_PLAN_SEARCH")) plan_search_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("QTB_EXCHANGE_TMP")) no_alt_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_JIT_MINB")) jit_min_blocks_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_DIRECT_BITS")) direct_bits_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PIPE")) pipe_ = std::atoi(e) != 0;
@@ -141,6 +144,7 @@ State::~State() {
   cudaSetDevice(device_);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto& kv : ckpt_) cudaFree(kv.second.first);
+  if (alt_) cudaFree(alt_);
   for (auto& t : timings_) {
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.stop);
@@ -734,23 +738,59 @@ std::vector<ExchangeStep> exchange_schedule(int rank, int nlocal,
     peers.push_back(pr);
     vbase.push_back(vb);
   }
+  // m consecutive pieces per peer per step (one NCCL group of npeer * m
+  // send / receive pairs, matched in issue order), so low victim bits
+  // (short runs) do not multiply the number of groups
+  const uint64_t total = runs * per_run;
+  const uint64_t m = std::max<uint64_t>(1, std::min<uint64_t>(total, tmp_amps / (piece * npeer)));
   std::vector<ExchangeStep> steps;
-  steps.reserve(runs * per_run);
-  for (uint64_t r = 0; r < runs; ++r) {
-    const uint64_t run_base = pdep(r, above);
-    for (uint64_t w = 0; w < per_run; ++w) {
-      ExchangeStep st;
-      st.piece = piece;
-      for (int i = 0; i < npeer; ++i) {
+  steps.reserve((total + m - 1) / m);
+  for (uint64_t p0 = 0; p0 < total; p0 += m) {
+    ExchangeStep st;
+    st.piece = piece;
+    const uint64_t p1 = std::min(total, p0 + m);
+    for (int i = 0; i < npeer; ++i) {
+      for (uint64_t p = p0; p < p1; ++p) {
+        const uint64_t run_base = pdep(p / per_run, above);
         st.peer.push_back(peers[i]);
-        st.send_off.push_back((run_base | vbase[i]) + w * piece);
-        st.recv_off.push_back(static_cast<uint64_t>(i) * piece);
+        st.send_off.push_back((run_base | vbase[i]) + (p % per_run) * piece);
+        st.recv_off.push_back((static_cast<uint64_t>(i) * m + (p - p0)) * piece);
       }
-      steps.push_back(std::move(st));
     }
+    steps.push_back(std::move(st));
   }
   return steps;
 }
+
+namespace {
+
+// The exchange's victim bits: this rank keeps the region whose victim-bit
+// pattern equals its own global bits; it is made of runs of 2^minv
+// amplitudes (minv = the lowest victim bit).
+int min_victim(int nlocal, const std::vector<std::pair<int, int>>& ex) {
+  int m = nlocal;
+  for (const auto& gv : ex) m = std::min(m, gv.second);
+  return m;
+}
+
+// this rank's own region of an exchange: the amplitudes whose victim bits
+// equal its global bits -- runs of 2^min_victim amplitudes at offsets
+// pdep(r, above) | vpat
+void own_region(int rank, int nlocal, const std::vector<std::pair<int, int>>& ex,
+                uint64_t* above, uint64_t* vpat) {
+  const int minv = min_victim(nlocal, ex);
+  uint64_t vmask = 0;
+  *vpat = 0;
+  for (const auto& gv : ex) {
+    vmask |= 1ull << gv.second;
+    if ((rank >> (gv.first - nlocal)) & 1) *vpat |= 1ull << gv.second;
+  }
+  *above = 0;
+  for (int b = minv; b < nlocal; ++b)
+    if (!((vmask >> b) & 1)) *above |= 1ull << b;
+}
+
+}  // namespace
 
 void State::exchange(const PlanPass& pass) {
   if (mode_ == Mode::Loopback) {
@@ -762,42 +802,84 @@ void State::exchange(const PlanPass& pass) {
   }
   if (mode_ != Mode::Sharded) fail(QT_ERR_ARG, "exchange on an unsharded state");
   const int k = static_cast<int>(pass.exchange.size());
-  // receive buffer: at most 1/8 of the shard, split across the peers
-  uint64_t want = std::max<uint64_t>(1, (1ull << nlocal_) / 8);
-  want = std::min<uint64_t>(want, 1ull << 27);  // 2 GiB
-  // every step receives at least one amplitude from each of the 2^k - 1
-  // peers (small shards: 1/8 of the shard can be less than that)
-  want = std::max<uint64_t>(want, (1ull << k) - 1);
-  if (d_tmp_amps_ < want) {
+  const int npeer = (1 << k) - 1;
+  const uint64_t region = 1ull << (nlocal_ - k);
+  // The step structure (piece size, offsets) depends only on the shard
+  // geometry, never on this rank's buffer scheme: every rank of the group
+  // must make the same sequence of grouped send/recv calls. At most 1/8 of
+  // the shard (<= 2 GiB) is in flight per step, at least one amplitude per
+  // peer.
+  uint64_t cap = std::max<uint64_t>(1, (1ull << nlocal_) / 8);
+  cap = std::min<uint64_t>(cap, 1ull << 27);
+  cap = std::max<uint64_t>(cap, static_cast<uint64_t>(npeer));
+  const std::vector<ExchangeStep> steps = exchange_schedule(rank_, nlocal_, pass.exchange, cap);
+  // Two-buffer exchange (when a second shard fits in HBM): every peer's
+  // piece is received straight into its final place in the second buffer,
+  // this rank's own region is copied over with one device copy, and the
+  // buffers swap roles -- the only HBM traffic beyond the transfer itself is
+  // that 1/2^k of the shard (the receive-buffer scheme below copies the other
+  // (2^k-1)/2^k back out of the receive buffer).
+  if (!alt_ && !alt_tried_ && bound_ == 0) {
+    // one decision at a time per process (emulated ranks share a device)
+    static std::mutex alloc_mu;
+    std::lock_guard<std::mutex> lk(alloc_mu);
+    alt_tried_ = true;
+    size_t fr = 0, tot = 0;
+    const size_t bytes = sizeof(double2) << nlocal_;
+    if (!no_alt_ && cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > bytes + (size_t(4) << 30)) {
+      if (cudaMalloc(&alt_, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        alt_ = nullptr;
+      }
+    }
+  }
+  const bool two = alt_ && bound_ == 0;
+  if (!two && d_tmp_amps_ < cap) {
+    static std::mutex alloc_mu2;
+    std::lock_guard<std::mutex> lk(alloc_mu2);
     cuda_check(cudaStreamSynchronize(stream_), "sync");
     cudaFree(d_tmp_);
     d_tmp_ = nullptr;
-    d_tmp_amps_ = want;
+    d_tmp_amps_ = cap;
     cuda_check(cudaMalloc(&d_tmp_, d_tmp_amps_ * sizeof(double2)), "exchange buffer");
   }
-  const std::vector<ExchangeStep> steps =
-      exchange_schedule(rank_, nlocal_, pass.exchange, d_tmp_amps_);
-  const int npeer = (1 << k) - 1;
-  std::vector<const void*> sends(npeer);
-  std::vector<void*> recvs(npeer);
-  std::vector<int> peers(npeer);
   std::string err;
+  std::vector<const void*> sends;
+  std::vector<void*> recvs;
+  std::vector<int> peers;
   for (const ExchangeStep& st : steps) {
-    for (int i = 0; i < npeer; ++i) {
+    const size_t ne = st.peer.size();
+    sends.resize(ne);
+    recvs.resize(ne);
+    peers.resize(ne);
+    for (size_t i = 0; i < ne; ++i) {
       peers[i] = st.peer[i];
       sends[i] = psi_ + st.send_off[i];
-      recvs[i] = d_tmp_ + st.recv_off[i];
+      recvs[i] = two ? alt_ + st.send_off[i] : d_tmp_ + st.recv_off[i];
     }
-    if (!comm_->sendrecv(npeer, peers.data(), sends.data(), recvs.data(),
+    if (!comm_->sendrecv(static_cast<int>(ne), peers.data(), sends.data(), recvs.data(),
                          st.piece * sizeof(double2), stream_, &err))
       fail(QT_ERR_NCCL, err);
-    for (int i = 0; i < npeer; ++i)
-      cuda_check(cudaMemcpyAsync(const_cast<void*>(sends[i]), recvs[i],
-                                 st.piece * sizeof(double2), cudaMemcpyDeviceToDevice, stream_),
-                 "exchange copy");
+    if (!two)
+      for (size_t i = 0; i < ne; ++i)
+        cuda_check(cudaMemcpyAsync(const_cast<void*>(sends[i]), recvs[i],
+                                   st.piece * sizeof(double2), cudaMemcpyDeviceToDevice, stream_),
+                   "exchange copy");
   }
-  const uint64_t region = 1ull << (nlocal_ - k);
   stats.exchanged_bytes += static_cast<uint64_t>(npeer) * region * sizeof(double2);
+  if (two) {
+    // this rank's own region: the victim bits equal its global bits
+    uint64_t above = 0, vpat = 0;
+    own_region(rank_, nlocal_, pass.exchange, &above, &vpat);
+    cuda_check(launch_copy_runs(alt_, psi_, above, vpat, min_victim(nlocal_, pass.exchange), region,
+                                stream_),
+               "exchange own region");
+    std::swap(psi_, alt_);
+    pool_[0] = psi_;
+    stats.exchange_local_bytes += 2ull * region * sizeof(double2);
+  } else {
+    stats.exchange_local_bytes += 2ull * npeer * region * sizeof(double2);
+  }
 }
 
 // Top-K readout (the reference's amplitude report, qtask_cli.cpp:53-86:

@@ -35,10 +35,12 @@ struct PassTiming {
   int kind = 0;  // 0 tile, 1 exchange
 };
 
-// One grouped send/recv step of a sharded exchange (State::exchange): with
-// each peer[i], send `piece` amplitudes at shard offset send_off[i] and
-// receive as many into the exchange buffer at recv_off[i], then copy them
-// back over send_off[i].
+// One grouped send/recv step of a sharded exchange (State::exchange): for
+// each entry i, send `piece` amplitudes at shard offset send_off[i] to
+// peer[i] and receive as many from peer[i] into the exchange buffer at
+// recv_off[i], then copy them back over send_off[i] (or, two-buffer scheme,
+// receive straight into the second buffer at send_off[i]). A peer can appear
+// in several entries of a step; its sends and receives match in order.
 struct ExchangeStep {
   uint64_t piece = 0;
   std::vector<int> peer;
@@ -89,6 +91,10 @@ class State {
   // sorted; logical indices. Single / loopback states (State::top_k).
   std::vector<TopkItem> top_k(uint64_t k);
   void sync();  // also raises QT_ERR_NUMERIC if a pass saw a non-finite value
+  // a call on this rank failed: release the group's other ranks
+  void abort_comm(const std::string& why) {
+    if (comm_) comm_->abort(why);
+  }
 
   void checkpoint_save(int slot);
   void checkpoint_restore(int slot);
@@ -157,6 +163,9 @@ class State {
   // kernel-parameter blocks (ops travel in the launch's constant bank)
   std::unique_ptr<KPassSmall> kp_small_;
   std::unique_ptr<KPassLarge> kp_large_;
+  double2* alt_ = nullptr;        // second shard buffer of the two-buffer exchange
+  bool alt_tried_ = false;
+  bool no_alt_ = false;           // QTB_EXCHANGE_TMP=1: always the receive-buffer scheme
   double2* d_tmp_ = nullptr;      // exchange receive buffer
   size_t d_tmp_amps_ = 0;
   std::vector<int> perm_;         // logical -> physical

@@ -197,9 +197,12 @@ class RankGroup:
             t.start()
         for t in th:
             t.join()
-        for e in errs:
-            if e is not None:
-                raise e
+        # the root cause first: a rank whose peers failed reports "a peer
+        # rank failed: ..." (in-process transport), so prefer another error
+        first = [e for e in errs if e is not None]
+        root = [e for e in first if "peer rank failed" not in str(e)]
+        if first:
+            raise (root or first)[0]
         return out
 
     def set_basis(self, index: int = 0):

@@ -46,12 +46,27 @@ def test_c4_family_n26_vs_oracle(gpu, world):
     assert len({s["exchanged_bytes"] for s in stats}) == 1
 
 
-@pytest.mark.parametrize("world", [2, 8])
-def test_group_bitwise_equals_loopback(gpu, world):
+@pytest.mark.parametrize("world,scheme", [(2, "two"), (8, "two"), (4, "tmp"), (8, "tmp")])
+def test_group_bitwise_equals_loopback(gpu, world, scheme, monkeypatch):
     """Same plan, same per-amplitude operations: the group's rank-offset
-    kernels + transport must give exactly the loopback shards' state."""
+    kernels + transport must give exactly the loopback shards' state, with
+    either exchange scheme (two-buffer, or receive buffer + copy back:
+    QTB_EXCHANGE_TMP=1)."""
+    if scheme == "tmp":
+        monkeypatch.setenv("QTB_EXCHANGE_TMP", "1")
     w = W.config4(n=22, ngates=600)
-    got, nrm, _ = run_group(w.n, w.gates, world)
+    got, nrm, stats = run_group(w.n, w.gates, world)
+    # local HBM copy traffic of the exchanges: the own region only (two) or
+    # every received region copied back (tmp)
+    k_sent = stats[0]["exchanged_bytes"]
+    if scheme == "two":
+        # 2 x own region per exchange: a 1/(2^k - 1) share of what was sent
+        if world == 2:
+            assert stats[0]["exchange_local_bytes"] == 2 * k_sent
+        else:
+            assert stats[0]["exchange_local_bytes"] < 2 * k_sent
+    else:
+        assert stats[0]["exchange_local_bytes"] == 2 * k_sent
     lb = StateVector(w.n, mode="loopback", shards=world)
     lb.apply(w.gates)
     want = lb.read()
