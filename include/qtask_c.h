@@ -94,7 +94,11 @@ typedef struct qt_config {
                                 0 = interpreter. qt_sim: 0 = hybrid (its
                                 re-simulated segments repeat), -1 =
                                 interpreter only                            */
-  int32_t reserved[2];
+  int32_t partition_model;   /* qt_sim: the reference-unit partition model
+                                (UpdateStats in partitions / blocks, stage
+                                views, graph): 0 = auto (states of <= 4096
+                                partition blocks), 1 = on, -1 = off         */
+  int32_t reserved;
 } qt_config;
 
 /* Result of the last qt_apply / update (UpdateStats, engine.hpp:32-39, in
@@ -265,6 +269,74 @@ int qt_sim_gate_info(const qt_sim* sim, uint32_t gate, qt_gate* out,
                      uint32_t* net);
 int qt_sim_export_gates(const qt_sim* sim, qt_gate* out, size_t cap,
                         size_t* count);
+
+/* ---- reference-unit partition model (qt_config.partition_model) ----------
+ * The reference's partition DAG restated on the host from the modifier
+ * stream (csrc/qt_partition.hpp): UpdateStats in partition / block units
+ * (engine.hpp:32-39) and the introspection members (engine.hpp:77-100).
+ * valid = 0 when the model is off for this simulator. */
+typedef struct qt_update_account {
+  int32_t valid;
+  int32_t full;
+  uint64_t executed_partitions;
+  uint64_t materialized_blocks;
+  uint64_t rewritten_amplitudes;
+  uint64_t rewritten_block_count;
+} qt_update_account;
+/* The last update's accounting; up to `cap` rewritten block indices (sorted)
+ * into `blocks` (may be NULL). */
+int qt_sim_update_account(qt_sim* sim, qt_update_account* out, uint64_t* blocks, size_t cap);
+
+typedef struct qt_model_stage {
+  uint32_t id, net, gate;
+  int32_t kind;          /* 0 Sync, 1 MatrixVector, 2 PermuteScale */
+  uint64_t first_part;   /* into the partition array */
+  uint64_t num_parts;
+} qt_model_stage;
+typedef struct qt_model_part {
+  uint64_t first_block, last_block;  /* inclusive */
+  uint64_t node;                     /* graph node id */
+  uint64_t first_task, num_tasks;    /* into the task array */
+} qt_model_part;
+typedef struct qt_model_task {
+  uint64_t first_op, last_op, region_lo, region_hi;  /* inclusive */
+} qt_model_task;
+typedef struct qt_model_sizes {
+  int32_t valid;
+  int32_t reserved;
+  uint64_t stages, parts, tasks, edges, blocks, frontiers;
+} qt_model_sizes;
+/* Snapshot of the model: stages in execution order, their partitions and
+ * tasks, the graph's edges as (from, to) node pairs sorted, each stage's
+ * materialised blocks (stages x blocks bytes, row-major) and the frontier
+ * nodes. Call with NULL arrays for the sizes, then with arrays that large. */
+int qt_sim_model_snapshot(qt_sim* sim, qt_model_sizes* sizes, qt_model_stage* stages,
+                          qt_model_part* parts, qt_model_task* tasks, uint64_t* edges,
+                          uint8_t* materialized, uint64_t* frontiers);
+/* Reference node names (engine.cpp:570-586) and the DOT dump (graph.cpp:
+ * 302-327); two-call pattern on `needed`. */
+int qt_sim_node_name(qt_sim* sim, uint64_t node, char* buf, size_t cap, size_t* needed);
+int qt_sim_dump_graph(qt_sim* sim, char* buf, size_t cap, size_t* needed);
+/* The reference gate database (gate.cpp:42-106): the dense matrix (dim 2 or
+ * 4, row-major, interleaved re/im into m[2*dim*dim]) and the classification
+ * (1 = superposition). */
+int qt_gate_matrix(int kind, double theta, double phi, double lambda, double* m, int* dim);
+int qt_classify_gate(int kind, double theta, double phi, double lambda);
+
+/* Host-only handle on the partition model alone (no device): the same
+ * restatement qt_sim runs, driven directly with modifier events whose ids
+ * and validity the caller guarantees -- for differential tests against the
+ * reference engine. where: 0 = front, 1 = back, 2 = after `after`. */
+typedef struct qt_pm qt_pm;
+int qt_pm_create(int num_qubits, uint64_t block_size, qt_pm** out);
+int qt_pm_destroy(qt_pm* pm);
+int qt_pm_insert_net(qt_pm* pm, uint32_t net, int where, uint32_t after);
+int qt_pm_remove_net(qt_pm* pm, uint32_t net);
+int qt_pm_insert_gate(qt_pm* pm, uint32_t gate, const qt_gate* g, uint32_t net);
+int qt_pm_remove_gate(qt_pm* pm, uint32_t gate);
+int qt_pm_update(qt_pm* pm);
+int qt_pm_account(qt_pm* pm, qt_update_account* out, uint64_t* blocks, size_t cap);
+int qt_pm_dump_graph(qt_pm* pm, char* buf, size_t cap, size_t* needed);
 
 /* Host-only audit of a sharded exchange (State::exchange): the grouped
  * send/recv steps `rank` performs to swap the k global rank bits gbit[j]

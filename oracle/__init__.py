@@ -99,6 +99,10 @@ def ref_lib():
         lib.ref_sim_norm.argtypes = [ctypes.c_void_p]
         lib.ref_sim_norm.restype = ctypes.c_double
         lib.ref_sim_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        lib.ref_sim_dump.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_size_t]
+        lib.ref_sim_dump.restype = ctypes.c_size_t
+        lib.ref_sim_rewritten_blocks.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+        lib.ref_sim_rewritten_blocks.restype = ctypes.c_size_t
         lib.ref_qasm_parse.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_size_t,
                                        ctypes.POINTER(ctypes.c_uint32),
@@ -253,5 +257,15 @@ class RefSimulator:
     def stats(self):
         out = np.zeros(4, dtype=np.uint64)
         self.lib.ref_sim_stats(self.h, out.ctypes.data)
+        n = self.lib.ref_sim_rewritten_blocks(self.h, None, 0)
+        blocks = np.zeros(max(1, n), dtype=np.uint64)
+        self.lib.ref_sim_rewritten_blocks(self.h, blocks.ctypes.data, n)
         return dict(full=bool(out[0]), executed_partitions=int(out[1]),
-                    materialized_blocks=int(out[2]), rewritten_amplitudes=int(out[3]))
+                    materialized_blocks=int(out[2]), rewritten_amplitudes=int(out[3]),
+                    rewritten_blocks=[int(b) for b in blocks[:n]])
+
+    def dump_graph(self) -> str:
+        need = self.lib.ref_sim_dump(self.h, None, 0)
+        buf = ctypes.create_string_buffer(need)
+        self.lib.ref_sim_dump(self.h, buf, need)
+        return buf.value.decode()

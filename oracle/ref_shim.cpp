@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <vector>
 
@@ -227,6 +228,28 @@ void ref_sim_stats(void* s, uint64_t* out4) {
   out4[1] = st.executed_partitions;
   out4[2] = st.materialized_blocks;
   out4[3] = st.rewritten_amplitudes;
+}
+
+// The reference's partition graph as DOT text (engine.cpp dump_graph) and
+// the last update's rewritten blocks: the checker for the drop-in's host
+// partition model (tests/test_partition_model.py). Returns the text length
+// (+1); copies at most cap bytes.
+size_t ref_sim_dump(void* s, char* buf, size_t cap) {
+  std::ostringstream os;
+  static_cast<qtask::Simulator*>(s)->dump_graph(os);
+  const std::string t = os.str();
+  if (buf && cap) {
+    const size_t n = t.size() < cap - 1 ? t.size() : cap - 1;
+    std::memcpy(buf, t.data(), n);
+    buf[n] = 0;
+  }
+  return t.size() + 1;
+}
+
+size_t ref_sim_rewritten_blocks(void* s, uint64_t* out, size_t cap) {
+  const auto& b = static_cast<qtask::Simulator*>(s)->last_update().rewritten_blocks;
+  for (size_t i = 0; i < b.size() && i < cap; ++i) out[i] = b[i];
+  return b.size();
 }
 
 // ---- the reference OpenQASM front end -------------------------------------

@@ -25,13 +25,21 @@ GATE_DTYPE = np.dtype(
 assert GATE_DTYPE.itemsize == 40
 
 
+class QtUpdateAccount(ctypes.Structure):
+    """qt_update_account: UpdateStats in the reference's units (partition
+    model, csrc/qt_partition.hpp)."""
+    _fields_ = [("valid", ctypes.c_int32), ("full", ctypes.c_int32),
+                ("executed_partitions", ctypes.c_uint64), ("materialized_blocks", ctypes.c_uint64),
+                ("rewritten_amplitudes", ctypes.c_uint64), ("rewritten_block_count", ctypes.c_uint64)]
+
+
 class QtConfig(ctypes.Structure):
     _fields_ = [("block_size", ctypes.c_uint64), ("threads", ctypes.c_uint32),
                 ("device", ctypes.c_int32), ("tile_qubits", ctypes.c_int32),
                 ("max_checkpoints", ctypes.c_int32),
                 ("checkpoint_fraction", ctypes.c_double),
                 ("segment_gates", ctypes.c_int32), ("compiled", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("partition_model", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class QtRunStats(ctypes.Structure):
@@ -65,6 +73,10 @@ HEADER_SYMBOLS = [
     "qt_sim_num_gates", "qt_sim_num_nets", "qt_sim_net_order", "qt_sim_net_gates",
     "qt_sim_gate_info", "qt_sim_export_gates", "qt_qasm_parse", "qt_qasm_build",
     "qt_exchange_schedule", "qt_top_k", "qt_sim_top_k",
+    "qt_sim_update_account", "qt_sim_model_snapshot", "qt_sim_node_name", "qt_sim_dump_graph",
+    "qt_gate_matrix", "qt_classify_gate",
+    "qt_pm_create", "qt_pm_destroy", "qt_pm_insert_net", "qt_pm_remove_net", "qt_pm_insert_gate",
+    "qt_pm_remove_gate", "qt_pm_update", "qt_pm_account", "qt_pm_dump_graph",
 ]
 
 _lib = None
@@ -83,6 +95,20 @@ _SIGS = {
     "qt_group_destroy": ([_vp], _c.c_int),
     "qt_state_create_group": ([_c.c_int, _vp, _c.c_int, _vp, _c.POINTER(_vp)], _c.c_int),
     "qt_nccl_unique_id": ([_vp], _c.c_int),
+    "qt_pm_create": ([_c.c_int, _c.c_uint64, _c.POINTER(_vp)], _c.c_int),
+    "qt_pm_destroy": ([_vp], _c.c_int),
+    "qt_pm_insert_net": ([_vp, _c.c_uint32, _c.c_int, _c.c_uint32], _c.c_int),
+    "qt_pm_remove_net": ([_vp, _c.c_uint32], _c.c_int),
+    "qt_pm_insert_gate": ([_vp, _c.c_uint32, _vp, _c.c_uint32], _c.c_int),
+    "qt_pm_remove_gate": ([_vp, _c.c_uint32], _c.c_int),
+    "qt_pm_update": ([_vp], _c.c_int),
+    "qt_pm_account": ([_vp, _vp, _vp, _c.c_size_t], _c.c_int),
+    "qt_pm_dump_graph": ([_vp, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
+    "qt_sim_update_account": ([_vp, _vp, _vp, _c.c_size_t], _c.c_int),
+    "qt_sim_dump_graph": ([_vp, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
+    "qt_sim_node_name": ([_vp, _c.c_uint64, _c.c_char_p, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
+    "qt_gate_matrix": ([_c.c_int, _c.c_double, _c.c_double, _c.c_double, _vp, _c.POINTER(_c.c_int)], _c.c_int),
+    "qt_classify_gate": ([_c.c_int, _c.c_double, _c.c_double, _c.c_double], _c.c_int),
     "qt_state_destroy": ([_vp], _c.c_int),
     "qt_state_num_qubits": ([_vp], _c.c_int),
     "qt_set_basis": ([_vp, _c.c_uint64], _c.c_int),
@@ -173,7 +199,8 @@ def check(rc: int) -> int:
 
 
 def make_config(block_size=256, threads=0, device=-1, tile_qubits=0, max_checkpoints=0,
-                checkpoint_fraction=0.0, segment_gates=0, compiled=False) -> QtConfig:
+                checkpoint_fraction=0.0, segment_gates=0, compiled=False,
+                partition_model=0) -> QtConfig:
     cfg = QtConfig()
     cfg.block_size = block_size
     cfg.threads = threads
@@ -183,6 +210,7 @@ def make_config(block_size=256, threads=0, device=-1, tile_qubits=0, max_checkpo
     cfg.checkpoint_fraction = checkpoint_fraction
     cfg.segment_gates = segment_gates
     cfg.compiled = int(compiled) if not isinstance(compiled, bool) else (1 if compiled else 0)
+    cfg.partition_model = partition_model
     return cfg
 
 

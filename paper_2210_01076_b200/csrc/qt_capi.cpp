@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <sstream>
 #include <string>
 
 #include "qt_gates.hpp"
@@ -419,6 +420,197 @@ int qt_sim_last_update(const qt_sim* sim, qt_run_stats* outp) {
   if (!sim || !outp) return null_arg();
   *outp = sim->s->last_update();
   return QT_OK;
+}
+
+int qt_sim_update_account(qt_sim* sim, qt_update_account* out, uint64_t* blocks, size_t cap) {
+  if (!sim || !out) return null_arg();
+  return guard([&] {
+    *out = qt_update_account{};
+    std::unique_lock<std::mutex> lk;
+    const qtb::PartitionModel* m = sim->s->model(&lk);
+    if (!m) return;
+    const qtb::PmAccount& a = m->account();
+    out->valid = 1;
+    out->full = a.full ? 1 : 0;
+    out->executed_partitions = a.executed_partitions;
+    out->materialized_blocks = a.materialized_blocks;
+    out->rewritten_amplitudes = a.rewritten_amplitudes;
+    out->rewritten_block_count = a.rewritten_blocks.size();
+    if (blocks)
+      for (size_t i = 0; i < a.rewritten_blocks.size() && i < cap; ++i) blocks[i] = a.rewritten_blocks[i];
+  });
+}
+
+int qt_sim_model_snapshot(qt_sim* sim, qt_model_sizes* sizes, qt_model_stage* stages,
+                          qt_model_part* parts, qt_model_task* tasks, uint64_t* edges,
+                          uint8_t* materialized, uint64_t* frontiers) {
+  if (!sim || !sizes) return null_arg();
+  return guard([&] {
+    *sizes = qt_model_sizes{};
+    std::unique_lock<std::mutex> lk;
+    const qtb::PartitionModel* m = sim->s->model(&lk);
+    if (!m) return;
+    const auto views = m->stages();
+    const auto es = m->edges();
+    sizes->valid = 1;
+    sizes->stages = views.size();
+    sizes->blocks = m->num_blocks();
+    sizes->edges = es.size();
+    sizes->frontiers = m->frontiers().size();
+    uint64_t np = 0, nt = 0;
+    for (size_t si = 0; si < views.size(); ++si) {
+      const auto& v = views[si];
+      if (stages)
+        stages[si] = qt_model_stage{v.id, v.net, v.gate, static_cast<int32_t>(v.kind), np,
+                                    static_cast<uint64_t>(v.parts->size())};
+      for (size_t k = 0; k < v.parts->size(); ++k) {
+        const qtb::PmPart& p = (*v.parts)[k];
+        if (parts)
+          parts[np] = qt_model_part{p.first_block, p.last_block, (*v.nodes)[k], nt,
+                                    static_cast<uint64_t>(p.tasks.size())};
+        for (const qtb::PmTask& t : p.tasks) {
+          if (tasks) tasks[nt] = qt_model_task{t.first_op, t.last_op, t.lo, t.hi};
+          ++nt;
+        }
+        ++np;
+      }
+      if (materialized) {
+        uint8_t* row = materialized + si * m->num_blocks();
+        for (uint64_t b = 0; b < m->num_blocks(); ++b)
+          row[b] = v.materialized->empty() ? 0 : (*v.materialized)[b];
+      }
+    }
+    sizes->parts = np;
+    sizes->tasks = nt;
+    if (edges)
+      for (size_t i = 0; i < es.size(); ++i) {
+        edges[2 * i] = es[i].first;
+        edges[2 * i + 1] = es[i].second;
+      }
+    if (frontiers) {
+      size_t i = 0;
+      for (uint64_t f : m->frontiers()) frontiers[i++] = f;
+    }
+  });
+}
+
+int qt_sim_node_name(qt_sim* sim, uint64_t node, char* buf, size_t cap, size_t* needed) {
+  if (!sim) return null_arg();
+  return guard([&] {
+    std::unique_lock<std::mutex> lk;
+    const qtb::PartitionModel* m = sim->s->model(&lk);
+    if (!m) qtb::fail(QT_ERR_ARG, "the partition model is off for this simulator");
+    copy_out(m->node_name(node), buf, cap, needed);
+  });
+}
+
+int qt_sim_dump_graph(qt_sim* sim, char* buf, size_t cap, size_t* needed) {
+  if (!sim) return null_arg();
+  return guard([&] {
+    std::unique_lock<std::mutex> lk;
+    const qtb::PartitionModel* m = sim->s->model(&lk);
+    if (!m) qtb::fail(QT_ERR_ARG, "the partition model is off for this simulator");
+    std::ostringstream os;
+    m->dump_dot(os);
+    copy_out(os.str(), buf, cap, needed);
+  });
+}
+
+struct qt_pm {
+  qtb::PartitionModel m;
+};
+
+int qt_pm_create(int num_qubits, uint64_t block_size, qt_pm** out) {
+  if (!out) return null_arg();
+  return guard([&] {
+    if (num_qubits < 1 || num_qubits > 30) qtb::fail(QT_ERR_BAD_QUBIT, "qubit count must be in [1, 30]");
+    if (block_size < 2 || (block_size & (block_size - 1)) != 0)
+      qtb::fail(QT_ERR_ARG, "block size must be a power of two >= 2");
+    *out = new qt_pm{qtb::PartitionModel(num_qubits, block_size)};
+  });
+}
+int qt_pm_destroy(qt_pm* pm) {
+  delete pm;
+  return QT_OK;
+}
+int qt_pm_insert_net(qt_pm* pm, uint32_t net, int where, uint32_t after) {
+  if (!pm) return null_arg();
+  return guard([&] {
+    if (where == 1) pm->m.insert_net_back(net);
+    else pm->m.insert_net(net, where == 0 ? 0 : after);
+  });
+}
+int qt_pm_remove_net(qt_pm* pm, uint32_t net) {
+  if (!pm) return null_arg();
+  return guard([&] { pm->m.remove_net(net); });
+}
+int qt_pm_insert_gate(qt_pm* pm, uint32_t gate, const qt_gate* g, uint32_t net) {
+  if (!pm || !g) return null_arg();
+  return guard([&] { pm->m.insert_gate(gate, *g, net); });
+}
+int qt_pm_remove_gate(qt_pm* pm, uint32_t gate) {
+  if (!pm) return null_arg();
+  return guard([&] { pm->m.remove_gate(gate); });
+}
+int qt_pm_update(qt_pm* pm) {
+  if (!pm) return null_arg();
+  return guard([&] { pm->m.update(); });
+}
+int qt_pm_account(qt_pm* pm, qt_update_account* out, uint64_t* blocks, size_t cap) {
+  if (!pm || !out) return null_arg();
+  return guard([&] {
+    const qtb::PmAccount& a = pm->m.account();
+    *out = qt_update_account{};
+    out->valid = a.valid ? 1 : 0;
+    out->full = a.full ? 1 : 0;
+    out->executed_partitions = a.executed_partitions;
+    out->materialized_blocks = a.materialized_blocks;
+    out->rewritten_amplitudes = a.rewritten_amplitudes;
+    out->rewritten_block_count = a.rewritten_blocks.size();
+    if (blocks)
+      for (size_t i = 0; i < a.rewritten_blocks.size() && i < cap; ++i) blocks[i] = a.rewritten_blocks[i];
+  });
+}
+int qt_pm_dump_graph(qt_pm* pm, char* buf, size_t cap, size_t* needed) {
+  if (!pm) return null_arg();
+  return guard([&] {
+    std::ostringstream os;
+    pm->m.dump_dot(os);
+    copy_out(os.str(), buf, cap, needed);
+  });
+}
+
+int qt_gate_matrix(int kind, double theta, double phi, double lambda, double* m, int* dim) {
+  if (!m || !dim) return null_arg();
+  return guard([&] {
+    if (!qtb::valid_kind(kind)) qtb::fail(QT_ERR_ARG, "unknown gate kind");
+    if (qtb::is_two_qubit_kind(kind)) {
+      // 4x4 with the sub-index (first << 1) | second (gate.hpp:39-41)
+      for (int i = 0; i < 32; ++i) m[i] = 0.0;
+      auto set = [&](int r, int c) { m[2 * (r * 4 + c)] = 1.0; };
+      if (kind == QT_CNOT) { set(0, 0); set(1, 1); set(2, 3); set(3, 2); }
+      else if (kind == QT_SWAP) { set(0, 0); set(1, 2); set(2, 1); set(3, 3); }
+      else { set(0, 0); set(1, 1); set(2, 2); m[2 * 15] = -1.0; }
+      *dim = 4;
+      return;
+    }
+    const qtb::Mat2 g = kind == QT_U3 ? qtb::u3_matrix(theta, phi, lambda) : qtb::gate_matrix_1q(kind, theta);
+    for (int i = 0; i < 4; ++i) {
+      m[2 * i] = g[i].re;
+      m[2 * i + 1] = g[i].im;
+    }
+    *dim = 2;
+  });
+}
+
+int qt_classify_gate(int kind, double theta, double phi, double lambda) {
+  qt_gate g{};
+  g.kind = kind;
+  g.theta = theta;
+  g.phi = phi;
+  g.lambda = lambda;
+  if (!qtb::valid_kind(kind)) return QT_ERR_ARG;
+  return qtb::is_superposition_gate(g) ? 1 : 0;
 }
 
 size_t qt_sim_num_gates(const qt_sim* sim) { return sim ? sim->s->num_gates() : 0; }

@@ -16,7 +16,7 @@ namespace qtb {
 
 namespace {
 constexpr double kInvSqrt2 = 0.70710678118654752440084436210484903928;
-constexpr double kZeroThreshold = 1e-12;
+
 
 inline cplx mk(double re, double im) { return cplx{re, im}; }
 }  // namespace

@@ -12,6 +12,9 @@ namespace qtb {
 
 using Mat2 = std::array<cplx, 4>;
 
+// structural-zero threshold of the gate classification (gate.hpp:50-53)
+constexpr double kZeroThreshold = 1e-12;
+
 bool valid_kind(int kind);
 bool is_two_qubit_kind(int kind);
 bool is_rotation_kind(int kind);

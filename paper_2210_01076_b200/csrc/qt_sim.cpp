@@ -33,6 +33,9 @@
 namespace qtb {
 
 constexpr uint64_t kMinSegmentGates = 256;
+// the partition model runs (auto) for states of at most this many partition
+// blocks: its graph holds one node per block for every MxV stage
+constexpr uint64_t kModelMaxBlocks = 4096;
 constexpr size_t kSegmentPlanCache = 512;  // cached segment plans (cleared when full)
 
 Sim::Sim(int nqubits, const qt_config* cfg) : n_(nqubits) {
@@ -57,6 +60,69 @@ Sim::Sim(int nqubits, const qt_config* cfg) : n_(nqubits) {
   const double frac = cfg_.checkpoint_fraction > 0 ? cfg_.checkpoint_fraction : 0.85;
   nbuf_ = st_->grow_pool(want, frac);
   if (const char* e = std::getenv("QTB_SIM_TRACE")) trace_ = std::atoi(e) != 0;
+  const int pm = cfg_.partition_model;
+  if (pm > 0 || (pm == 0 && nblocks_ <= kModelMaxBlocks)) {
+    model_.reset(new PartitionModel(n_, cfg_.block_size));
+    model_thread_ = std::thread([this] { model_worker(); });
+  }
+}
+
+Sim::~Sim() {
+  if (model_thread_.joinable()) {
+    {
+      std::lock_guard<std::mutex> lk(q_mu_);
+      stop_ = true;
+    }
+    q_cv_.notify_all();
+    model_thread_.join();
+  }
+}
+
+void Sim::post(std::function<void(PartitionModel&)> ev) {
+  if (!model_) return;
+  {
+    std::lock_guard<std::mutex> lk(q_mu_);
+    events_.push_back(std::move(ev));
+  }
+  q_cv_.notify_one();
+}
+
+void Sim::model_worker() {
+  for (;;) {
+    std::function<void(PartitionModel&)> ev;
+    {
+      std::unique_lock<std::mutex> lk(q_mu_);
+      q_cv_.wait(lk, [&] { return stop_ || !events_.empty(); });
+      if (events_.empty()) return;  // stop_
+      ev = std::move(events_.front());
+      events_.pop_front();
+      busy_ = true;
+    }
+    {
+      std::lock_guard<std::mutex> mk(model_mu_);
+      try {
+        ev(*model_);
+      } catch (const std::exception& e) {
+        if (model_error_.empty()) model_error_ = e.what();
+      }
+    }
+    {
+      std::lock_guard<std::mutex> lk(q_mu_);
+      busy_ = false;
+    }
+    drained_cv_.notify_all();
+  }
+}
+
+const PartitionModel* Sim::model(std::unique_lock<std::mutex>* lk) {
+  if (!model_) return nullptr;
+  {
+    std::unique_lock<std::mutex> q(q_mu_);
+    drained_cv_.wait(q, [&] { return events_.empty() && !busy_; });
+  }
+  *lk = std::unique_lock<std::mutex>(model_mu_);
+  if (!model_error_.empty()) fail(QT_ERR_ARG, "partition model: " + model_error_);
+  return model_.get();
 }
 
 // ---- circuit model (circuit.cpp) -------------------------------------------
@@ -69,13 +135,23 @@ uint32_t Sim::new_net(size_t at) {
   return id;
 }
 
-uint32_t Sim::insert_net_front() { return new_net(0); }
-uint32_t Sim::insert_net_back() { return new_net(order_.size()); }
+uint32_t Sim::insert_net_front() {
+  const uint32_t id = new_net(0);
+  post([id](PartitionModel& m) { m.insert_net(id, 0); });
+  return id;
+}
+uint32_t Sim::insert_net_back() {
+  const uint32_t id = new_net(order_.size());
+  post([id](PartitionModel& m) { m.insert_net_back(id); });
+  return id;
+}
 
 uint32_t Sim::insert_net_after(uint32_t after) {
   auto it = std::find(order_.begin(), order_.end(), after);
   if (it == order_.end()) fail(QT_ERR_INVALID_POSITION, "insert_net: unknown anchor net");
-  return new_net(static_cast<size_t>(it - order_.begin()) + 1);
+  const uint32_t id = new_net(static_cast<size_t>(it - order_.begin()) + 1);
+  post([id, after](PartitionModel& m) { m.insert_net(id, after); });
+  return id;
 }
 
 void Sim::remove_net(uint32_t net) {
@@ -85,6 +161,7 @@ void Sim::remove_net(uint32_t net) {
   for (uint32_t g : gs) remove_gate(g);
   nets_.erase(net);
   order_.erase(std::find(order_.begin(), order_.end(), net));
+  post([net](PartitionModel& m) { m.remove_net(net); });
   pending_ = true;
 }
 
@@ -167,6 +244,7 @@ uint32_t Sim::insert_gate(int kind, const double* params, uint32_t net,
   gates_.emplace(id, GateRec{g, net});
   it->second.push_back(id);
   edited_at(pos);
+  post([id, g, net](PartitionModel& m) { m.insert_gate(id, g, net); });
   return id;
 }
 
@@ -178,6 +256,7 @@ void Sim::remove_gate(uint32_t gate) {
   gs.erase(std::find(gs.begin(), gs.end(), gate));
   gates_.erase(it);
   edited_at(pos);
+  post([gate](PartitionModel& m) { m.remove_gate(gate); });
 }
 
 std::vector<qt_gate> Sim::flatten(std::vector<uint32_t>* ids) const {
@@ -203,6 +282,7 @@ void Sim::update_state() {
   stats.full = ran_full_ ? 0 : 1;
   if (ran_full_ && !pending_) {
     last_ = stats;  // nothing pending: nothing executes
+    post([](PartitionModel& m) { m.update(); });
     return;
   }
   std::vector<uint32_t> ids;
@@ -352,6 +432,7 @@ void Sim::update_state() {
   last_ = stats;
   pending_ = false;
   ran_full_ = true;
+  post([](PartitionModel& m) { m.update(); });
 }
 
 void Sim::amplitudes(uint64_t first, uint64_t last, double* out) {

@@ -2,12 +2,18 @@
 // (qtask::Simulator, engine.hpp:46-151) on the device state of qt_state.
 #pragma once
 
+#include <condition_variable>
 #include <cstdint>
+#include <deque>
+#include <functional>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
 
+#include "qt_partition.hpp"
 #include "qt_state.hpp"
 
 namespace qtb {
@@ -15,6 +21,7 @@ namespace qtb {
 class Sim {
  public:
   Sim(int nqubits, const qt_config* cfg);
+  ~Sim();
 
   int nqubits() const { return n_; }
   uint64_t block_size() const { return bs_; }
@@ -42,6 +49,12 @@ class Sim {
   void gate_info(uint32_t gate, qt_gate* out, uint32_t* net) const;
   std::vector<qt_gate> flatten(std::vector<uint32_t>* ids = nullptr) const;
   State& state() { return *st_; }
+
+  // The reference-unit partition model (qt_partition.hpp), caught up with
+  // every modifier / update so far; nullptr when it is off for this state
+  // (auto: at most kModelMaxBlocks partition blocks). Callers hold the
+  // returned lock while reading the model.
+  const PartitionModel* model(std::unique_lock<std::mutex>* lk);
 
  private:
   struct GateRec {
@@ -75,6 +88,18 @@ class Sim {
   std::unordered_map<std::string, std::shared_ptr<State::PreparedPlan>> seg_plans_;
   int nbuf_ = 1;
   qt_run_stats last_{};
+  // partition model on its own thread: modifiers post events, queries wait
+  // for the queue to drain (the reference's graph upkeep costs O(stages x
+  // partitions) per edit; it never delays the device work)
+  void post(std::function<void(PartitionModel&)> ev);
+  void model_worker();
+  std::unique_ptr<PartitionModel> model_;
+  std::mutex q_mu_, model_mu_;
+  std::condition_variable q_cv_, drained_cv_;
+  std::deque<std::function<void(PartitionModel&)>> events_;
+  bool busy_ = false, stop_ = false;
+  std::string model_error_;
+  std::thread model_thread_;
   bool trace_ = false;  // QTB_SIM_TRACE=1: per-segment timing / cache lines on stderr
   uint64_t trace_hits_ = 0, trace_misses_ = 0;
 };

@@ -13,9 +13,8 @@
 #include <vector>
 
 #include "qtask/engine.hpp"
+#include "qtask/oracle.hpp"
 #include "qtask/qasm.hpp"
-
-extern "C" int qo_apply(int n, double* state, const void* gates, size_t count, int threads);
 
 using namespace qtask;
 
@@ -30,13 +29,8 @@ void report(const char* name, bool ok, const std::string& detail = "") {
 }
 
 std::vector<Complex> dense_oracle(const Simulator& sim) {
-  const int n = sim.num_qubits();
-  std::vector<Complex> st(std::size_t{1} << n, Complex{0, 0});
-  st[0] = Complex{1, 0};
-  const std::vector<qt_gate> gs = sim.circuit().gates();
-  if (qo_apply(n, reinterpret_cast<double*>(st.data()), gs.data(), gs.size(), 4) != 0)
-    std::printf("oracle rejected the circuit\n");
-  return st;
+  // the reference's oracle API over the test-only C restatement
+  return oracle::simulate_dense(sim.circuit());
 }
 
 double max_dev(const Simulator& sim) {

@@ -309,6 +309,25 @@ def test_cpp_dropin_program(gpu):
     assert "[FAIL]" not in out.stdout
 
 
+def test_reference_acceptance_suite(gpu):
+    """The reference's OWN acceptance suite (proj/tests/acceptance.cpp with
+    its test_support.hpp), compiled unmodified against include/qtask/*.hpp
+    (tests/cpp/Makefile, where the reference exists; the binary travels with
+    the repo) and run on the B200 engine: all nine criteria -- oracle
+    equivalence full / incremental, golden partitions, golden incremental
+    impact, golden connectivity, normalisation, determinism, locality and
+    the block-size sweep."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "ref_acceptance")
+    assert os.path.exists(exe), "tests/cpp/ref_acceptance was not built (build() in this container)"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("[PASS]") == 9 and "[FAIL]" not in out.stdout
+
+
 def test_config5_shape_hybrid_compiled(gpu):
     """The incremental engine's default at >= 20 qubits: hybrid compiled
     passes (segments found in the compile cache run compiled, the others on
