@@ -510,6 +510,14 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   kc.param = sp.kparam;
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
   const std::string outer = hexu(sp.outer_mask);
+  // element offsets fit 32 bits for buffers of <= 2^32 amplitudes
+  const bool narrow = sp.ntiles <= (1ull << 20) && (sp.lo_mask >> 32) == 0 && (sp.outer_mask >> 32) == 0 &&
+                      (dl.tmask >> 32) == 0;
+  const char* ix = narrow ? "u32" : "u64";
+  static const bool asm_smem = [] {
+    const char* e = std::getenv("QTB_JIT_ASMSMEM");
+    return e && std::atoi(e) != 0;
+  }();
   os << "FI void mbar_wait(u32 a, u32 ph) {\n"
      << "  asm volatile(\"{\\n .reg .pred p;\\n W:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n"
         " @!p bra W;\\n }\" :: \"r\"(a), \"r\"(ph) : \"memory\");\n}\n"
@@ -523,35 +531,43 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      << "  const u32 fb = smbase + " << 3 * TB << "u;  // 6 mbarriers (8 B each)\n"
      << "  const u32 grp = threadIdx.x >> " << (k - R) << ";\n"
      << "  const u32 t = threadIdx.x & " << (T - 1) << "u;\n"
-     << "  const u64 off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
+     << "  const " << ix << " off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
      << "  const u32 st4 = swz(t) << 4;\n";
-  if (dl.ok) os << "  const u64 off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
-  os << "  const u64 t0 = u64(blockIdx.x) * per;\n"
-     << "  const u64 t1 = t0 + per < " << hexu(sp.ntiles) << " ? t0 + per : " << hexu(sp.ntiles) << ";\n"
-     << "  const u64 cnt = t1 > t0 ? t1 - t0 : 0;\n"
+  if (dl.ok) os << "  const " << ix << " off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
+  // tile counters in 32 bits (<= 2^28 tiles): fewer live registers
+  os << "  const u32 t0 = blockIdx.x * static_cast<u32>(per);\n"
+     << "  const u32 t1 = t0 + static_cast<u32>(per) < " << sp.ntiles << "u ? t0 + static_cast<u32>(per) : "
+     << sp.ntiles << "u;\n"
+     << "  const u32 cnt = t1 > t0 ? t1 - t0 : 0u;\n"
      << "  if (threadIdx.x == 0) {\n"
      << "    for (u32 b = 0; b < 6; ++b)\n"
      << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], %1;\" :: \"r\"(fb + 8 * b), \"r\"(" << T
      << ") : \"memory\");\n"
      << "  }\n"
      << "  __syncthreads();\n"
-     << "  auto load = [&](u64 i) {\n"
-     << "    const char* s = reinterpret_cast<const char*>(src + pdep64(t0 + i, " << outer << ") + off_t);\n"
+     << "  auto load = [&](u32 i) {\n"
+     << "    const char* s = reinterpret_cast<const char*>(src + static_cast<" << ix << ">(pdep64(t0 + i, " << outer
+     << ")) + off_t);\n"
      << "    const u32 b = static_cast<u32>(i % 3);\n"
      << "    const u32 d = smbase + b * " << TB << "u;\n";
+  // the swizzled smem address is formed inside each asm statement: as
+  // plain C++ the 2^R loop-invariant (st4 ^ slot) values would be hoisted
+  // out of the tile loop and pin 2^R registers (spills at 128)
   for (int s2 = 0; s2 < NS; ++s2)
-    os << "    asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"(d + (st4 ^ " << sp.slot_sb[s2]
-       << "u)), \"l\"(s + " << sp.slot_gb[s2] << "ull) : \"memory\");\n";
+    os << "    asm volatile(\"{ .reg .b32 q; xor.b32 q, %0, " << sp.slot_sb[s2]
+       << "; add.u32 q, q, %1; cp.async.cg.shared.global [q], [%2], 16; }\" :: \"r\"(st4), \"r\"(d), \"l\"(s + "
+       << sp.slot_gb[s2] << "ull) : \"memory\");\n";
   os << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(fb + 8 * static_cast<u32>(i % 6)) : \"memory\");\n"
      << "  };\n"
      << "  if (grp == 0) { if (cnt > 0) load(0); if (cnt > 2) load(2); }\n"
      << "  else if (cnt > 1) load(1);\n"
      << "  bool bad = false;\n"
-     << "  for (u64 j = grp; j < cnt; j += 2) {\n"
+     << "  for (u32 j = grp; j < cnt; j += 2) {\n"
      << "    const u32 bi = static_cast<u32>(j % 3);\n"
-     << "    char* const smb = sm0 + bi * " << TB << "u;\n"
+     << "    const u32 smb = smbase + bi * " << TB << "u;\n"
+     << "    char* const smp = sm0 + bi * " << TB << "u;\n"
      << "    mbar_wait(fb + 8 * static_cast<u32>(j % 6), static_cast<u32>((j / 6) & 1));\n"
-     << "    const u64 base = pdep64(t0 + j, " << outer << ");\n"
+     << "    const " << ix << " base = static_cast<" << ix << ">(pdep64(t0 + j, " << outer << "));\n"
      << "    const u64 g = gbase_hi | base;\n";
   for (size_t r = 0; r < nr; ++r) {
     const DRound& rd = sp.rounds[r];
@@ -563,8 +579,14 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
     for (int s2 = 0; s2 < NS; ++s2)
       for (int i = 0; i < R; ++i)
         if (s2 & (1 << i)) sb[s2] ^= rd.sbit[i];
-    for (int s2 = 0; s2 < NS; ++s2)
-      os << " double2 v" << s2 << " = *reinterpret_cast<const double2*>(smb + (a ^ " << sb[s2] << "u));";
+    for (int s2 = 0; s2 < NS; ++s2) {
+      if (asm_smem)
+        os << " double2 v" << s2 << "; asm volatile(\"{ .reg .b32 q; xor.b32 q, %2, " << sb[s2]
+           << "; add.u32 q, q, %3; ld.shared.v2.f64 {%0, %1}, [q]; }\" : \"=d\"(v" << s2 << ".x), \"=d\"(v" << s2
+           << ".y) : \"r\"(a), \"r\"(smb));";
+      else
+        os << " double2 v" << s2 << " = *reinterpret_cast<const double2*>(smp + (a ^ " << sb[s2] << "u));";
+    }
     os << "\n";
     const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
     for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
@@ -580,16 +602,22 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
       os << " }\n    }\n";
     } else {
       os << "     ";
-      for (int s2 = 0; s2 < NS; ++s2)
-        os << " *reinterpret_cast<double2*>(smb + (a ^ " << sb[s2] << "u)) = v" << s2 << ";";
+      for (int s2 = 0; s2 < NS; ++s2) {
+        if (asm_smem)
+          os << " asm volatile(\"{ .reg .b32 q; xor.b32 q, %0, " << sb[s2]
+             << "; add.u32 q, q, %1; st.shared.v2.f64 [q], {%2, %3}; }\" :: \"r\"(a), \"r\"(smb), \"d\"(v" << s2
+             << ".x), \"d\"(v" << s2 << ".y) : \"memory\");";
+        else
+          os << " *reinterpret_cast<double2*>(smp + (a ^ " << sb[s2] << "u)) = v" << s2 << ";";
+      }
       os << "\n      gbar(1 + grp);\n    }\n";
     }
   }
   if (!dl.ok) {
     os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
     for (int s2 = 0; s2 < NS; ++s2) {
-      os << "      { const double2 x = *reinterpret_cast<const double2*>(smb + (st4 ^ " << sp.slot_sb[s2]
-         << "u));";
+      os << "      { double2 x; asm volatile(\"{ .reg .b32 q; xor.b32 q, %2, " << sp.slot_sb[s2]
+         << "; add.u32 q, q, %3; ld.shared.v2.f64 {%0, %1}, [q]; }\" : \"=d\"(x.x), \"=d\"(x.y) : \"r\"(st4), \"r\"(smb));";
       if (sp.check) os << " bad = bad || !finite2(x);";
       os << " __stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s2] << "ull), x); }\n";
     }
