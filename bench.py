@@ -212,10 +212,13 @@ def measure_incremental(make_sim, w, nmods, reference=False, tail_split=True):
     return out
 
 
-def incremental_section(nmods_c5):
+def incremental_section(nmods_c5, nmods_c5_ref=4):
     """Config 5 (28 qubits, 5000 gates, alternating insert/remove) on the GPU
-    engine, and config 1 (16 qubits, 400 gates + 20 modifiers) on the GPU
-    engine and on the reference engine (qtask::Simulator, all host threads)."""
+    engine, with its CPU references: the reference engine on the same
+    generator at reduced n (and the GPU engine beside it) and the
+    multithreaded oracle's full re-simulation at 28 qubits; config 1 (16
+    qubits, 400 gates + 20 modifiers) on the GPU engine and on the reference
+    engine (qtask::Simulator, all host threads)."""
     import oracle
     from paper_2210_01076_b200 import Config, Simulator
     from paper_2210_01076_b200 import workloads as W
@@ -226,8 +229,48 @@ def incremental_section(nmods_c5):
     w1 = W.config1()
     out["c1_gpu"] = dict(measure_incremental(lambda n: Simulator(n, Config()), w1, 20,
                                              tail_split=False), workload=w1.name)
+    threads = os.cpu_count() or 1
     if oracle.ref_available():
-        threads = os.cpu_count() or 1
+        # C5's generator at the largest n the reference engine holds in a
+        # bounded run (n = 16: 2^8 blocks of 256; its memory is O(stages x
+        # 2^n), 7 GiB here, and n = 28 is out of reach), beside the GPU
+        # engine on the identical reduced-n workload
+        w5r = W.config5(n=16, nmods=max(4, nmods_c5_ref))
+        out["c5_reference_cpu_reduced_n"] = dict(
+            measure_incremental(lambda n: oracle.RefSimulator(n, 256, 0), w5r, nmods_c5_ref,
+                                reference=True),
+            workload=w5r.name + "@n=16", cores=threads, block_size=256, modifiers=nmods_c5_ref,
+            note="REDUCED n (16 instead of 28): the reference qtask::Simulator (engine.cpp, "
+                 "compiled from its sources) on C5's generator -- 5000 gates, alternating "
+                 "insert / remove, uniform / last-10% positions -- threads = "
+                 "hardware_concurrency; CZ as H,CX,H nets")
+        out["c5_gpu_reduced_n"] = dict(
+            measure_incremental(lambda n: Simulator(n, Config()), w5r, nmods_c5_ref),
+            workload=w5r.name + "@n=16", modifiers=nmods_c5_ref,
+            note="the GPU engine on the identical reduced-n workload")
+    # the non-incremental CPU figure at the real size: the multithreaded
+    # restated oracle (bit-identical to the reference's oracle.cpp) re-simulating
+    # C5 at 28 qubits, timed on a prefix and scaled to the 5000 gates
+    # (oracle time is linear in the gate count)
+    import numpy as np
+    sample = 40
+    st = np.zeros(1 << w5.n, dtype=np.complex128)
+    st[0] = 1.0
+    from paper_2210_01076_b200.gates import lower_to_reference
+    ref_gates = lower_to_reference(w5.gates)
+    t0 = time.perf_counter()
+    oracle.simulate(w5.n, ref_gates[:sample], state=st, threads=threads)
+    per_gate = (time.perf_counter() - t0) / sample
+    del st
+    out["c5_oracle_cpu_n28"] = {
+        "full_resimulation_ms": per_gate * len(ref_gates) * 1e3,
+        "per_reference_gate_ms": per_gate * 1e3, "sample_gates": sample,
+        "reference_gates": len(ref_gates), "cores": threads,
+        "note": "NON-INCREMENTAL CPU: the multithreaded oracle restatement (oracle/qt_oracle.c, "
+                "memcmp-identical to oracle.cpp:15-50) re-simulating C5 at 28 qubits from "
+                "|0...0>, timed on the first 40 reference gates and scaled to all; a full run "
+                "measured 350 s at 16 threads (profiles/r02_c5_full_size.json)"}
+    if oracle.ref_available():
         out["c1_reference_cpu"] = dict(
             measure_incremental(lambda n: oracle.RefSimulator(n, 256, 0), w1, 20,
                                 reference=True, tail_split=False),

@@ -161,6 +161,9 @@ constexpr int kJitTileBits = 12;
 constexpr int kJitRegBits = 4;
 constexpr int kJitLowBits = 4;
 constexpr int kHybridLowBits = 3;
+// hybrid passes run the R = 4 ring kernel when compiled (C5 at 28 q: 2.16 vs
+// 2.36 ms per pass with R = 3); misses run the R = 4 interpreter
+constexpr int kHybridRegBits = 4;
 constexpr int kJitDirectBits = 3;
 // hybrid compiled passes (incremental engine) from this many local qubits up
 constexpr int kHybridMinQubits = 20;

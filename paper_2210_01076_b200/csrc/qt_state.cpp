@@ -86,7 +86,7 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   // geometry: compiled R = 4 / 2^12 tiles / 128-B runs; hybrid R = 3 (its
   // misses run on the interpreter, whose R = 4 variant is slow) with 2^12
   // tiles / 128-B runs; interpreter R = 3 / 2^10 tiles / 256-B runs
-  opt_.reg_bits = jit_mode_ == 1 ? kJitRegBits : kDefaultRegBits;
+  opt_.reg_bits = jit_mode_ == 1 ? kJitRegBits : jit_mode_ == 2 ? kHybridRegBits : kDefaultRegBits;
   opt_.tile_bits = jit_mode_ ? kJitTileBits : kDefaultTileBits;
   if (jit_mode_) opt_.low_bits = jit_mode_ == 1 ? kJitLowBits : kHybridLowBits;
   if (cfg && cfg->tile_qubits > 0)

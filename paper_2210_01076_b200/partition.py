@@ -38,9 +38,9 @@ class PartitionModel:
         check(lib().qt_pm_remove_net(self._h, net))
 
     def insert_gate(self, gate: int, kind: int, net: int, target: int, control: int = -1,
-                    theta: float = 0.0):
+                    theta: float = 0.0, phi: float = 0.0, lam: float = 0.0):
         from .gates import gate as row, gate_array
-        g = gate_array([row(kind, target, control, theta)])
+        g = gate_array([row(kind, target, control, theta, phi, lam)])
         check(lib().qt_pm_insert_gate(self._h, gate, g.ctypes.data, net))
 
     def remove_gate(self, gate: int):
