@@ -427,6 +427,11 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     return e && std::atoi(e) != 0;
   }();
   sp.kparam = sp.ring && kparam_env;
+  static const int debug_env = [] {
+    const char* e = std::getenv("QTB_JIT_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  sp.debug = debug_env;
   sp.rounds.resize(ps.rounds.size());
   for (size_t r = 0; r < ps.rounds.size(); ++r) {
     const PlanRound& pr = ps.rounds[r];
@@ -509,6 +514,16 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   Consts kc;
   kc.param = sp.kparam;
   const Direct dl = nr ? direct_round(sp, sp.rounds.back()) : Direct{};
+  // QTB_JIT_DEBUG (test builds): bit 0 -- every shared / global index is
+  // range-checked (a violation sets flag bit 2 and skips the access: the
+  // state's sync raises); bit 1 -- the two groups are skewed by pseudo-
+  // random sleeps, so the mbarrier / named-barrier protocol meets other
+  // interleavings (the results must not change by a bit)
+  const bool bounds = (sp.debug & 1) != 0, skew = (sp.debug & 2) != 0;
+  const uint64_t amps = sp.ntiles << k;
+  auto ok_s = [&](const std::string& off) {  // shared byte offset within a tile buffer
+    return bounds ? "if ((" + off + ") >= " + std::to_string(TB) + "u) { atomicOr(flag, 4); } else " : std::string();
+  };
   const std::string outer = hexu(sp.outer_mask);
   // element offsets fit 32 bits for buffers of <= 2^32 amplitudes
   const bool narrow = sp.ntiles <= (1ull << 20) && (sp.lo_mask >> 32) == 0 && (sp.outer_mask >> 32) == 0 &&
@@ -553,6 +568,9 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   // the swizzled smem address is formed inside each asm statement: as
   // plain C++ the 2^R loop-invariant (st4 ^ slot) values would be hoisted
   // out of the tile loop and pin 2^R registers (spills at 128)
+  if (bounds)
+    os << "    if (u64(pdep64(t0 + i, " << outer << ")) + off_t + " << (sp.slot_gb[NS - 1] / 16) << "ull >= " << amps
+       << "ull || (st4 ^ " << sp.slot_sb[NS - 1] << "u) >= " << TB << "u) atomicOr(flag, 4);\n";
   for (int s2 = 0; s2 < NS; ++s2)
     os << "    asm volatile(\"{ .reg .b32 q; xor.b32 q, %0, " << sp.slot_sb[s2]
        << "; add.u32 q, q, %1; cp.async.cg.shared.global [q], [%2], 16; }\" :: \"r\"(st4), \"r\"(d), \"l\"(s + "
@@ -561,14 +579,16 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      << "  };\n"
      << "  if (grp == 0) { if (cnt > 0) load(0); if (cnt > 2) load(2); }\n"
      << "  else if (cnt > 1) load(1);\n"
-     << "  bool bad = false;\n"
-     << "  for (u32 j = grp; j < cnt; j += 2) {\n"
+     << "  bool bad = false;\n";
+  os << "  for (u32 j = grp; j < cnt; j += 2) {\n"
      << "    const u32 bi = static_cast<u32>(j % 3);\n"
      << "    const u32 smb = smbase + bi * " << TB << "u;\n"
      << "    char* const smp = sm0 + bi * " << TB << "u;\n"
      << "    mbar_wait(fb + 8 * static_cast<u32>(j % 6), static_cast<u32>((j / 6) & 1));\n"
      << "    const " << ix << " base = static_cast<" << ix << ">(pdep64(t0 + j, " << outer << "));\n"
      << "    const u64 g = gbase_hi | base;\n";
+  if (skew)
+    os << "    if (((j * 2654435761u) >> 29) == grp) __nanosleep(((j * 40503u) & 1023u) + 64u);\n";
   for (size_t r = 0; r < nr; ++r) {
     const DRound& rd = sp.rounds[r];
     const bool last_direct = r + 1 == nr && dl.ok;
@@ -585,7 +605,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
            << "; add.u32 q, q, %3; ld.shared.v2.f64 {%0, %1}, [q]; }\" : \"=d\"(v" << s2 << ".x), \"=d\"(v" << s2
            << ".y) : \"r\"(a), \"r\"(smb));";
       else
-        os << " double2 v" << s2 << " = *reinterpret_cast<const double2*>(smp + (a ^ " << sb[s2] << "u));";
+        os << " double2 v" << s2 << " = make_double2(0.0, 0.0); " << ok_s("a ^ " + std::to_string(sb[s2]) + "u")
+           << "v" << s2 << " = *reinterpret_cast<const double2*>(smp + (a ^ " << sb[s2] << "u));";
     }
     os << "\n";
     const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
@@ -597,6 +618,9 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
          << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
       for (int s2 = 0; s2 < NS; ++s2) {
         if (sp.check) os << " bad = bad || !finite2(v" << s2 << ");";
+        if (bounds)
+          os << " if (u64(base) + off_dl + " << dl.off[s2] / 16 << "ull >= " << amps
+             << "ull) atomicOr(flag, 4); else";
         os << " __stcs(reinterpret_cast<double2*>(gd + " << dl.off[s2] << "ull), v" << s2 << ");";
       }
       os << " }\n    }\n";
@@ -608,7 +632,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
              << "; add.u32 q, q, %1; st.shared.v2.f64 [q], {%2, %3}; }\" :: \"r\"(a), \"r\"(smb), \"d\"(v" << s2
              << ".x), \"d\"(v" << s2 << ".y) : \"memory\");";
         else
-          os << " *reinterpret_cast<double2*>(smp + (a ^ " << sb[s2] << "u)) = v" << s2 << ";";
+          os << " " << ok_s("a ^ " + std::to_string(sb[s2]) + "u") << "*reinterpret_cast<double2*>(smp + (a ^ "
+             << sb[s2] << "u)) = v" << s2 << ";";
       }
       os << "\n      gbar(1 + grp);\n    }\n";
     }
@@ -791,7 +816,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   // every input of jit_source, as bytes (exact: no hash collisions)
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
-  const int32_t head[] = {sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam,
+  const int32_t head[] = {sp.device, sp.debug, sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam,
                           sp.coalesce_bits,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),

@@ -39,6 +39,9 @@ struct JitPassSpec {
   bool check = false;
   bool pipe = false;    // double-buffered tiles: the next tile streams in (cp.async) during the rounds
   int pf_bits = 0;      // > 0: L2 prefetch of the next tile in runs of 2^pf_bits amplitudes
+  int debug = 0;        // QTB_JIT_DEBUG test builds: 1 bounds checks, 2 group skew (ring kernel)
+  int device = 0;       // CUDA ordinal the kernel is loaded for (part of the cache key:
+                        // launch attributes / occupancy are per device)
   bool kparam = false;  // FP64 constants in a kernel-parameter block (ring kernel), not literals
   bool ring = false;    // persistent CTA, two consumer groups, 3-buffer cp.async + mbarrier ring (jit_source_ring)
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)

@@ -30,6 +30,8 @@
 
 #include "qt_gates.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace qtb {
 
 constexpr uint64_t kMinSegmentGates = 256;
@@ -278,6 +280,10 @@ std::vector<qt_gate> Sim::flatten(std::vector<uint32_t>* ids) const {
 
 void Sim::update_state() {
   const auto t0 = std::chrono::steady_clock::now();
+  struct Range {  // NVTX range of the whole update (no-op without a profiler)
+    Range() { nvtxRangePushA("qtask update_state"); }
+    ~Range() { nvtxRangePop(); }
+  } nvtx_range;
   qt_run_stats stats{};
   stats.full = ran_full_ ? 0 : 1;
   if (ran_full_ && !pending_) {

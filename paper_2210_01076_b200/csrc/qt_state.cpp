@@ -25,6 +25,8 @@
 #include "qt_gates.hpp"
 #include "qt_kernels.hpp"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace qtb {
 
 void fail(int code, const std::string& msg) { throw QtError{code, msg}; }
@@ -344,19 +346,26 @@ void State::apply(const qt_gate* gates, size_t count) {
 int State::grow_pool(int count, double max_fraction_of_free) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   const size_t bytes = sizeof(double2) * buffer_amps();
+  // one budget from the free memory at the start: the pool may take
+  // max_fraction_of_free of it in total (not of what each allocation leaves)
+  size_t fre0 = 0, tot = 0;
+  cudaMemGetInfo(&fre0, &tot);
+  const double budget = max_fraction_of_free * static_cast<double>(fre0);
+  // keep a reserve for plan / exchange buffers and the caller
+  const size_t reserve = std::max<size_t>(tot / 50, size_t(2) << 30);
+  size_t taken = 0;
   while (static_cast<int>(pool_.size()) < count) {
-    size_t fre = 0, tot = 0;
+    size_t fre = 0;
     cudaMemGetInfo(&fre, &tot);
-    // keep a reserve for plan / exchange buffers and the caller
-    const size_t reserve = std::max<size_t>(tot / 50, size_t(2) << 30);
     if (fre < reserve + bytes) break;
-    if (static_cast<double>(bytes) > max_fraction_of_free * static_cast<double>(fre)) break;
+    if (static_cast<double>(taken + bytes) > budget) break;
     double2* b = nullptr;
     if (cudaMalloc(&b, bytes) != cudaSuccess) {
       cudaGetLastError();
       break;
     }
     pool_.push_back(b);
+    taken += bytes;
   }
   return static_cast<int>(pool_.size());
 }
@@ -510,6 +519,7 @@ State::Prepared State::prepare(const Plan& plan) {
                 (pipe_max_fp64_ <= 0.0 || micro_fp64_per_amp(micro[pi], sp.R) <= pipe_max_fp64_);
       if (sp.pipe) sp.ring = false;
       sp.min_blocks = jit_min_blocks_;
+      sp.device = device_;
       sp.coalesce_bits = direct_bits_;
       if (pf_ && !sp.pipe) {
         int run = 0;
@@ -544,7 +554,10 @@ void State::upload_and_launch(const Plan& plan, const double2* src) { launch_pre
 void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2* src) {
   cuda_check(cudaEventRecord(ev0_, stream_), "event");
   size_t timing_idx = timings_used_;  // events accumulate until collected
+  // NVTX ranges per pass / exchange (nvtx3 is header-only: the calls are
+  // no-ops unless a profiler injects itself, e.g. nsys / ncu --nvtx)
   auto tstart = [&](int kind) {
+    nvtxRangePushA(kind == 1 ? "qtask exchange" : "qtask tile pass");
     if (!timing_) return;
     if (timing_idx >= timings_.size()) {
       PassTiming t;
@@ -556,6 +569,7 @@ void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2*
     cudaEventRecord(timings_[timing_idx].start, stream_);
   };
   auto tstop = [&]() {
+    nvtxRangePop();
     if (!timing_) return;
     cudaEventRecord(timings_[timing_idx].stop, stream_);
     ++timing_idx;
@@ -1060,9 +1074,12 @@ void State::sync() {
   if (cudaEventElapsedTime(&ms, ev0_, ev1_) == cudaSuccess) stats.device_ms = ms;
   cudaGetLastError();  // an unrecorded event pair is not an error here
   if (*h_flag_) {
+    const int f = *h_flag_;
     *h_flag_ = 0;
     cuda_check(cudaMemsetAsync(d_flag_, 0, sizeof(int), stream_), "flag reset");
     cuda_check(cudaStreamSynchronize(stream_), "stream sync");
+    // bit 2: a QTB_JIT_DEBUG bounds check of a compiled pass failed
+    if (f & 4) fail(QT_ERR_CUDA, "compiled pass: index out of bounds (QTB_JIT_DEBUG)");
     fail(QT_ERR_NUMERIC, "non-finite amplitude");
   }
 }
