@@ -9,7 +9,7 @@
 // introspection members (stage_views, graph, node_name, frontier_nodes,
 // dump_graph) report the reference's partition DAG in its own units, from
 // the engine's host partition model (csrc/qt_partition.hpp; on for states of
-// at most 4096 partition blocks unless Config::partition_model says
+// at most 1024 partition blocks unless Config::partition_model says
 // otherwise). The device does not execute partitions: it runs fused tile
 // passes over whole checkpoint segments (UpdateStats::passes / gates /
 // segments / restart_gate report that work).

@@ -23,7 +23,7 @@ struct Config {
   double checkpoint_fraction = 0.0;
   int segment_gates = 0;
   int compiled = 0;         // 0: hybrid compiled passes (NVRTC, cached segments), -1: interpreter only
-  int partition_model = 0;  // reference-unit accounting / introspection: 0 auto (<= 4096 blocks), 1 on, -1 off
+  int partition_model = 0;  // reference-unit accounting / introspection: 0 auto (<= 1024 blocks), 1 on, -1 off
 };
 
 /// block_size must be a power of two >= 2 (plan.cpp:7-13).

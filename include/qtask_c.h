@@ -96,7 +96,7 @@ typedef struct qt_config {
                                 interpreter only                            */
   int32_t partition_model;   /* qt_sim: the reference-unit partition model
                                 (UpdateStats in partitions / blocks, stage
-                                views, graph): 0 = auto (states of <= 4096
+                                views, graph): 0 = auto (states of <= 1024
                                 partition blocks), 1 = on, -1 = off         */
   int32_t reserved;
 } qt_config;

@@ -37,7 +37,7 @@ namespace qtb {
 constexpr uint64_t kMinSegmentGates = 256;
 // the partition model runs (auto) for states of at most this many partition
 // blocks: its graph holds one node per block for every MxV stage
-constexpr uint64_t kModelMaxBlocks = 4096;
+constexpr uint64_t kModelMaxBlocks = 1024;
 constexpr size_t kSegmentPlanCache = 512;  // cached segment plans (cleared when full)
 
 Sim::Sim(int nqubits, const qt_config* cfg) : n_(nqubits) {
@@ -95,7 +95,7 @@ void Sim::model_worker() {
     {
       std::unique_lock<std::mutex> lk(q_mu_);
       q_cv_.wait(lk, [&] { return stop_ || !events_.empty(); });
-      if (events_.empty()) return;  // stop_
+      if (stop_) return;  // destruction: the model goes away, pending events with it
       ev = std::move(events_.front());
       events_.pop_front();
       busy_ = true;

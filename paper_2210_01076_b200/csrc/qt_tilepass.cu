@@ -517,13 +517,16 @@ __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uin
       const bool tb = (jb & dl) != 0 || (g & dg) != 0;
       const int ds = static_cast<int>((w.y >> 16) & 15u) - 1;
       const bool ph1 = (w.y & M_TD_PHASE1) != 0;
-      const double2 d0 = pl[(off >> 1) + 2], d1 = pl[(off >> 1) + 3];
+      // the factor is loaded per slot (short live range: the lean R = 3
+      // instantiation stays within its 64 registers)
+      const double2* dp = pl + (off >> 1) + 2;
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
         if (!((w.y >> s) & 1u)) continue;
         const bool b = ds >= 0 ? ((s >> ds) & 1) != 0 : tb;
         if (ph1 && !b) continue;
-        cscale(v[s], b ? d1.x : d0.x, b ? d1.y : d0.y);
+        const double2 d = dp[b ? 1 : 0];
+        cscale(v[s], d.x, d.y);
       }
       continue;
     }
@@ -568,9 +571,11 @@ __device__ __forceinline__ void run_layers(double2 (&v)[1 << R], const P& p, uin
 // tiles) at <= 64 registers (32 warps per SM); R = 4: 16 amplitudes per
 // thread, up to 256 threads (2^12 tiles) at <= 128 registers. The kernel is
 // latency-bound at low occupancy, so the R = 3 bound trades registers for
-// resident warps. kTileMaxThreads (qt_kernels.hpp) must match.
+// resident warps. R <= 2 runs only on tiny states (launch-bound): the same
+// 64-register bound keeps its generic instantiations from spilling.
+// kTileMaxThreads (qt_kernels.hpp) must match.
 template <int R>
-constexpr int kMinBlocks = R >= 4 ? 2 : (R == 3 ? 2 : 4);
+constexpr int kMinBlocks = 2;  // R <= 2 (tiny states) too: 64 registers, no spills
 template <int R>
 constexpr int kMaxThreads = R >= 4 ? 256 : 512;
 
