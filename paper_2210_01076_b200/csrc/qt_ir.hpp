@@ -161,9 +161,11 @@ constexpr int kJitTileBits = 12;
 constexpr int kJitRegBits = 4;
 constexpr int kJitLowBits = 4;
 constexpr int kHybridLowBits = 3;
-// hybrid passes run the R = 4 ring kernel when compiled (C5 at 28 q: 2.16 vs
-// 2.36 ms per pass with R = 3); misses run the R = 4 interpreter
-constexpr int kHybridRegBits = 4;
+// hybrid passes: R = 3 -- compiled the R = 4 ring kernel is faster (C5 at
+// 28 q: 2.16 vs 2.36 ms per pass), but the misses run the interpreter, whose
+// R = 4 variant is slower (5.5 vs 4.7 ms): measured on C5's modifiers, R = 3
+// keeps the last-10% class faster and the uniform class unchanged
+constexpr int kHybridRegBits = 3;
 constexpr int kJitDirectBits = 3;
 // hybrid compiled passes (incremental engine) from this many local qubits up
 constexpr int kHybridMinQubits = 20;

@@ -5,6 +5,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -389,6 +390,39 @@ JitStats g_stats;
 
 // What a compiled pass bakes in: the same tile geometry the interpreter
 // kernel gets in its KPassHead, plus the rounds.
+namespace {
+
+uint32_t swz_map(uint32_t j, const uint8_t* v, int k) {
+  uint32_t m = j;
+  for (int b = 3; b < k; ++b)
+    if ((j >> b) & 1u) m ^= v[b];
+  return m;
+}
+
+// GF(2) rank of up to three 3-bit vectors
+int rank3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t basis[3];
+  int n = 0;
+  for (uint32_t x : {a, b, c}) {
+    for (int i = 0; i < n; ++i) x = std::min(x, x ^ basis[i]);
+    if (x) basis[n++] = x;
+  }
+  return n;
+}
+
+// Extra smem wavefronts of a swizzle over the rounds' lane patterns: a
+// quarter-warp's 8 lanes differ in the round's three lowest thread (non-
+// register) tile bits; they hit 8 distinct bank groups iff those bits'
+// contributions are linearly independent.
+int swizzle_conflicts(const std::vector<std::array<int, 3>>& lanes, const uint8_t* v) {
+  int extra = 0;
+  auto contrib = [&](int b) -> uint32_t { return b < 3 ? (1u << b) : v[b]; };
+  for (const auto& t : lanes) extra += (8 >> rank3(contrib(t[0]), contrib(t[1]), contrib(t[2]))) - 1;
+  return extra;
+}
+
+}  // namespace
+
 JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool check) {
   JitPassSpec sp;
   const int k = static_cast<int>(ps.tile_phys.size());
@@ -409,7 +443,6 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     for (int i = 0; i < R; ++i)
       if ((s >> i) & 1u) off |= 1ull << ps.tile_phys[k - R + i];
     sp.slot_gb[s] = off * sizeof(double2);
-    sp.slot_sb[s] = swz_host(s << (k - R)) << 4;
   }
   sp.tile_phys = ps.tile_phys;
   // the ring kernel (jit_source_ring): 3 tile buffers must fit one CTA's
@@ -432,6 +465,35 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     return e ? std::atoi(e) : 0;
   }();
   sp.debug = debug_env;
+  // the smem swizzle: the default (qt_device.cuh swz), or for the ring kernel
+  // the first of a fixed pseudo-random sequence of maps that leaves no round
+  // with bank conflicts (C5: 71 of 244 rounds conflict under the default)
+  for (int b = 3; b < k; ++b) sp.swzv[b] = static_cast<uint8_t>(1u << (b % 3));
+  if (sp.ring) {
+    std::vector<std::array<int, 3>> lanes;
+    for (const PlanRound& pr : ps.rounds) {
+      std::array<int, 3> t{};
+      int nt = 0;
+      for (int b = 0; b < k && nt < 3; ++b)
+        if (std::find(pr.reg.begin(), pr.reg.end(), b) == pr.reg.end()) t[nt++] = b;
+      if (nt == 3) lanes.push_back(t);
+    }
+    int best = swizzle_conflicts(lanes, sp.swzv);
+    uint32_t rng = 0x9e3779b9u;
+    uint8_t cand[kMaxTileBits + 3] = {};
+    for (int tries = 0; best > 0 && tries < 4096; ++tries) {
+      for (int b = 3; b < k; ++b) {
+        rng = rng * 1664525u + 1013904223u;
+        cand[b] = static_cast<uint8_t>((rng >> 29) & 7u);
+      }
+      const int c = swizzle_conflicts(lanes, cand);
+      if (c < best) {
+        best = c;
+        std::copy(cand, cand + k, sp.swzv);
+      }
+    }
+  }
+  for (uint32_t s = 0; s < (1u << R); ++s) sp.slot_sb[s] = swz_map(s << (k - R), sp.swzv, k) << 4;
   sp.rounds.resize(ps.rounds.size());
   for (size_t r = 0; r < ps.rounds.size(); ++r) {
     const PlanRound& pr = ps.rounds[r];
@@ -442,7 +504,7 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     for (size_t i = 0; i < pr.reg.size() && i < static_cast<size_t>(kMaxRegBits); ++i) {
       dr.reg[i] = static_cast<uint8_t>(pr.reg[i]);
       dr.sreg[i] = static_cast<uint8_t>(sorted[i]);
-      dr.sbit[i] = swz_host(1u << pr.reg[i]) << 4;
+      dr.sbit[i] = swz_map(1u << pr.reg[i], sp.swzv, k) << 4;
     }
   }
   return sp;
@@ -533,6 +595,11 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
     const char* e = std::getenv("QTB_JIT_ASMSMEM");
     return e && std::atoi(e) != 0;
   }();
+  // this pass's smem swizzle (make_jit_spec: no bank conflicts in any round)
+  os << "FI u32 swzp(u32 j) {\n  u32 m = j;\n";
+  for (int bb = 3; bb < k; ++bb)
+    if (sp.swzv[bb]) os << "  m ^= (0u - ((j >> " << bb << ") & 1u)) & " << int(sp.swzv[bb]) << "u;\n";
+  os << "  return m;\n}\n";
   os << "FI void mbar_wait(u32 a, u32 ph) {\n"
      << "  asm volatile(\"{\\n .reg .pred p;\\n W:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n"
         " @!p bra W;\\n }\" :: \"r\"(a), \"r\"(ph) : \"memory\");\n}\n"
@@ -547,7 +614,7 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      << "  const u32 grp = threadIdx.x >> " << (k - R) << ";\n"
      << "  const u32 t = threadIdx.x & " << (T - 1) << "u;\n"
      << "  const " << ix << " off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
-     << "  const u32 st4 = swz(t) << 4;\n";
+     << "  const u32 st4 = swzp(t) << 4;\n";
   if (dl.ok) os << "  const " << ix << " off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
   // tile counters in 32 bits (<= 2^28 tiles): fewer live registers
   os << "  const u32 t0 = blockIdx.x * static_cast<u32>(per);\n"
@@ -594,7 +661,7 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
     const bool last_direct = r + 1 == nr && dl.ok;
     os << "    { // round " << r << "\n      u32 jb = t;";
     for (int i = 0; i < R; ++i) os << " jb = insert_zero(jb, " << int(rd.sreg[i]) << "u);";
-    os << "\n      const u32 a = swz(jb) << 4;\n     ";
+    os << "\n      const u32 a = swzp(jb) << 4;\n     ";
     std::vector<uint32_t> sb(NS, 0);
     for (int s2 = 0; s2 < NS; ++s2)
       for (int i = 0; i < R; ++i)
@@ -828,6 +895,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   put(&sp.outer_mask, 8);
   put(sp.slot_gb, sizeof(sp.slot_gb));
   put(sp.slot_sb, sizeof(sp.slot_sb));
+  put(sp.swzv, sizeof(sp.swzv));
   put(sp.rounds.data(), sp.rounds.size() * sizeof(DRound));
   put(sp.tile_phys.data(), sp.tile_phys.size() * sizeof(int));
   put(mp.round_first.data(), mp.round_first.size() * 2);

@@ -39,6 +39,11 @@ struct JitPassSpec {
   bool check = false;
   bool pipe = false;    // double-buffered tiles: the next tile streams in (cp.async) during the rounds
   int pf_bits = 0;      // > 0: L2 prefetch of the next tile in runs of 2^pf_bits amplitudes
+  // smem bank swizzle of the ring kernel, GF(2)-linear on the tile index j:
+  // bank group = (j & 7) ^ XOR of swzv[b] over the set bits b >= 3 of j,
+  // chosen per pass so every round's quarter-warp hits 8 distinct 16-B bank
+  // groups (make_jit_spec); default swzv[b] = 1 << (b % 3) (= qt_device.cuh swz)
+  uint8_t swzv[kMaxTileBits + 3] = {};
   int debug = 0;        // QTB_JIT_DEBUG test builds: 1 bounds checks, 2 group skew (ring kernel)
   int device = 0;       // CUDA ordinal the kernel is loaded for (part of the cache key:
                         // launch attributes / occupancy are per device)

@@ -348,10 +348,15 @@ void Sim::update_state() {
       chain_.push_back(Ckpt{0, b, id});
     }
     uint64_t a = restart;
+    // the last 10 % of the circuit gets half-length segments: edits there
+    // (the reference's level-by-level building, the tail class of C5)
+    // restart closer to the edit and re-plan (and run uncompiled) fewer gates
+    const uint64_t tail_start = N - N / 10;
     while (a < N) {
-      uint64_t b = std::min(N, a + seg);
+      const uint64_t len = (a >= tail_start && seg >= 128) ? seg / 2 : seg;
+      uint64_t b = std::min(N, a + len);
       auto ob = std::upper_bound(old_bounds.begin(), old_bounds.end(), a);
-      if (ob != old_bounds.end() && *ob - a >= seg / 2 && *ob - a <= 2 * seg) b = *ob;
+      if (ob != old_bounds.end() && *ob - a >= len / 2 && *ob - a <= 2 * len) b = *ob;
       int dst = take_free();
       bool in_place = false;
       if (dst < 0) {
