@@ -215,6 +215,10 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits,
 /* Process-wide compiled-pass statistics (qt_config.compiled states): passes
  * compiled, compile-cache hits, total NVRTC + load milliseconds. */
 int qt_jit_stats(uint64_t* compiled, uint64_t* cache_hits, double* compile_ms);
+/* Persistent cubin cache ($QTB_JIT_CACHE_DIR, default ~/.cache/qtask_b200;
+ * "off" disables): compiled passes found on disk (no NVRTC run) and entries
+ * written by this process. */
+int qt_jit_disk_stats(uint64_t* disk_hits, uint64_t* disk_writes);
 /* Passes queued or compiling in the background (hybrid mode). */
 int qt_jit_pending(uint64_t* pending);
 

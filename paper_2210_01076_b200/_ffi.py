@@ -64,7 +64,7 @@ HEADER_SYMBOLS = [
     "qt_group_create", "qt_group_destroy", "qt_state_create_group",
     "qt_nccl_unique_id", "qt_state_destroy", "qt_state_num_qubits", "qt_set_basis",
     "qt_write", "qt_read", "qt_apply", "qt_norm_squared", "qt_sync", "qt_last_stats",
-    "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe", "qt_jit_probe", "qt_jit_stats", "qt_jit_pending",
+    "qt_checkpoint_save", "qt_checkpoint_restore", "qt_plan_json", "qt_plan_probe", "qt_jit_probe", "qt_jit_stats", "qt_jit_disk_stats", "qt_jit_pending",
     "qt_sim_create", "qt_sim_destroy", "qt_sim_num_qubits", "qt_sim_block_size",
     "qt_sim_total_blocks", "qt_sim_insert_net_front", "qt_sim_insert_net_back",
     "qt_sim_insert_net_after", "qt_sim_remove_net", "qt_sim_insert_gate",
@@ -131,6 +131,7 @@ _SIGS = {
     "qt_jit_stats": ([_c.POINTER(_c.c_uint64), _c.POINTER(_c.c_uint64), _c.POINTER(_c.c_double)],
                      _c.c_int),
     "qt_jit_pending": ([_c.POINTER(_c.c_uint64)], _c.c_int),
+    "qt_jit_disk_stats": ([_c.POINTER(_c.c_uint64), _c.POINTER(_c.c_uint64)], _c.c_int),
     "qt_state_stream": ([_vp], _vp),
     "qt_set_timing": ([_vp, _c.c_int], _c.c_int),
     "qt_last_timings": ([_vp, _vp, _vp, _c.c_size_t, _c.POINTER(_c.c_size_t)], _c.c_int),
@@ -256,7 +257,10 @@ def jit_stats() -> dict:
     total NVRTC + load time."""
     c, h, ms = ctypes.c_uint64(0), ctypes.c_uint64(0), ctypes.c_double(0.0)
     check(lib().qt_jit_stats(ctypes.byref(c), ctypes.byref(h), ctypes.byref(ms)))
-    return {"compiled": c.value, "cache_hits": h.value, "compile_ms": ms.value}
+    dh, dw = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    check(lib().qt_jit_disk_stats(ctypes.byref(dh), ctypes.byref(dw)))
+    return {"compiled": c.value, "cache_hits": h.value, "compile_ms": ms.value,
+            "disk_hits": dh.value, "disk_writes": dw.value}
 
 
 def jit_wait(timeout_s: float = 120.0) -> bool:

@@ -888,6 +888,14 @@ int qt_jit_stats(uint64_t* compiled, uint64_t* cache_hits, double* compile_ms) {
   return QT_OK;
 }
 
+int qt_jit_disk_stats(uint64_t* disk_hits, uint64_t* disk_writes) {
+  if (!disk_hits || !disk_writes) return null_arg();
+  const qtb::JitStats st = qtb::jit_stats();
+  *disk_hits = st.disk_hits;
+  *disk_writes = st.disk_writes;
+  return QT_OK;
+}
+
 int qt_jit_pending(uint64_t* pending) {
   if (!pending) return null_arg();
   *pending = qtb::jit_pending();

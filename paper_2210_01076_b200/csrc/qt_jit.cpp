@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cerrno>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -23,6 +24,10 @@
 #include <thread>
 
 #include <pthread.h>
+#include <dirent.h>
+#include <sys/stat.h>
+#include <sys/types.h>
+#include <unistd.h>
 #include <unordered_map>
 
 #include "qt_gates.hpp"
@@ -313,6 +318,7 @@ struct Nvrtc {
   decltype(&nvrtcGetCUBIN) cubin = nullptr;
   decltype(&nvrtcDestroyProgram) destroy = nullptr;
   decltype(&nvrtcGetErrorString) errstr = nullptr;
+  decltype(&nvrtcVersion) version = nullptr;
   std::string why;
   bool ok = false;
 };
@@ -343,6 +349,7 @@ const Nvrtc& nvrtc() {
     QT_SYM(cubin, nvrtcGetCUBIN)
     QT_SYM(destroy, nvrtcDestroyProgram)
     QT_SYM(errstr, nvrtcGetErrorString)
+    QT_SYM(version, nvrtcVersion)
 #undef QT_SYM
     r.ok = true;
     return r;
@@ -350,7 +357,7 @@ const Nvrtc& nvrtc() {
   return n;
 }
 
-std::vector<char> compile_cubin(const std::string& src) {
+std::vector<char> compile_cubin_nvrtc(const std::string& src) {
   const Nvrtc& n = nvrtc();
   if (!n.ok) throw std::runtime_error("compiled passes unavailable: " + n.why);
   nvrtcProgram prog;
@@ -371,6 +378,133 @@ std::vector<char> compile_cubin(const std::string& src) {
   std::vector<char> bin(cs);
   n.cubin(prog, bin.data());
   n.destroy(&prog);
+  return bin;
+}
+
+std::atomic<uint64_t> g_disk_hits{0}, g_disk_writes{0};
+
+// ---- persistent cubin cache -------------------------------------------------
+// A fresh process pays no NVRTC for passes some earlier process compiled: the
+// CUBIN of every compiled pass is kept on disk under
+//   $QTB_JIT_CACHE_DIR  (empty or "off": no disk cache), else
+//   $XDG_CACHE_HOME/qtask_b200, else $HOME/.cache/qtask_b200,
+// in a file named by a 128-bit hash of (NVRTC version, compile options, the
+// generated source). The file stores the source itself and a hit requires it
+// to match byte for byte, so neither a hash collision nor a changed code
+// generator can return a stale kernel. Files are written to a temporary name
+// and renamed (concurrent processes never see partial entries).
+constexpr const char* kJitOptions = "sm_100a;c++17;device-default";
+constexpr size_t kDiskCacheMaxFiles = 8192;  // no new entries beyond this many
+
+struct DiskCache {
+  std::string dir;  // empty: disabled
+  std::string tag;  // NVRTC version + options
+  std::atomic<size_t> files{0};
+};
+
+DiskCache& disk_cache() {
+  static DiskCache* dc = [] {
+    auto* d = new DiskCache();
+    std::string dir;
+    if (const char* e = std::getenv("QTB_JIT_CACHE_DIR")) {
+      dir = e;
+      if (dir.empty() || dir == "off" || dir == "0") return d;
+    } else if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) {
+      dir = std::string(x) + "/qtask_b200";
+    } else if (const char* h = std::getenv("HOME"); h && *h) {
+      dir = std::string(h) + "/.cache/qtask_b200";
+    } else {
+      return d;
+    }
+    // mkdir -p
+    for (size_t i = 1; i <= dir.size(); ++i)
+      if (i == dir.size() || dir[i] == '/') {
+        const std::string part = dir.substr(0, i);
+        if (::mkdir(part.c_str(), 0755) != 0 && errno != EEXIST) return d;
+      }
+    if (::access(dir.c_str(), W_OK | X_OK) != 0) return d;
+    size_t n = 0;
+    if (DIR* dp = ::opendir(dir.c_str())) {
+      while (::readdir(dp)) ++n;
+      ::closedir(dp);
+    }
+    d->files = n;
+    int major = 0, minor = 0;
+    if (nvrtc().ok) nvrtc().version(&major, &minor);
+    d->tag = "nvrtc " + std::to_string(major) + "." + std::to_string(minor) + ";" + kJitOptions;
+    d->dir = dir;
+    return d;
+  }();
+  return *dc;
+}
+
+uint64_t fnv1a(const std::string& a, const std::string& b, uint64_t h) {
+  for (const std::string* s : {&a, &b})
+    for (unsigned char c : *s) {
+      h ^= c;
+      h *= 0x100000001b3ull;
+    }
+  return h;
+}
+
+std::string disk_path(const DiskCache& dc, const std::string& src) {
+  char name[40];
+  std::snprintf(name, sizeof(name), "%016llx%016llx.qtc",
+                static_cast<unsigned long long>(fnv1a(dc.tag, src, 0xcbf29ce484222325ull)),
+                static_cast<unsigned long long>(fnv1a(src, dc.tag, 0x9e3779b97f4a7c15ull)));
+  return dc.dir + "/" + name;
+}
+
+// file: "QTC1" | u64 tag_len | tag | u64 src_len | src | u64 bin_len | bin
+bool disk_read(const std::string& path, const std::string& tag, const std::string& src, std::vector<char>* bin) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  bool ok = false;
+  char magic[4];
+  auto get = [&](std::string* out) {
+    uint64_t n = 0;
+    if (std::fread(&n, 8, 1, f) != 1 || n > (uint64_t(1) << 30)) return false;
+    out->resize(n);
+    return n == 0 || std::fread(&(*out)[0], 1, n, f) == n;
+  };
+  std::string t, s, b;
+  if (std::fread(magic, 1, 4, f) == 4 && std::memcmp(magic, "QTC1", 4) == 0 && get(&t) && t == tag && get(&s) &&
+      s == src && get(&b) && !b.empty()) {
+    bin->assign(b.begin(), b.end());
+    ok = true;
+  }
+  std::fclose(f);
+  return ok;
+}
+
+void disk_write(DiskCache& dc, const std::string& path, const std::string& src, const std::vector<char>& bin) {
+  if (dc.files.load() >= kDiskCacheMaxFiles) return;
+  static std::atomic<unsigned> seq{0};
+  const std::string tmp = path + ".tmp" + std::to_string(::getpid()) + "_" + std::to_string(seq.fetch_add(1));
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  auto put = [&](const void* p, uint64_t n) { return std::fwrite(&n, 8, 1, f) == 1 && (n == 0 || std::fwrite(p, 1, n, f) == n); };
+  const bool ok = std::fwrite("QTC1", 1, 4, f) == 4 && put(dc.tag.data(), dc.tag.size()) && put(src.data(), src.size()) &&
+                  put(bin.data(), bin.size());
+  if (std::fclose(f) != 0 || !ok || std::rename(tmp.c_str(), path.c_str()) != 0) {
+    std::remove(tmp.c_str());
+    return;
+  }
+  dc.files.fetch_add(1);
+  g_disk_writes.fetch_add(1);
+}
+
+std::vector<char> compile_cubin(const std::string& src) {
+  DiskCache& dc = disk_cache();
+  if (dc.dir.empty()) return compile_cubin_nvrtc(src);
+  const std::string path = disk_path(dc, src);
+  std::vector<char> bin;
+  if (disk_read(path, dc.tag, src, &bin)) {
+    g_disk_hits.fetch_add(1);
+    return bin;
+  }
+  bin = compile_cubin_nvrtc(src);
+  disk_write(dc, path, src, bin);
   return bin;
 }
 
@@ -1166,7 +1300,10 @@ std::vector<char> jit_compile_cubin(const std::string& src) { return compile_cub
 
 JitStats jit_stats() {
   std::lock_guard<std::mutex> lk(g_mu);
-  return g_stats;
+  JitStats st = g_stats;
+  st.disk_hits = g_disk_hits.load();
+  st.disk_writes = g_disk_writes.load();
+  return st;
 }
 
 }  // namespace qtb

@@ -110,6 +110,7 @@ bool jit_available(std::string* why = nullptr);
 // Process-wide compile statistics (for benchmarks).
 struct JitStats {
   uint64_t compiled = 0, cache_hits = 0, misses = 0, background = 0, failed = 0;
+  uint64_t disk_hits = 0, disk_writes = 0;  // persistent cubin cache (qt_jit.cpp)
   double compile_ms = 0.0;
 };
 JitStats jit_stats();

@@ -47,6 +47,53 @@ def test_generated_passes_compile(name):
         assert js["lowered"] >= 1 and js["cubin_bytes"] > 0
 
 
+_DISK_SCRIPT = """
+import json, sys
+sys.path.insert(0, %r)
+from paper_2210_01076_b200 import workloads as W
+from paper_2210_01076_b200._ffi import jit_probe, jit_stats
+w = W.config3(n=14, layers=4)
+js = json.loads(jit_probe(w.n, w.gates, compile=True))
+print(json.dumps({"probe": js, "stats": jit_stats()}))
+"""
+
+
+def test_persistent_cubin_cache(tmp_path):
+    """A second process finds every compiled pass on disk (no NVRTC run), an
+    entry whose stored source differs is ignored, and "off" disables it."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(cache_dir):
+        env = dict(os.environ, QTB_JIT_CACHE_DIR=cache_dir)
+        out = subprocess.run([sys.executable, "-c", _DISK_SCRIPT % root], env=env, check=True,
+                             capture_output=True, text=True).stdout
+        return json.loads(out.strip().splitlines()[-1])
+
+    d = str(tmp_path / "cubins")
+    a = run(d)
+    n = a["probe"]["compiled"]
+    # (jit_probe runs twice per call: size query, then fill -- the second
+    # run of the first process already finds its own entries)
+    assert n >= 1 and a["stats"]["disk_hits"] == n and a["stats"]["disk_writes"] == n
+    files = sorted(os.listdir(d))
+    assert len(files) == n and all(f.endswith(".qtc") for f in files)
+    b = run(d)
+    assert b["stats"]["disk_hits"] == 2 * n and b["stats"]["disk_writes"] == 0
+    assert b["probe"]["cubin_bytes"] == a["probe"]["cubin_bytes"]
+    # corrupt one entry's stored source: it must be recompiled, not trusted
+    path = os.path.join(d, files[0])
+    blob = bytearray(open(path, "rb").read())
+    blob[200] ^= 0x20
+    open(path, "wb").write(bytes(blob))
+    c = run(d)
+    assert c["stats"]["disk_hits"] == 2 * n - 1 and c["stats"]["disk_writes"] == 1
+    off = run("off")
+    assert off["stats"]["disk_hits"] == 0 and off["stats"]["disk_writes"] == 0
+
+
 def test_source_is_deterministic_and_literal():
     w = W.config3(n=14, layers=3)
     a = jit_probe(w.n, w.gates, source_pass=0)
