@@ -352,6 +352,13 @@ int qt_exchange_schedule(int rank, int nlocal, int k, const int* gbit, const int
                          uint64_t tmp_amps, uint64_t* rows, size_t cap, size_t* count,
                          uint64_t* piece);
 
+/* Host-only audit of the circuit's net order index (csrc/qt_netindex.hpp, the
+ * O(log nets) replacement of the list walks of circuit.cpp:67-120): drives
+ * `ops` seeded random net inserts / removals and gate-count changes into the
+ * index and into a plain array, comparing rank, gates-before, net-at-position
+ * and the order after every step. *mismatches = failed comparisons. */
+int qt_netindex_audit(uint64_t seed, uint32_t ops, uint64_t* mismatches);
+
 /* ---- OpenQASM 2.0 front end (reference qasm.hpp:11-66, qasm.cpp:34-426) --
  * Same accepted subset, errors (line / column of the offending token) and
  * ASAP levelling as the reference; implementation: include/qtask/qasm.hpp. */

@@ -19,6 +19,7 @@
 #include "qt_kernels.hpp"
 #include "qt_micro.hpp"
 #include "qt_plan.hpp"
+#include "qt_netindex.hpp"
 #include "qt_sim.hpp"
 #include "qt_state.hpp"
 #include "qtask_c.h"
@@ -894,6 +895,76 @@ int qt_jit_disk_stats(uint64_t* disk_hits, uint64_t* disk_writes) {
   *disk_hits = st.disk_hits;
   *disk_writes = st.disk_writes;
   return QT_OK;
+}
+
+int qt_netindex_audit(uint64_t seed, uint32_t ops, uint64_t* mismatches) {
+  if (!mismatches) return null_arg();
+  return guard([&] {
+    qtb::NetIndex ix;
+    std::vector<std::pair<uint32_t, uint64_t>> flat;  // (net, gates) in order
+    uint64_t bad = 0, rng = seed * 0x9e3779b97f4a7c15ull + 1;
+    auto next = [&] {
+      rng ^= rng << 13;
+      rng ^= rng >> 7;
+      rng ^= rng << 17;
+      return rng;
+    };
+    uint32_t next_id = 1;
+    std::vector<uint32_t> order;
+    for (uint32_t step = 0; step < ops; ++step) {
+      const uint64_t r = next() % 10;
+      if (flat.empty() || r < 3) {
+        const size_t at = static_cast<size_t>(next() % (flat.size() + 1));
+        ix.insert(next_id, at);
+        flat.insert(flat.begin() + static_cast<std::ptrdiff_t>(at), {next_id, 0});
+        ++next_id;
+      } else if (r < 4) {
+        const size_t at = static_cast<size_t>(next() % flat.size());
+        ix.erase(flat[at].first);
+        flat.erase(flat.begin() + static_cast<std::ptrdiff_t>(at));
+      } else {
+        const size_t at = static_cast<size_t>(next() % flat.size());
+        int64_t d = static_cast<int64_t>(next() % 5) - 1;
+        if (static_cast<int64_t>(flat[at].second) + d < 0) d = 1;
+        ix.add_gates(flat[at].first, d);
+        flat[at].second = static_cast<uint64_t>(static_cast<int64_t>(flat[at].second) + d);
+      }
+      // compare
+      uint64_t total = 0;
+      for (const auto& e : flat) total += e.second;
+      bad += ix.nets() != flat.size();
+      bad += ix.gates() != total;
+      if (!flat.empty()) {
+        const size_t at = static_cast<size_t>(next() % flat.size());
+        uint64_t before = 0;
+        for (size_t i = 0; i < at; ++i) before += flat[i].second;
+        bad += ix.rank(flat[at].first) != at;
+        bad += ix.gates_before(flat[at].first) != before;
+        bad += ix.gates_of(flat[at].first) != flat[at].second;
+        if (total) {
+          const uint64_t pos = next() % total;
+          uint64_t acc = 0, first = 0;
+          uint32_t want = 0;
+          for (const auto& e : flat) {
+            if (pos < acc + e.second) {
+              want = e.first;
+              first = acc;
+              break;
+            }
+            acc += e.second;
+          }
+          uint64_t got_first = 0;
+          bad += ix.net_at_gate(pos, &got_first) != want;
+          bad += got_first != first;
+        }
+        const size_t from = static_cast<size_t>(next() % (flat.size() + 1));
+        ix.order(&order, from);
+        bad += order.size() != flat.size() - from;
+        for (size_t i = 0; i < order.size() && from + i < flat.size(); ++i) bad += order[i] != flat[from + i].first;
+      }
+    }
+    *mismatches = bad;
+  });
 }
 
 int qt_jit_pending(uint64_t* pending) {

@@ -132,7 +132,8 @@ const PartitionModel* Sim::model(std::unique_lock<std::mutex>* lk) {
 uint32_t Sim::new_net(size_t at) {
   const uint32_t id = next_net_++;
   nets_.emplace(id, std::vector<uint32_t>{});
-  order_.insert(order_.begin() + static_cast<std::ptrdiff_t>(at), id);
+  index_.insert(id, at);
+  order_valid_ = false;
   pending_ = true;
   return id;
 }
@@ -143,15 +144,14 @@ uint32_t Sim::insert_net_front() {
   return id;
 }
 uint32_t Sim::insert_net_back() {
-  const uint32_t id = new_net(order_.size());
+  const uint32_t id = new_net(index_.nets());
   post([id](PartitionModel& m) { m.insert_net_back(id); });
   return id;
 }
 
 uint32_t Sim::insert_net_after(uint32_t after) {
-  auto it = std::find(order_.begin(), order_.end(), after);
-  if (it == order_.end()) fail(QT_ERR_INVALID_POSITION, "insert_net: unknown anchor net");
-  const uint32_t id = new_net(static_cast<size_t>(it - order_.begin()) + 1);
+  if (!index_.has(after)) fail(QT_ERR_INVALID_POSITION, "insert_net: unknown anchor net");
+  const uint32_t id = new_net(index_.rank(after) + 1);
   post([id, after](PartitionModel& m) { m.insert_net(id, after); });
   return id;
 }
@@ -162,7 +162,8 @@ void Sim::remove_net(uint32_t net) {
   const std::vector<uint32_t> gs = it->second;
   for (uint32_t g : gs) remove_gate(g);
   nets_.erase(net);
-  order_.erase(std::find(order_.begin(), order_.end(), net));
+  index_.erase(net);
+  order_valid_ = false;
   post([net](PartitionModel& m) { m.remove_net(net); });
   pending_ = true;
 }
@@ -180,26 +181,26 @@ void Sim::gate_info(uint32_t gate, qt_gate* out, uint32_t* net) const {
   if (net) *net = it->second.net;
 }
 
-uint64_t Sim::position_of_net_end(uint32_t net) const {
-  uint64_t pos = 0;
-  for (uint32_t m : order_) {
-    pos += nets_.at(m).size();
-    if (m == net) return pos;
+const std::vector<uint32_t>& Sim::net_order() const {
+  if (!order_valid_) {
+    index_.order(&order_);
+    order_valid_ = true;
   }
-  fail(QT_ERR_UNKNOWN_NET, "unknown net");
+  return order_;
+}
+
+uint64_t Sim::position_of_net_end(uint32_t net) const {
+  if (!index_.has(net)) fail(QT_ERR_UNKNOWN_NET, "unknown net");
+  return index_.gates_before(net) + index_.gates_of(net);
 }
 
 uint64_t Sim::position_of_gate(uint32_t gate) const {
-  const uint32_t net = gates_.at(gate).net;
-  uint64_t pos = 0;
-  for (uint32_t m : order_) {
-    const auto& gs = nets_.at(m);
-    if (m == net) {
-      return pos + static_cast<uint64_t>(std::find(gs.begin(), gs.end(), gate) - gs.begin());
-    }
-    pos += gs.size();
-  }
-  fail(QT_ERR_UNKNOWN_GATE, "unknown gate");
+  auto it = gates_.find(gate);
+  if (it == gates_.end()) fail(QT_ERR_UNKNOWN_GATE, "unknown gate");
+  // a net holds at most one gate per qubit (circuit.cpp:122-135): a short scan
+  const auto& gs = nets_.at(it->second.net);
+  return index_.gates_before(it->second.net) +
+         static_cast<uint64_t>(std::find(gs.begin(), gs.end(), gate) - gs.begin());
 }
 
 void Sim::edited_at(uint64_t pos) {
@@ -245,6 +246,7 @@ uint32_t Sim::insert_gate(int kind, const double* params, uint32_t net,
   const uint32_t id = next_gate_++;
   gates_.emplace(id, GateRec{g, net});
   it->second.push_back(id);
+  index_.add_gates(net, 1);
   edited_at(pos);
   post([id, g, net](PartitionModel& m) { m.insert_gate(id, g, net); });
   return id;
@@ -256,23 +258,33 @@ void Sim::remove_gate(uint32_t gate) {
   const uint64_t pos = position_of_gate(gate);
   auto& gs = nets_.at(it->second.net);
   gs.erase(std::find(gs.begin(), gs.end(), gate));
+  index_.add_gates(it->second.net, -1);
   gates_.erase(it);
   edited_at(pos);
   post([gate](PartitionModel& m) { m.remove_gate(gate); });
 }
 
-std::vector<qt_gate> Sim::flatten(std::vector<uint32_t>* ids) const {
+std::vector<qt_gate> Sim::flatten(std::vector<uint32_t>* ids, uint64_t from) const {
   std::vector<qt_gate> out;
-  out.reserve(gates_.size());
-  if (ids) {
-    ids->clear();
-    ids->reserve(gates_.size());
-  }
-  for (uint32_t net : order_)
-    for (uint32_t g : nets_.at(net)) {
-      out.push_back(gates_.at(g).g);
-      if (ids) ids->push_back(g);
+  const uint64_t total = index_.gates();
+  if (ids) ids->clear();
+  if (from >= total) return out;
+  out.reserve(total - from);
+  if (ids) ids->reserve(total - from);
+  // the net holding position `from`, then the nets after it
+  uint64_t first = 0;
+  const uint32_t start = index_.net_at_gate(from, &first);
+  std::vector<uint32_t> tail;
+  index_.order(&tail, index_.rank(start));
+  uint64_t skip = from - first;
+  for (uint32_t net : tail) {
+    const auto& gs = nets_.at(net);
+    for (size_t i = static_cast<size_t>(std::min<uint64_t>(skip, gs.size())); i < gs.size(); ++i) {
+      out.push_back(gates_.at(gs[i]).g);
+      if (ids) ids->push_back(gs[i]);
     }
+    skip = 0;
+  }
   return out;
 }
 
@@ -291,27 +303,25 @@ void Sim::update_state() {
     post([](PartitionModel& m) { m.update(); });
     return;
   }
-  std::vector<uint32_t> ids;
-  const std::vector<qt_gate> gates = flatten(&ids);
-  const uint64_t N = gates.size();
-  // segment boundaries of the last run, by gate identity: re-simulated
-  // segments after an edit keep the same gates, hence the same plans (and
-  // compiled passes in hybrid mode)
-  std::vector<uint64_t> old_bounds;
-  {
-    std::unordered_map<uint32_t, uint64_t> pos;
-    pos.reserve(ids.size());
-    for (uint64_t i = 0; i < ids.size(); ++i) pos.emplace(ids[i], i);
-    for (uint32_t g : bound_ids_) {
-      auto it = pos.find(g);
-      if (it != pos.end()) old_bounds.push_back(it->second);
-    }
-    std::sort(old_bounds.begin(), old_bounds.end());
-  }
+  const uint64_t N = index_.gates();
   if (!ran_full_) chain_.clear();
   const uint64_t restart = chain_.empty() ? 0 : chain_.back().pos;
   const size_t chain_keep = chain_.size();
   stats.restart_gate = restart;
+  // only the gates from the restart position on are touched: ids[i - restart]
+  // is the gate at circuit position i
+  std::vector<uint32_t> ids;
+  const std::vector<qt_gate> gates = flatten(&ids, restart);
+  // segment boundaries of the last run, by gate identity: re-simulated
+  // segments after an edit keep the same gates, hence the same plans (and
+  // compiled passes in hybrid mode)
+  std::vector<uint64_t> old_bounds;
+  for (uint32_t g : bound_ids_) {
+    if (!gates_.count(g)) continue;
+    const uint64_t p = position_of_gate(g);
+    if (p > restart) old_bounds.push_back(p);
+  }
+  std::sort(old_bounds.begin(), old_bounds.end());
 
   // segment length: the chain has nbuf_ buffers for N gates
   uint64_t seg = cfg_.segment_gates > 0 ? static_cast<uint64_t>(cfg_.segment_gates) : 0;
@@ -345,7 +355,7 @@ void Sim::update_state() {
       for (int q = 0; q < n_; ++q) id[q] = q;
       st_->bind(b, id);
       st_->set_basis(0);
-      chain_.push_back(Ckpt{0, b, id});
+      chain_.push_back(Ckpt{0, b, id, 0});
     }
     uint64_t a = restart;
     // the last 10 % of the circuit gets half-length segments: edits there
@@ -369,7 +379,7 @@ void Sim::update_state() {
       const Ckpt src = chain_.back();
       // a segment's gates (by identity) from the same qubit map plan the
       // same way: the plan and its lowering are cached across updates
-      std::string key(reinterpret_cast<const char*>(ids.data() + a), (b - a) * sizeof(uint32_t));
+      std::string key(reinterpret_cast<const char*>(ids.data() + (a - restart)), (b - a) * sizeof(uint32_t));
       key.append(reinterpret_cast<const char*>(src.perm.data()), src.perm.size() * sizeof(int));
       std::shared_ptr<State::PreparedPlan> pp;
       auto hit = seg_plans_.find(key);
@@ -379,7 +389,7 @@ void Sim::update_state() {
         std::vector<LOp> ops;
         ops.reserve(static_cast<size_t>(b - a));
         for (uint64_t i = a; i < b; ++i) {
-          const int rc = lower_gate(gates[i], n_, static_cast<uint32_t>(i), ops, &err);
+          const int rc = lower_gate(gates[i - restart], n_, static_cast<uint32_t>(i), ops, &err);
           if (rc != QT_OK) fail(rc, err);
         }
         fuse_ops(ops, n_);
@@ -395,7 +405,7 @@ void Sim::update_state() {
       } else {
         st_->bind(dst, src.perm);
         st_->apply_prepared(*pp, b - a, st_->buffer(src.buf), &src.perm);
-        chain_.push_back(Ckpt{b, dst, st_->perm()});
+        chain_.push_back(Ckpt{b, dst, st_->perm(), 0});
       }
       if (trace_) {
         const JitStats js = jit_stats();
@@ -424,8 +434,12 @@ void Sim::update_state() {
                    std::chrono::duration<double, std::milli>(ts - t0).count(),
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts).count());
     bound_ids_.clear();
-    for (const Ckpt& c : chain_)
-      if (c.pos > 0 && c.pos < N) bound_ids_.push_back(ids[c.pos]);
+    for (Ckpt& c : chain_) {
+      // checkpoints before the restart keep the gate that followed them
+      // (gates before an edit are untouched); the others take it from this run
+      if (c.pos >= restart) c.next_id = c.pos < N ? ids[c.pos - restart] : 0;
+      if (c.pos > 0 && c.pos < N && c.next_id) bound_ids_.push_back(c.next_id);
+    }
   } catch (const QtError&) {
     // keep the pending edits; checkpoints written by this run are dropped
     if (chain_.size() > chain_keep) chain_.resize(chain_keep);

@@ -13,6 +13,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "qt_netindex.hpp"
 #include "qt_partition.hpp"
 #include "qt_state.hpp"
 
@@ -44,10 +45,11 @@ class Sim {
   const qt_run_stats& last_update() const { return last_; }
 
   size_t num_gates() const { return gates_.size(); }
-  const std::vector<uint32_t>& net_order() const { return order_; }
+  const std::vector<uint32_t>& net_order() const;
   const std::vector<uint32_t>& net_gates(uint32_t net) const;
   void gate_info(uint32_t gate, qt_gate* out, uint32_t* net) const;
-  std::vector<qt_gate> flatten(std::vector<uint32_t>* ids = nullptr) const;
+  // gates (and their ids) in circuit order from gate position `from` on
+  std::vector<qt_gate> flatten(std::vector<uint32_t>* ids = nullptr, uint64_t from = 0) const;
   State& state() { return *st_; }
 
   // The reference-unit partition model (qt_partition.hpp), caught up with
@@ -69,7 +71,11 @@ class Sim {
   int n_;
   uint64_t bs_, nblocks_;
   qt_config cfg_{};
-  std::vector<uint32_t> order_;
+  // net order with subtree gate counts (qt_netindex.hpp): positions of nets
+  // and gates in O(log nets); order_ is the flat copy net_order() hands out
+  NetIndex index_;
+  mutable std::vector<uint32_t> order_;
+  mutable bool order_valid_ = true;
   std::unordered_map<uint32_t, std::vector<uint32_t>> nets_;
   std::unordered_map<uint32_t, GateRec> gates_;
   uint32_t next_net_ = 1, next_gate_ = 1;
@@ -79,6 +85,7 @@ class Sim {
     uint64_t pos;           // state after the first `pos` gates
     int buf;                // pool buffer holding it
     std::vector<int> perm;  // its logical -> physical qubit map
+    uint32_t next_id = 0;   // the gate that followed it when it was written (0: none)
   };
   std::unique_ptr<State> st_;
   std::vector<Ckpt> chain_;  // valid checkpoints, increasing pos

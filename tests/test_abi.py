@@ -98,3 +98,9 @@ def test_config_block_size_validated_like_the_reference():
     for bs in (0, 1, 3, 384):
         with pytest.raises(Error):
             Simulator(4, Config(block_size=bs))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_net_order_index_matches_a_plain_array(seed):
+    """csrc/qt_netindex.hpp (O(log nets) positions) against an array walk."""
+    assert _ffi.netindex_audit(seed, 3000) == 0
