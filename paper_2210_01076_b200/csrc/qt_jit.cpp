@@ -594,11 +594,23 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     return e && std::atoi(e) != 0;
   }();
   sp.kparam = sp.ring && kparam_env;
+  // TMA stores need runs of >= 4 amplitudes (64 B) contiguous in the tile
+  static const bool tma_env = [] {
+    const char* e = std::getenv("QTB_JIT_TMA");
+    return e && std::atoi(e) != 0;
+  }();
+  {
+    int run = 0;
+    while (run < k && ps.tile_phys[run] == run) ++run;
+    sp.tma_store = sp.ring && tma_env && run >= 2;
+  }
   static const int debug_env = [] {
     const char* e = std::getenv("QTB_JIT_DEBUG");
     return e ? std::atoi(e) : 0;
   }();
   sp.debug = debug_env;
+  if (sp.debug & (4 | 8 | 16)) sp.check = false;  // timing ablations compute garbage
+  if (sp.debug) sp.tma_store = false;             // test / ablation builds use the st.global path
   // the smem swizzle: the default (qt_device.cuh swz), or for the ring kernel
   // the first of a fixed pseudo-random sequence of maps that leaves no round
   // with bank conflicts (C5: 71 of 244 rounds conflict under the default)
@@ -664,11 +676,17 @@ Direct direct_round(const JitPassSpec& sp, const DRound& rd) {
   uint32_t regs = 0;
   for (int i = 0; i < R; ++i) regs |= 1u << rd.reg[i];
   for (int b = 0; b < sp.coalesce_bits; ++b) {
-    // physical bit b must be a thread bit of the tile
+    // physical bit b must be a thread bit of the tile; a shrunk tile's run
+    // of low bits may be shorter than coalesce_bits (the bits above the run
+    // are outer bits then: nothing to check)
     int ti = -1;
     for (int i = 0; i < k; ++i)
       if (sp.tile_phys[i] == b) ti = i;
-    if (ti < 0 || ((regs >> ti) & 1u)) return d;
+    if (ti < 0) {
+      if (b == 0) return d;
+      break;
+    }
+    if ((regs >> ti) & 1u) return d;
   }
   for (int i = 0; i < k; ++i)
     if (!((regs >> i) & 1u)) d.tmask |= 1ull << sp.tile_phys[i];
@@ -716,6 +734,11 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   // random sleeps, so the mbarrier / named-barrier protocol meets other
   // interleavings (the results must not change by a bit)
   const bool bounds = (sp.debug & 1) != 0, skew = (sp.debug & 2) != 0;
+  // timing ablations (WRONG results, profiling only): 4 -- the HBM stores are
+  // skipped (behind a run-time-false test, so the arithmetic stays), 8 -- the
+  // cp.async tile loads likewise, 16 -- no arithmetic
+  const bool no_st = (sp.debug & 4) != 0, no_ld = (sp.debug & 8) != 0, no_fp = (sp.debug & 16) != 0;
+  const std::string st_guard = no_st ? "if (per == 0xffffffffffffull) " : "";
   const uint64_t amps = sp.ntiles << k;
   auto ok_s = [&](const std::string& off) {  // shared byte offset within a tile buffer
     return bounds ? "if ((" + off + ") >= " + std::to_string(TB) + "u) { atomicOr(flag, 4); } else " : std::string();
@@ -725,9 +748,34 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   const bool narrow = sp.ntiles <= (1ull << 20) && (sp.lo_mask >> 32) == 0 && (sp.outer_mask >> 32) == 0 &&
                       (dl.tmask >> 32) == 0;
   const char* ix = narrow ? "u32" : "u64";
+  // TMA store geometry: the tile's lowest c bits are physical bits 0..c-1, so
+  // its amplitudes form 2^(k-c) runs of 2^c contiguous amplitudes; run r sits
+  // at shared byte r * run_bytes of the (unswizzled) staging layout. Thread t
+  // issues runs t, t + T, ... (rpt of them), or the first nruns threads one.
+  const bool tma = sp.tma_store;
+  int crun = 0;
+  while (crun < k && sp.tile_phys[crun] == crun) ++crun;
+  const uint32_t run_bytes = 16u << crun;
+  const uint32_t nruns = 1u << (k - crun);
+  const uint32_t rpt = nruns > static_cast<uint32_t>(T) ? nruns / T : 1u;
+  const uint32_t run_threads = std::min<uint32_t>(nruns, T);
+  uint64_t run_tmask = 0;              // physical bits the issuing thread's index deposits into
+  std::vector<uint64_t> run_off(rpt, 0);  // amplitude offset of the thread's i-th run
+  {
+    int tb = 0;
+    while ((1u << tb) < run_threads) ++tb;
+    for (int b = 0; b < tb; ++b) run_tmask |= 1ull << sp.tile_phys[crun + b];
+    for (uint32_t i = 0; i < rpt; ++i)
+      for (int b = 0; crun + tb + b < k; ++b)
+        if ((i >> b) & 1u) run_off[i] |= 1ull << sp.tile_phys[crun + tb + b];
+  }
   static const bool asm_smem = [] {
     const char* e = std::getenv("QTB_JIT_ASMSMEM");
     return e && std::atoi(e) != 0;
+  }();
+  static const bool early = [] {
+    const char* e = std::getenv("QTB_JIT_EARLY");
+    return !e || std::atoi(e) != 0;
   }();
   // this pass's smem swizzle (make_jit_spec: no bank conflicts in any round)
   os << "FI u32 swzp(u32 j) {\n  u32 m = j;\n";
@@ -738,7 +786,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      << "  asm volatile(\"{\\n .reg .pred p;\\n W:\\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\\n"
         " @!p bra W;\\n }\" :: \"r\"(a), \"r\"(ph) : \"memory\");\n}\n"
      << "FI void gbar(u32 id) { asm volatile(\"bar.sync %0, " << T << ";\" :: \"r\"(id) : \"memory\"); }\n"
-     << "extern \"C\" __global__ void __launch_bounds__(" << 2 * T << ", 1)\n"
+     // smaller tiles: several CTAs per SM (512 threads of <= 128 registers in all)
+     << "extern \"C\" __global__ void __launch_bounds__(" << 2 * T << ", " << std::max(1, 512 / (2 * T)) << ")\n"
      << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per"
      << (sp.kparam ? ", const __grid_constant__ KP K" : "") << ") {\n"
      << "  extern __shared__ __align__(16) double2 sm[];\n"
@@ -749,7 +798,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      << "  const u32 t = threadIdx.x & " << (T - 1) << "u;\n"
      << "  const " << ix << " off_t = pdep64(t, " << hexu(sp.lo_mask) << ");\n"
      << "  const u32 st4 = swzp(t) << 4;\n";
-  if (dl.ok) os << "  const " << ix << " off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
+  if (dl.ok && !tma) os << "  const " << ix << " off_dl = pdep64(t, " << hexu(dl.tmask) << ");\n";
+  if (tma) os << "  const u64 off_run = pdep64(t, " << hexu(run_tmask) << ");\n";
   // tile counters in 32 bits (<= 2^28 tiles): fewer live registers
   os << "  const u32 t0 = blockIdx.x * static_cast<u32>(per);\n"
      << "  const u32 t1 = t0 + static_cast<u32>(per) < " << sp.ntiles << "u ? t0 + static_cast<u32>(per) : "
@@ -772,10 +822,12 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   if (bounds)
     os << "    if (u64(pdep64(t0 + i, " << outer << ")) + off_t + " << (sp.slot_gb[NS - 1] / 16) << "ull >= " << amps
        << "ull || (st4 ^ " << sp.slot_sb[NS - 1] << "u) >= " << TB << "u) atomicOr(flag, 4);\n";
+  if (no_ld) os << "    if (per == 0xffffffffffffull) {\n";
   for (int s2 = 0; s2 < NS; ++s2)
     os << "    asm volatile(\"{ .reg .b32 q; xor.b32 q, %0, " << sp.slot_sb[s2]
        << "; add.u32 q, q, %1; cp.async.cg.shared.global [q], [%2], 16; }\" :: \"r\"(st4), \"r\"(d), \"l\"(s + "
        << sp.slot_gb[s2] << "ull) : \"memory\");\n";
+  if (no_ld) os << "    }\n";
   os << "    asm volatile(\"cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\" :: \"r\"(fb + 8 * static_cast<u32>(i % 6)) : \"memory\");\n"
      << "  };\n"
      << "  if (grp == 0) { if (cnt > 0) load(0); if (cnt > 2) load(2); }\n"
@@ -790,7 +842,97 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      << "    const u64 g = gbase_hi | base;\n";
   if (skew)
     os << "    if (((j * 2654435761u) >> 29) == grp) __nanosleep(((j * 40503u) & 1023u) + 64u);\n";
-  for (size_t r = 0; r < nr; ++r) {
+  // ---- TMA-store variant of the tile body -------------------------------
+  // The buffer of this group's previous tile (j - 2) is being read by its
+  // bulk stores; it is refilled with tile j + 1 at this tile's first group
+  // barrier, after every thread has waited for its own bulk reads.
+  auto pin = [&](const char* v) {
+    os << "     ";
+    for (int s2 = 0; s2 < NS; ++s2)
+      os << " asm volatile(\"\" : \"+d\"(" << v << s2 << ".x), \"+d\"(" << v << s2 << ".y));";
+    os << "\n";
+  };
+  auto first_barrier = [&]() {
+    os << "      asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+       << "      gbar(1 + grp);\n"
+       << "      if (j >= 2 && j + 1 < cnt) load(j + 1);\n";
+  };
+  auto bulk_stores = [&]() {
+    // the staged tile is complete and visible to the async proxy: one bulk
+    // copy per run, issued by the threads that own runs
+    os << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+       << "      gbar(1 + grp);\n";
+    if (run_threads < static_cast<uint32_t>(T)) os << "      if (t < " << run_threads << "u)";
+    os << "      {\n        const char* gd = reinterpret_cast<const char*>(psi + base + off_run);\n"
+       << "        const u32 ss = smb + t * " << run_bytes << "u;\n";
+    for (uint32_t i = 0; i < rpt; ++i)
+      os << "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], " << run_bytes
+         << ";\" :: \"l\"(gd + " << run_off[i] * 16 << "ull), \"r\"(ss + " << i * T * run_bytes
+         << "u) : \"memory\");\n";
+    os << "        asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n      }\n";
+  };
+  for (size_t r = 0; tma && r < nr; ++r) {
+    const DRound& rd = sp.rounds[r];
+    const bool last_direct = r + 1 == nr && dl.ok;
+    os << "    { // round " << r << "\n      u32 jb = t;";
+    for (int i = 0; i < R; ++i) os << " jb = insert_zero(jb, " << int(rd.sreg[i]) << "u);";
+    os << "\n      const u32 a = swzp(jb) << 4;\n     ";
+    std::vector<uint32_t> sb(NS, 0), lit(NS, 0);
+    for (int s2 = 0; s2 < NS; ++s2)
+      for (int i = 0; i < R; ++i)
+        if (s2 & (1 << i)) {
+          sb[s2] ^= rd.sbit[i];
+          lit[s2] |= 16u << rd.reg[i];
+        }
+    for (int s2 = 0; s2 < NS; ++s2)
+      os << " double2 v" << s2 << " = *reinterpret_cast<const double2*>(smp + (a ^ " << sb[s2] << "u));";
+    os << "\n";
+    const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
+    if (last_direct) {
+      // every thread has read the (swizzled) buffer before anyone overwrites
+      // it with the unswizzled staging layout
+      pin("v");
+      if (r == 0) first_barrier();
+      else os << "      gbar(1 + grp);\n";
+    }
+    for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
+    os << "     ";
+    for (int s2 = 0; s2 < NS; ++s2) {
+      if (last_direct) {
+        if (sp.check) os << " bad = bad || !finite2(v" << s2 << ");";
+        os << " *reinterpret_cast<double2*>(smp + ((jb << 4) | " << lit[s2] << "u)) = v" << s2 << ";";
+      } else {
+        os << " *reinterpret_cast<double2*>(smp + (a ^ " << sb[s2] << "u)) = v" << s2 << ";";
+      }
+    }
+    os << "\n";
+    if (last_direct) {
+      bulk_stores();
+    } else if (r == 0) {
+      first_barrier();
+    } else {
+      os << "      gbar(1 + grp);\n";
+    }
+    os << "    }\n";
+  }
+  if (tma && !dl.ok) {
+    // the last round kept low bits in registers: re-read the tile with the
+    // coalesced (load) mapping and stage it unswizzled
+    os << "    {\n";
+    for (int s2 = 0; s2 < NS; ++s2)
+      os << "      double2 x" << s2 << " = *reinterpret_cast<const double2*>(smp + (st4 ^ " << sp.slot_sb[s2] << "u));\n";
+    pin("x");
+    os << "      gbar(1 + grp);\n     ";
+    for (int s2 = 0; s2 < NS; ++s2) {
+      if (sp.check) os << " bad = bad || !finite2(x" << s2 << ");";
+      os << " *reinterpret_cast<double2*>(smp + ((t << 4) | " << (static_cast<uint32_t>(s2) << (k - R + 4)) << "u)) = x" << s2 << ";";
+    }
+    os << "\n";
+    bulk_stores();
+    os << "    }\n";
+  }
+  if (tma && nr == 0) throw std::logic_error("compiled pass without rounds");
+  for (size_t r = 0; !tma && r < nr; ++r) {
     const DRound& rd = sp.rounds[r];
     const bool last_direct = r + 1 == nr && dl.ok;
     os << "    { // round " << r << "\n      u32 jb = t;";
@@ -811,18 +953,31 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
     }
     os << "\n";
     const uint32_t w0 = mp.round_first[r], w1 = w0 + mp.round_count[r];
-    for (uint32_t w = w0; w < w1; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
+    // the group's buffer is free once every thread has read it for the last
+    // time: with `early` the refill (tile j + 3) is issued right after the
+    // last round's shared-memory reads have landed in registers, before that
+    // round's arithmetic, so the HBM read gets the round's compute time as
+    // extra lead (the empty asm statements pin the loads before the barrier)
+    const bool early_refill = last_direct && early;
+    if (early_refill) {
+      os << "     ";
+      for (int s2 = 0; s2 < NS; ++s2)
+        os << " asm volatile(\"\" : \"+d\"(v" << s2 << ".x), \"+d\"(v" << s2 << ".y));";
+      os << "\n      gbar(1 + grp);\n"
+         << "      if (j + 3 < cnt) load(j + 3);\n";
+    }
+    for (uint32_t w = w0; w < w1 && !no_fp; ++w) emit_word(os, kc, R, mp.words[2 * w], mp.words[2 * w + 1], mp.pool);
     if (last_direct) {
-      // the group's buffer is free once every thread has read it
-      os << "      gbar(1 + grp);\n"
-         << "      if (j + 3 < cnt) load(j + 3);\n"
-         << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
+      if (!early_refill)
+        os << "      gbar(1 + grp);\n"
+           << "      if (j + 3 < cnt) load(j + 3);\n";
+      os << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
       for (int s2 = 0; s2 < NS; ++s2) {
         if (sp.check) os << " bad = bad || !finite2(v" << s2 << ");";
         if (bounds)
           os << " if (u64(base) + off_dl + " << dl.off[s2] / 16 << "ull >= " << amps
              << "ull) atomicOr(flag, 4); else";
-        os << " __stcs(reinterpret_cast<double2*>(gd + " << dl.off[s2] << "ull), v" << s2 << ");";
+        os << " " << st_guard << "__stcs(reinterpret_cast<double2*>(gd + " << dl.off[s2] << "ull), v" << s2 << ");";
       }
       os << " }\n    }\n";
     } else {
@@ -839,7 +994,28 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
       os << "\n      gbar(1 + grp);\n    }\n";
     }
   }
-  if (!dl.ok) {
+  if (tma) {
+    // handled above
+  } else if (!dl.ok && early) {
+    // copy-out: the whole tile share goes to registers first, so the refill
+    // of this buffer starts before the HBM stores are issued
+    os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
+    for (int s2 = 0; s2 < NS; ++s2)
+      os << "      double2 x" << s2 << "; asm volatile(\"{ .reg .b32 q; xor.b32 q, %2, " << sp.slot_sb[s2]
+         << "; add.u32 q, q, %3; ld.shared.v2.f64 {%0, %1}, [q]; }\" : \"=d\"(x" << s2 << ".x), \"=d\"(x" << s2
+         << ".y) : \"r\"(st4), \"r\"(smb));\n";
+    os << "     ";
+    for (int s2 = 0; s2 < NS; ++s2)
+      os << " asm volatile(\"\" : \"+d\"(x" << s2 << ".x), \"+d\"(x" << s2 << ".y));";
+    os << "\n      gbar(1 + grp);\n"
+       << "      if (j + 3 < cnt) load(j + 3);\n";
+    for (int s2 = 0; s2 < NS; ++s2) {
+      os << "     ";
+      if (sp.check) os << " bad = bad || !finite2(x" << s2 << ");";
+      os << " " << st_guard << "__stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s2] << "ull), x" << s2 << ");\n";
+    }
+    os << "    }\n";
+  } else if (!dl.ok) {
     os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
     for (int s2 = 0; s2 < NS; ++s2) {
       os << "      { double2 x; asm volatile(\"{ .reg .b32 q; xor.b32 q, %2, " << sp.slot_sb[s2]
@@ -852,6 +1028,7 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
        << "    if (j + 3 < cnt) load(j + 3);\n";
   }
   os << "  }\n";
+  if (tma) os << "  asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);\n";
   os << "}\n";
   std::string head = kPrelude;
@@ -1017,7 +1194,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   // every input of jit_source, as bytes (exact: no hash collisions)
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
-  const int32_t head[] = {sp.device, sp.debug, sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam,
+  const int32_t head[] = {sp.device, sp.debug, sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam, sp.tma_store,
                           sp.coalesce_bits,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),

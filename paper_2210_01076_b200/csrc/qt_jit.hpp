@@ -49,6 +49,11 @@ struct JitPassSpec {
                         // launch attributes / occupancy are per device)
   bool kparam = false;  // FP64 constants in a kernel-parameter block (ring kernel), not literals
   bool ring = false;    // persistent CTA, two consumer groups, 3-buffer cp.async + mbarrier ring (jit_source_ring)
+  // ring kernel: results leave through shared memory and the TMA engine
+  // (cp.async.bulk shared -> global, one bulk copy per contiguous run) instead
+  // of 2^R st.global per thread, which sit in the LSU queue at HBM write speed
+  // and block the other group's shared-memory traffic
+  bool tma_store = false;
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
   std::vector<DRound> rounds;  // reg / sreg / sbit per round
   std::vector<int> tile_phys;  // physical bit of each tile bit (ascending)

@@ -969,8 +969,29 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
         if (nblocked == nqubits) break;
       }
     }
+    // Tile shrinking (opt.shrink_min_bits): the low bits were reserved for
+    // coalescing only; those above the run bits that no op of the pass uses
+    // as an X-role bit leave the tile (highest first) while it keeps at least
+    // shrink_min_bits bits. The pass holds the same ops; the smaller tile
+    // needs less shared memory, so more CTAs of the compiled kernel (each with
+    // its own ring of tile buffers) are resident per SM and their load /
+    // compute / store phases overlap.
+    if (opt.shrink_min_bits > 0 && qcount > opt.shrink_min_bits) {
+      std::vector<char> xbit(nlocal, 0);
+      for (const LOp& pop : pass.ops) {
+        const int nr = roles(pop, rl);
+        for (int t = 0; t < nr; ++t)
+          if (rl[t].r == XRole && rl[t].q < nlocal) xbit[rl[t].q] = 1;
+      }
+      for (int b = m - 1; b >= std::max(0, opt.shrink_run_bits) && qcount > opt.shrink_min_bits; --b) {
+        if (inQ[b] && !xbit[b]) {
+          inQ[b] = 0;
+          --qcount;
+        }
+      }
+    }
     // complete the tile to K bits with the lowest unused local bits
-    for (int p = 0; p < nlocal && qcount < K; ++p) {
+    for (int p = 0; p < nlocal && qcount < (opt.shrink_min_bits > 0 ? std::min(K, opt.shrink_min_bits) : K); ++p) {
       if (!inQ[p]) {
         inQ[p] = 1;
         ++qcount;

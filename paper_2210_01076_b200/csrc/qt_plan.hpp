@@ -23,6 +23,11 @@ struct PlanOptions {
   // non-diagonal op counts ~3 (scaled rotation + its share of a table).
   // Balances FP64-heavy passes against HBM-bound ones (QTB_PASS_FP64).
   double max_pass_fp64 = 0.0;
+  // tile shrinking (0 = off): a pass's tile drops the reserved low bits in
+  // [shrink_run_bits, low_bits) that none of its ops needs as an X-role bit,
+  // down to shrink_min_bits tile bits (QTB_SHRINK_MIN / QTB_SHRINK_RUN)
+  int shrink_min_bits = 0;
+  int shrink_run_bits = 2;
   // exchanges pick their local victim bits among the top victim_span local
   // bits (QTB_VICTIM_SPAN)
   int victim_span = 10;

@@ -105,6 +105,8 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PASS_FP64")) opt_.max_pass_fp64 = std::atof(e);
   if (const char* e = std::getenv("QTB_VICTIM_SPAN")) opt_.victim_span = std::atoi(e);
+  if (const char* e = std::getenv("QTB_SHRINK_MIN")) opt_.shrink_min_bits = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("QTB_SHRINK_RUN")) opt_.shrink_run_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PLAN_SEARCH")) plan_search_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_EXCHANGE_TMP")) no_alt_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("QTB_JIT_MINB")) jit_min_blocks_ = std::max(0, std::atoi(e));
