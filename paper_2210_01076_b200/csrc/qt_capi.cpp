@@ -786,6 +786,8 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
     if (low_bits > 0) opt.low_bits = low_bits;
     if (const char* e = std::getenv("QTB_PASS_FP64")) opt.max_pass_fp64 = std::atof(e);
     if (const char* e = std::getenv("QTB_VICTIM_SPAN")) opt.victim_span = std::atoi(e);
+    if (const char* e = std::getenv("QTB_WINDOW_SEARCH")) opt.window_search = std::atoi(e) != 0;
+    if (const char* e = std::getenv("QTB_WINDOW_BEAM")) opt.window_beam = std::atoi(e);
     if (const char* e = std::getenv("QTB_SHRINK_MIN")) opt.shrink_min_bits = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("QTB_SHRINK_RUN")) opt.shrink_run_bits = std::max(0, std::atoi(e));
     std::vector<int> perm(num_qubits);

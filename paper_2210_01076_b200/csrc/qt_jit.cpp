@@ -595,14 +595,15 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
   }();
   sp.kparam = sp.ring && kparam_env;
   // TMA stores need runs of >= 4 amplitudes (64 B) contiguous in the tile
-  static const bool tma_env = [] {
+  static const int tma_env = [] {
     const char* e = std::getenv("QTB_JIT_TMA");
-    return e && std::atoi(e) != 0;
+    return e ? std::atoi(e) : 0;
   }();
   {
     int run = 0;
     while (run < k && ps.tile_phys[run] == run) ++run;
-    sp.tma_store = sp.ring && tma_env && run >= 2;
+    sp.tma_store = (sp.ring && run >= 2) ? tma_env : 0;
+    if (sp.tma_store == 2 && (k - R < 5 || run < 3)) sp.tma_store = 0;  // whole warps, runs of >= 128 B
   }
   static const int debug_env = [] {
     const char* e = std::getenv("QTB_JIT_DEBUG");
@@ -610,7 +611,7 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
   }();
   sp.debug = debug_env;
   if (sp.debug & (4 | 8 | 16)) sp.check = false;  // timing ablations compute garbage
-  if (sp.debug) sp.tma_store = false;             // test / ablation builds use the st.global path
+  if (sp.debug) sp.tma_store = 0;                 // test / ablation builds use the st.global path
   // the smem swizzle: the default (qt_device.cuh swz), or for the ring kernel
   // the first of a fixed pseudo-random sequence of maps that leaves no round
   // with bank conflicts (C5: 71 of 244 rounds conflict under the default)
@@ -752,7 +753,9 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   // its amplitudes form 2^(k-c) runs of 2^c contiguous amplitudes; run r sits
   // at shared byte r * run_bytes of the (unswizzled) staging layout. Thread t
   // issues runs t, t + T, ... (rpt of them), or the first nruns threads one.
-  const bool tma = sp.tma_store;
+  const bool tma = sp.tma_store == 1;
+  const bool wdrain = sp.tma_store == 2;
+  const uint32_t stage_off = 3 * TB + 1024;  // per-warp staging areas (wdrain), after the mbarriers
   int crun = 0;
   while (crun < k && sp.tile_phys[crun] == crun) ++crun;
   const uint32_t run_bytes = 16u << crun;
@@ -932,6 +935,45 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
     os << "    }\n";
   }
   if (tma && nr == 0) throw std::logic_error("compiled pass without rounds");
+  // Warp-staged drain (tma_store == 2): the warp's 2^R result slots leave in
+  // batches of two through its own staging area; the lanes that start a
+  // contiguous run of 2^cl amplitudes issue one bulk copy per slot. The warp
+  // waits for its own bulk reads only (cp.async.bulk.wait_group.read), so a
+  // slow drain (HBM write back-pressure) blocks neither the LSU nor the other
+  // group's shared-memory traffic.
+  auto staged_drain = [&](const char* v, const std::string& gptr, const uint64_t* off, int cl) {
+    const uint32_t rb = 16u << cl;
+    os << "      {\n        const u32 lane = threadIdx.x & 31u;\n"
+       << "        const u32 wst = " << stage_off << "u + (threadIdx.x >> 5) * 2048u + lane * 16u;\n"
+       << "        const bool lead = (lane & " << ((1u << cl) - 1) << "u) == 0;\n";
+    for (int q = 0; q < NS / 2; ++q) {
+      const uint32_t hb = (q & 1) * 1024u;
+      os << "        asm volatile(\"cp.async.bulk.wait_group.read 1;\" ::: \"memory\");\n        __syncwarp();\n       ";
+      for (int i = 0; i < 2; ++i) {
+        const int s2 = 2 * q + i;
+        if (sp.check) os << " bad = bad || !finite2(" << v << s2 << ");";
+        os << " *reinterpret_cast<double2*>(sm0 + wst + " << (hb + i * 512u) << "u) = " << v << s2 << ";";
+      }
+      os << "\n        asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n        __syncwarp();\n"
+         << "        if (lead) {\n";
+      for (int i = 0; i < 2; ++i) {
+        const int s2 = 2 * q + i;
+        os << "          asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], " << rb
+           << ";\" :: \"l\"(" << gptr << " + " << off[s2] << "ull), \"r\"(smbase + wst + " << (hb + i * 512u)
+           << "u) : \"memory\");\n";
+      }
+      os << "          asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n        }\n";
+    }
+    os << "      }\n";
+  };
+  // lane-contiguous low bits of the last round's direct mapping / of the load mapping
+  int cl_direct = 0, cl_load = 0;
+  if (wdrain && nr) {
+    uint32_t regs = 0;
+    for (int i = 0; i < R; ++i) regs |= 1u << sp.rounds.back().reg[i];
+    while (cl_direct < 5 && cl_direct < crun && !((regs >> cl_direct) & 1u)) ++cl_direct;
+    cl_load = std::min(5, std::min(crun, k - R));
+  }
   for (size_t r = 0; !tma && r < nr; ++r) {
     const DRound& rd = sp.rounds[r];
     const bool last_direct = r + 1 == nr && dl.ok;
@@ -972,6 +1014,12 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
         os << "      gbar(1 + grp);\n"
            << "      if (j + 3 < cnt) load(j + 3);\n";
       os << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
+      if (wdrain && cl_direct >= 3) {
+        os << "\n";
+        staged_drain("v", "gd", dl.off, cl_direct);
+        os << "      }\n    }\n";
+        continue;
+      }
       for (int s2 = 0; s2 < NS; ++s2) {
         if (sp.check) os << " bad = bad || !finite2(v" << s2 << ");";
         if (bounds)
@@ -1009,7 +1057,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
       os << " asm volatile(\"\" : \"+d\"(x" << s2 << ".x), \"+d\"(x" << s2 << ".y));";
     os << "\n      gbar(1 + grp);\n"
        << "      if (j + 3 < cnt) load(j + 3);\n";
-    for (int s2 = 0; s2 < NS; ++s2) {
+    if (wdrain && cl_load >= 3) staged_drain("x", "d", sp.slot_gb, cl_load);
+    for (int s2 = 0; s2 < NS && !(wdrain && cl_load >= 3); ++s2) {
       os << "     ";
       if (sp.check) os << " bad = bad || !finite2(x" << s2 << ");";
       os << " " << st_guard << "__stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s2] << "ull), x" << s2 << ");\n";
@@ -1028,7 +1077,7 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
        << "    if (j + 3 < cnt) load(j + 3);\n";
   }
   os << "  }\n";
-  if (tma) os << "  asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
+  if (tma || wdrain) os << "  asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
   if (sp.check) os << "  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);\n";
   os << "}\n";
   std::string head = kPrelude;
@@ -1230,6 +1279,9 @@ CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp,
   }
   e.k.threads = (sp.ring ? 2 : 1) << (sp.k - sp.R);
   e.k.smem = sp.ring ? 3 * (sizeof(double2) << sp.k) + 64 : (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
+  // warp-staged drain: 2 KiB per warp after the mbarriers (jit_source_ring stage_off)
+  if (sp.ring && sp.tma_store == 2)
+    e.k.smem = 3 * (sizeof(double2) << sp.k) + 1024 + (static_cast<size_t>(2) << (sp.k - sp.R)) / 32 * 2048;
   const void* fn = reinterpret_cast<const void*>(e.k.fn);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(e.k.smem)) != cudaSuccess ||

@@ -53,7 +53,10 @@ struct JitPassSpec {
   // (cp.async.bulk shared -> global, one bulk copy per contiguous run) instead
   // of 2^R st.global per thread, which sit in the LSU queue at HBM write speed
   // and block the other group's shared-memory traffic
-  bool tma_store = false;
+  // 1: the whole tile is staged in place and its buffer refilled one tile
+  //    later; 2: every warp drains its own results through a 2 KiB staging
+  //    area (two halves of 1 KiB), waiting on its own bulk reads only
+  int tma_store = 0;
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
   std::vector<DRound> rounds;  // reg / sreg / sbit per round
   std::vector<int> tile_phys;  // physical bit of each tile bit (ascending)

@@ -23,6 +23,7 @@
 #include <limits>
 #include <sstream>
 #include <stdexcept>
+#include <unordered_map>
 
 namespace qtb {
 
@@ -847,6 +848,9 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
   QR rl[3];
 
   std::vector<char> blockAll(nqubits), blockX(nqubits), inQ(nlocal);
+  std::vector<std::vector<int>> beam_seeds;  // window choice of every pass (beam search)
+  size_t beam_pos = 0;
+  bool beam_tried = false;
   while (true) {
     while (first < nops && done[first]) ++first;
     if (first >= nops) break;
@@ -909,65 +913,197 @@ Plan make_plan(const std::vector<LOp>& ops, int nqubits, int nlocal,
     }
 
     // ---- tile pass --------------------------------------------------------
-    std::fill(blockAll.begin(), blockAll.end(), 0);
-    std::fill(blockX.begin(), blockX.end(), 0);
-    std::fill(inQ.begin(), inQ.end(), 0);
-    for (int b = 0; b < m; ++b) inQ[b] = 1;
-    int qcount = m;
-    int nblocked = 0;
-    PlanPass pass;
-    size_t scanned = 0;
-    double fp64 = 0.0;
-    for (size_t i = first; i < nops && scanned < static_cast<size_t>(opt.lookahead); ++i) {
-      if (done[i]) continue;
-      ++scanned;
-      const LOp& op = ops[i];
-      const int nr = roles(op, rl);
-      bool can = true;
-      const double cost = (op.kind == LKind::Dense) ? 3.0 : 0.0;
-      if (opt.max_pass_fp64 > 0.0 && !pass.ops.empty() && fp64 + cost > opt.max_pass_fp64) can = false;
-      for (int t = 0; t < nr; ++t) {
-        if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
-      }
-      if (can) {
-        int need[2], nn = 0;
-        for (int t = 0; t < nr; ++t) {
-          if (rl[t].r != XRole) continue;
-          const int p = cur[rl[t].q];
-          if (p >= nlocal) {
-            can = false;
-            break;
-          }
-          if (!inQ[p]) {
-            bool dup = false;
-            for (int u = 0; u < nn; ++u) dup = dup || need[u] == p;
-            if (!dup) need[nn++] = p;
-          }
+    // One greedy fill: scan the undone ops in order; an op joins when nothing
+    // it must follow was skipped and its X-role bits are (or can still
+    // become) tile bits. `seed` bits are in the tile from the start.
+    struct Fill {
+      std::vector<size_t> taken;
+      std::vector<char> inQ;
+      int qcount = 0;
+      double fp64 = 0.0;
+    };
+    auto fill_pass = [&](const std::vector<char>& done, size_t first, const std::vector<int>& seed, Fill& f) {
+      std::fill(blockAll.begin(), blockAll.end(), 0);
+      std::fill(blockX.begin(), blockX.end(), 0);
+      f.taken.clear();
+      f.inQ.assign(nlocal, 0);
+      for (int b = 0; b < m; ++b) f.inQ[b] = 1;
+      f.qcount = m;
+      for (int p : seed)
+        if (p >= 0 && p < nlocal && !f.inQ[p] && f.qcount < K) {
+          f.inQ[p] = 1;
+          ++f.qcount;
         }
-        if (can && qcount + nn <= K) {
-          for (int u = 0; u < nn; ++u) inQ[need[u]] = 1;
-          qcount += nn;
-        } else {
-          can = false;
-        }
-      }
-      if (can) {
-        done[i] = 1;
-        fp64 += cost;
-        pass.ops.push_back(to_phys(op, cur));
-      } else {
+      f.fp64 = 0.0;
+      int nblocked = 0;
+      size_t scanned = 0;
+      for (size_t i = first; i < nops && scanned < static_cast<size_t>(opt.lookahead); ++i) {
+        if (done[i]) continue;
+        ++scanned;
+        const LOp& op = ops[i];
+        const int nr = roles(op, rl);
+        bool can = true;
+        const double cost = (op.kind == LKind::Dense) ? 3.0 : 0.0;
+        if (opt.max_pass_fp64 > 0.0 && !f.taken.empty() && f.fp64 + cost > opt.max_pass_fp64) can = false;
         for (int t = 0; t < nr; ++t) {
-          if (rl[t].r == XRole) {
-            if (!blockAll[rl[t].q]) {
-              blockAll[rl[t].q] = 1;
-              ++nblocked;
+          if (blockAll[rl[t].q] || (rl[t].r == XRole && blockX[rl[t].q])) can = false;
+        }
+        if (can) {
+          int need[2], nn = 0;
+          for (int t = 0; t < nr; ++t) {
+            if (rl[t].r != XRole) continue;
+            const int p = cur[rl[t].q];
+            if (p >= nlocal) {
+              can = false;
+              break;
             }
+            if (!f.inQ[p]) {
+              bool dup = false;
+              for (int u = 0; u < nn; ++u) dup = dup || need[u] == p;
+              if (!dup) need[nn++] = p;
+            }
+          }
+          if (can && f.qcount + nn <= K) {
+            for (int u = 0; u < nn; ++u) f.inQ[need[u]] = 1;
+            f.qcount += nn;
           } else {
-            blockX[rl[t].q] = 1;
+            can = false;
           }
         }
-        if (nblocked == nqubits) break;
+        if (can) {
+          f.fp64 += cost;
+          f.taken.push_back(i);
+        } else {
+          for (int t = 0; t < nr; ++t) {
+            if (rl[t].r == XRole) {
+              if (!blockAll[rl[t].q]) {
+                blockAll[rl[t].q] = 1;
+                ++nblocked;
+              }
+            } else {
+              blockX[rl[t].q] = 1;
+            }
+          }
+          if (nblocked == nqubits) break;
+        }
       }
+    };
+    // candidate seeds of a pass: none (first-need greedy) and every window of
+    // K - m consecutive physical bits
+    auto candidate_seeds = [&]() {
+      std::vector<std::vector<int>> c(1);
+      const int w = K - m;
+      for (int s0 = m; s0 + w <= nlocal; ++s0) {
+        c.emplace_back();
+        for (int b = 0; b < w; ++b) c.back().push_back(s0 + b);
+      }
+      return c;
+    };
+    // Beam search over the window choices (single-GPU plans only: no exchange
+    // changes the qubit map underneath): every level is one more pass, a node
+    // is the set of ops done so far, the `window_beam` nodes with the most
+    // FP64 work done survive a level, and the first level on which a node has
+    // every op done gives the seed sequence the passes below follow.
+    if (opt.window_search && opt.window_beam > 1 && nlocal == nqubits && beam_seeds.empty() && !beam_tried) {
+      beam_tried = true;
+      struct Node {
+        std::vector<char> done;
+        size_t first = 0, left = 0;
+        double fp = 0.0;
+        std::vector<std::vector<int>> seeds;
+      };
+      std::vector<Node> beam(1);
+      beam[0].done = done;
+      beam[0].first = first;
+      for (size_t i = 0; i < nops; ++i) beam[0].left += done[i] ? 0 : 1;
+      const std::vector<std::vector<int>> cands = candidate_seeds();
+      Fill f;
+      bool found = false;
+      for (int level = 0; level < 4096 && !found && !beam.empty(); ++level) {
+        std::vector<Node> next;
+        std::unordered_map<std::string, size_t> seen;
+        for (const Node& nd : beam) {
+          for (const std::vector<int>& sd : cands) {
+            fill_pass(nd.done, nd.first, sd, f);
+            if (f.taken.empty()) continue;
+            Node ch;
+            ch.done = nd.done;
+            for (size_t i : f.taken) ch.done[i] = 1;
+            std::string key(ch.done.begin(), ch.done.end());
+            auto it = seen.find(key);
+            if (it != seen.end()) continue;
+            seen.emplace(std::move(key), next.size());
+            ch.first = nd.first;
+            while (ch.first < nops && ch.done[ch.first]) ++ch.first;
+            ch.left = nd.left - f.taken.size();
+            ch.fp = nd.fp + f.fp64;
+            ch.seeds = nd.seeds;
+            ch.seeds.push_back(sd);
+            if (ch.left == 0) {
+              beam_seeds = ch.seeds;
+              found = true;
+              break;
+            }
+            next.push_back(std::move(ch));
+          }
+          if (found) break;
+        }
+        if (found) break;
+        std::sort(next.begin(), next.end(), [](const Node& a, const Node& b) {
+          if (a.fp != b.fp) return a.fp > b.fp;
+          return a.left < b.left;
+        });
+        if (next.size() > static_cast<size_t>(opt.window_beam)) next.resize(static_cast<size_t>(opt.window_beam));
+        beam.swap(next);
+      }
+      beam_pos = 0;
+    }
+    Fill best;
+    if (beam_pos < beam_seeds.size()) {
+      fill_pass(done, first, beam_seeds[beam_pos++], best);
+    } else {
+      fill_pass(done, first, {}, best);
+    }
+    if (opt.window_search && beam_seeds.empty()) {
+      // Candidate tiles: windows of K - m consecutive physical bits at every
+      // start; the fill that carries the most FP64 work (ties: most ops) wins.
+      // The first-need greedy above follows the op order, which on layered
+      // circuits spends tile bits on qubits whose neighbours block them after
+      // one layer; a window over qubits that can advance together carries
+      // several layers.
+      Fill trial;
+      std::vector<int> seed;
+      const int w = K - m;
+      for (int s0 = m; s0 + w <= nlocal; ++s0) {
+        seed.clear();
+        for (int b = 0; b < w; ++b) seed.push_back(s0 + b);
+        fill_pass(done, first, seed, trial);
+        if (trial.taken.empty()) continue;
+        if (trial.fp64 > best.fp64 + 1e-9 ||
+            (trial.fp64 > best.fp64 - 1e-9 && trial.taken.size() > best.taken.size()))
+          std::swap(best, trial);
+      }
+    }
+    PlanPass pass;
+    for (size_t i : best.taken) {
+      done[i] = 1;
+      pass.ops.push_back(to_phys(ops[i], cur));
+    }
+    inQ = best.inQ;
+    int qcount = best.qcount;
+    // seeded bits no op of the pass uses as an X-role bit leave the tile again
+    if (opt.window_search) {
+      std::vector<char> xb(nlocal, 0);
+      for (const LOp& pop : pass.ops) {
+        const int nr = roles(pop, rl);
+        for (int t = 0; t < nr; ++t)
+          if (rl[t].r == XRole && rl[t].q < nlocal) xb[rl[t].q] = 1;
+      }
+      for (int p = m; p < nlocal; ++p)
+        if (inQ[p] && !xb[p]) {
+          inQ[p] = 0;
+          --qcount;
+        }
     }
     // Tile shrinking (opt.shrink_min_bits): the low bits were reserved for
     // coalescing only; those above the run bits that no op of the pass uses

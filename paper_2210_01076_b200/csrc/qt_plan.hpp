@@ -23,6 +23,11 @@ struct PlanOptions {
   // non-diagonal op counts ~3 (scaled rotation + its share of a table).
   // Balances FP64-heavy passes against HBM-bound ones (QTB_PASS_FP64).
   double max_pass_fp64 = 0.0;
+  // per pass, also try tiles seeded with every window of consecutive
+  // physical bits and keep the fill with the most FP64 work (QTB_WINDOW_SEARCH)
+  bool window_search = false;
+  // > 1: beam search over the window choice of every pass (QTB_WINDOW_BEAM)
+  int window_beam = 0;
   // tile shrinking (0 = off): a pass's tile drops the reserved low bits in
   // [shrink_run_bits, low_bits) that none of its ops needs as an X-role bit,
   // down to shrink_min_bits tile bits (QTB_SHRINK_MIN / QTB_SHRINK_RUN)
@@ -36,9 +41,11 @@ struct PlanOptions {
 // Cost model of the compiled-mode plan search (qt_state.cpp State::plan):
 // FP64 pipe rate (DFMA/s, B200 probe at load clocks) and the ring kernel's
 // measured streaming rate (B/s, tools/tilebits_bench.py: ~5.9 TB/s).
-constexpr double kPlanFp64PerS = 1.75e13;
-constexpr double kPlanHbmBytesPerS = 5.9e12;
+constexpr double kPlanFp64PerS = 1.67e13;
+constexpr double kPlanHbmBytesPerS = 5.87e12;
+constexpr double kPlanExposedHbm = 0.56;  // share of a pass's HBM time not hidden under its FP64 time
 constexpr int kPlanSearchMinBits = 24;
+constexpr int kPlanBeamWidth = 16;  // window beam of the plan search's second phase
 
 // Merges runs of uncontrolled single-qubit ops on the same qubit into one
 // 2x2 (matrix product) and drops exact identities. Order-preserving:

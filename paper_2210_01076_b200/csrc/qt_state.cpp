@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cmath>
 #include <mutex>
+#include <limits>
 #include <thread>
 
 #include "qt_gates.hpp"
@@ -105,6 +106,12 @@ State::State(int nqubits, Mode mode, int shards, int rank, const void* nccl_id,
   if (const char* e = std::getenv("QTB_LOW_BITS")) opt_.low_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PASS_FP64")) opt_.max_pass_fp64 = std::atof(e);
   if (const char* e = std::getenv("QTB_VICTIM_SPAN")) opt_.victim_span = std::atoi(e);
+  // window search: unset = a candidate of the compiled-mode plan search, 0 = never, 1 = always
+  if (const char* e = std::getenv("QTB_WINDOW_SEARCH")) {
+    window_mode_ = std::atoi(e) != 0 ? 1 : 0;
+    opt_.window_search = window_mode_ == 1;
+  }
+  if (const char* e = std::getenv("QTB_WINDOW_BEAM")) opt_.window_beam = std::atoi(e);
   if (const char* e = std::getenv("QTB_SHRINK_MIN")) opt_.shrink_min_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_SHRINK_RUN")) opt_.shrink_run_bits = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("QTB_PLAN_SEARCH")) plan_search_ = std::atoi(e) != 0;
@@ -262,7 +269,10 @@ double plan_cost_ms(const Plan& p, int reg_bits, int nlocal) {
     if (p.passes[i].kind == PlanPass::Tile && mp[i].ok)
       fp = micro_fp64_per_amp(mp[i], std::min<int>(reg_bits, static_cast<int>(p.passes[i].tile_phys.size()))) *
            amps / kPlanFp64PerS * 1e3;
-    t += std::max(fp, hbm);
+    // measured on B200 (profiles/r02_ablation.md): a pass costs its FP64 time
+    // plus the share of its HBM time the ring kernel does not hide under the
+    // arithmetic, and never less than the streaming time
+    t += std::max(hbm, fp + kPlanExposedHbm * hbm);
   }
   return t;
 }
@@ -279,28 +289,64 @@ double plan_cost_ms(const Plan& p, int reg_bits, int nlocal) {
 Plan State::plan(const std::vector<LOp>& ops) const {
   if (jit_mode_ != 1 || nlocal_ < kPlanSearchMinBits || opt_.max_pass_fp64 > 0.0 || !plan_search_)
     return make_plan(ops, n_, nlocal_, perm_, opt_);
+  // Phase 1 candidates: every cap with the first-need greedy tiles and with
+  // the window search (PlanOptions::window_search: fewer, deeper passes on
+  // layered circuits -- C3 18 -> 13 passes; no gain on random circuits).
+  // Phase 2, only when a window plan won: the beam search over the window
+  // choices (window_beam) with the configured and one fewer reserved low bit
+  // (a window one qubit wider; C3: 10-11 passes, 150-154 ms).
+  struct Cand {
+    double cap;
+    bool window;
+    int beam, low;
+  };
   std::vector<double> caps{0.0};
   for (double c = 150.0; c <= 264.0; c += 6.0) caps.push_back(c);
-  std::vector<Plan> plans(caps.size());
-  std::vector<double> cost(caps.size(), 0.0);
-  std::vector<std::thread> th;
-  std::atomic<size_t> next{0};
-  const unsigned nt = std::max(1u, std::min<unsigned>(static_cast<unsigned>(caps.size()),
-                                                      std::thread::hardware_concurrency()));
-  for (unsigned w = 0; w < nt; ++w)
-    th.emplace_back([&] {
-      for (size_t i; (i = next.fetch_add(1)) < caps.size();) {
-        PlanOptions o = opt_;
-        o.max_pass_fp64 = caps[i];
-        plans[i] = make_plan(ops, n_, nlocal_, perm_, o);
-        cost[i] = plan_cost_ms(plans[i], o.reg_bits, nlocal_);
+  auto run = [&](const std::vector<Cand>& cands, Plan* best_plan, double* best_cost, Cand* best_cand) {
+    std::vector<Plan> plans(cands.size());
+    std::vector<double> cost(cands.size(), 0.0);
+    std::vector<std::thread> th;
+    std::atomic<size_t> next{0};
+    const unsigned nt = std::max(1u, std::min<unsigned>(static_cast<unsigned>(cands.size()),
+                                                        std::thread::hardware_concurrency()));
+    for (unsigned w = 0; w < nt; ++w)
+      th.emplace_back([&] {
+        for (size_t i; (i = next.fetch_add(1)) < cands.size();) {
+          PlanOptions o = opt_;
+          o.max_pass_fp64 = cands[i].cap;
+          o.window_search = cands[i].window;
+          o.window_beam = cands[i].beam;
+          o.low_bits = cands[i].low;
+          plans[i] = make_plan(ops, n_, nlocal_, perm_, o);
+          cost[i] = plan_cost_ms(plans[i], o.reg_bits, nlocal_);
+        }
+      });
+    for (std::thread& t : th) t.join();
+    for (size_t i = 0; i < cands.size(); ++i)
+      if (cost[i] < *best_cost - 1e-9) {
+        *best_cost = cost[i];
+        *best_plan = std::move(plans[i]);
+        *best_cand = cands[i];
       }
-    });
-  for (std::thread& t : th) t.join();
-  size_t best = 0;
-  for (size_t i = 1; i < caps.size(); ++i)
-    if (cost[i] < cost[best] - 1e-9) best = i;
-  return std::move(plans[best]);
+  };
+  std::vector<Cand> c1;
+  for (double c : caps) {
+    if (window_mode_ != 1) c1.push_back(Cand{c, false, 0, opt_.low_bits});
+    if (window_mode_ != 0) c1.push_back(Cand{c, true, opt_.window_beam, opt_.low_bits});
+  }
+  Plan best;
+  double best_cost = std::numeric_limits<double>::infinity();
+  Cand best_cand{0.0, false, 0, opt_.low_bits};
+  run(c1, &best, &best_cost, &best_cand);
+  if (best_cand.window && window_mode_ < 0 && opt_.window_beam <= 1) {
+    std::vector<Cand> c2;
+    for (double c : caps) {
+      c2.push_back(Cand{c, true, kPlanBeamWidth, opt_.low_bits});
+      if (opt_.low_bits > 3) c2.push_back(Cand{c, true, kPlanBeamWidth, opt_.low_bits - 1});
+    }
+    run(c2, &best, &best_cost, &best_cand);
+  }
+  return best;
 }
 
 void State::apply(const qt_gate* gates, size_t count) {

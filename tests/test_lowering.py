@@ -108,3 +108,37 @@ def test_scaled_rotations_renormalise_long_plans():
     assert np.isfinite(got).all()
     assert np.abs(got - want).max() <= 1e-10
     assert abs(float(np.vdot(got, got).real) - 1.0) <= 1e-12
+
+
+PLANNER_ENVS = [
+    {"QTB_WINDOW_SEARCH": "1"},
+    {"QTB_WINDOW_SEARCH": "1", "QTB_WINDOW_BEAM": "8"},
+    {"QTB_WINDOW_SEARCH": "1", "QTB_WINDOW_BEAM": "8", "QTB_PASS_FP64": "40"},
+    {"QTB_SHRINK_MIN": "5", "QTB_SHRINK_RUN": "1"},
+    {"QTB_WINDOW_SEARCH": "1", "QTB_SHRINK_MIN": "5"},
+]
+
+
+@pytest.mark.parametrize("env", range(len(PLANNER_ENVS)))
+@pytest.mark.parametrize("workload", ["c3", "c5"])
+def test_planner_options_keep_the_state(env, workload, monkeypatch):
+    """Window search (tiles seeded with every window of consecutive bits), its
+    beam search and tile shrinking only move pass boundaries / tile bits: the
+    replayed plan must still match the oracle, and on the layered circuit the
+    window search must not need more passes than the first-need greedy."""
+    w = W.config3(n=12, layers=8) if workload == "c3" else W.config5(n=11, ngates=250, nmods=0)
+    geom = dict(tile_qubits=7, reg_bits=3, low_bits=2)
+    base = json.loads(jit_probe(w.n, w.gates, source_pass=-2, **geom))
+    for k, v in PLANNER_ENVS[env].items():
+        monkeypatch.setenv(k, v)
+    plan = json.loads(jit_probe(w.n, w.gates, source_pass=-2, **geom))
+    if any(p["kind"] != "lowered" for p in plan["passes"]):
+        pytest.skip("plan has generic passes")
+    psi0 = np.zeros(1 << w.n, dtype=np.complex128)
+    psi0[0] = 1.0
+    got = apply_lowered(psi0, plan)
+    want = oracle.simulate(w.n, lower_to_reference(w.gates))
+    assert np.abs(got - want).max() <= 1e-12
+    if workload == "c3" and "QTB_WINDOW_SEARCH" in PLANNER_ENVS[env] and "QTB_PASS_FP64" not in PLANNER_ENVS[env] \
+            and "QTB_SHRINK_MIN" not in PLANNER_ENVS[env]:
+        assert len(plan["passes"]) <= len(base["passes"])
