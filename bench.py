@@ -132,6 +132,36 @@ def cpu_reference(w, budget_s: float = 20.0):
                       f"(oracle.cpp:15-50, single-threaded as written), {secs:.2f} s"}
 
 
+def cpu_port_multicore(w, budget_s: float = 10.0):
+    """The multithreaded restatement of the same dense kernel (oracle/qt_oracle.c,
+    memcmp-identical to oracle.cpp:15-50; threads split the pair loop) on the
+    first gates of the workload, all host threads: the honest multi-core CPU
+    figure beside the reference's single-threaded one."""
+    import numpy as np
+
+    import oracle
+    from paper_2210_01076_b200.gates import lower_to_reference
+    threads = os.cpu_count() or 1
+    st = np.zeros(1 << w.n, dtype=np.complex128)
+    st[w.basis] = 1.0
+    done = 0
+    secs = 0.0
+    count = 1
+    while done < len(w.gates):
+        sample = w.gates[done:done + count]
+        t0 = time.perf_counter()
+        oracle.simulate(w.n, lower_to_reference(sample), state=st, threads=threads)
+        dt = time.perf_counter() - t0
+        secs += dt
+        done += len(sample)
+        if secs >= budget_s:
+            break
+        count = max(1, int(count * min(4.0, (budget_s - secs) / max(dt, 1e-3) / 2)))
+    return {"value": done * float(1 << w.n) / secs, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {done} logical gates of {w.name} on the 2^{w.n} state, multithreaded "
+                      f"oracle restatement (oracle/qt_oracle.c), {threads} threads, {secs:.2f} s"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -444,8 +474,10 @@ def main():
                      "kernel": ("qtjit: compiled tile passes (qt_jit.cpp)" if compiled
                                 else "tile_pass_kernel (qt_tilepass.cu)"), "peak_kind": peak_kind,
                      "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms,
-                     "note": "the heavier C3 passes are FP64-bound, not HBM-bound (%d FP64 ops per "
-                             "amplitude over %d passes): see roofline_fp64 and DESIGN.md section 4"
+                     "note": "the time-optimal plan packs the gates into few FP64-bound passes (%d FP64 "
+                             "ops per amplitude over %d passes), so the HBM fraction per pass is low "
+                             "by construction: see roofline_fp64, profiles/r02_ablation.md (the ring "
+                             "streams at 0.90 of this peak without arithmetic) and DESIGN.md section 4"
                              % (round(sum(p["fp64_per_amp"] for p in tiles)), len(tiles))},
         "roofline_fp64": {"achieved_dfma_per_s": fp64_achieved, "peak_dfma_per_s": fp64_peak,
                           "frac": fp64_achieved / fp64_peak if fp64_peak else None,
@@ -470,6 +502,12 @@ def main():
                 "d2h_bytes_per_step": int(8 + 16 * head),
                 "note": "set_basis + apply (host gate array, plan reused) + norm + 2^16 "
                         "amplitudes read back, host wall clock per step"},
+        "e2e_cold": {"value": G * amps / (first_step_ms * 1e-3), "unit": UNIT, "ms": first_step_ms,
+                     "disk_cache_hits": j1.get("disk_hits", 0) - j0.get("disk_hits", 0),
+                     "note": "the first apply of this process through the public API: lowering, "
+                             "the plan search, code generation and the compile of every pass (NVRTC, "
+                             "or the on-disk cubin cache when this box compiled the passes before), "
+                             "then the passes; one-shot users without a warm cache pay this"},
         "check": {"norm_error": abs(nrm - 1.0),
                   "note": "|<psi|psi> - 1| of the last e2e step's state (deterministic "
                           "two-level reduction)"},
@@ -514,6 +552,7 @@ def main():
                                "kernel": "tile_pass_kernel (qt_tilepass.cu, layer-word interpreter)"}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(w)
+        line["cpu_multicore"] = cpu_port_multicore(w)
     if world == 1 and args.incremental_mods > 0:
         st.close()  # free the 16 GiB state for the incremental engine's checkpoints
         try:
