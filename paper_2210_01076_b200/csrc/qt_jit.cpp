@@ -604,6 +604,10 @@ JitPassSpec make_jit_spec(const PlanPass& ps, int reg_bits, int buf_bits, bool c
     while (run < k && ps.tile_phys[run] == run) ++run;
     sp.tma_store = (sp.ring && run >= 2) ? tma_env : 0;
     if (sp.tma_store == 2 && (k - R < 5 || run < 3)) sp.tma_store = 0;  // whole warps, runs of >= 128 B
+    // ... and the per-warp staging areas must fit beside the three tile buffers
+    if (sp.tma_store == 2 &&
+        3 * (sizeof(double2) << k) + 1024 + (static_cast<size_t>(2) << (k - R)) / 32 * 2048 > 227 * 1024)
+      sp.tma_store = 0;
   }
   static const int debug_env = [] {
     const char* e = std::getenv("QTB_JIT_DEBUG");

@@ -9,6 +9,7 @@ the same bar as the interpreter kernel (max |diff| <= 1e-10, norm 1e-12),
 including sharded (loopback) plans with exchanges, and compiled vs
 interpreted agreement plus the compile cache."""
 import json
+import os
 
 import numpy as np
 import pytest
@@ -184,6 +185,36 @@ def test_compiled_matches_interpreted_and_caches(gpu):
     assert after["compiled"] == before["compiled"]
     assert after["cache_hits"] > before["cache_hits"]
     assert got2.tobytes() == got.tobytes()
+
+
+@pytest.mark.gpu
+def test_plan_search_window_plan_vs_oracle(gpu):
+    """From 24 local qubits the compiled mode searches plans (FP64 caps x
+    {first-need greedy, window search}, then the beam over the window choices):
+    on the layered config the window plan wins and needs fewer passes than the
+    greedy one; its state must match the oracle (C3 family at 24 q, ~10 s of
+    multithreaded oracle)."""
+    w = W.config3(n=24, layers=20)
+    st = StateVector(24, compiled=True)
+    st.apply(w.gates)
+    searched = st.stats()["passes"]
+    got = st.read()
+    nrm = st.norm_squared()
+    st.close()
+    want = oracle.simulate(24, lower_to_reference(w.gates), threads=os.cpu_count() or 1)
+    assert np.abs(got - want).max() <= TOL
+    assert abs(nrm - 1) <= NORM_TOL
+    os.environ["QTB_PLAN_SEARCH"] = "0"
+    try:
+        st = StateVector(24, compiled=True)
+        st.apply(w.gates)
+        greedy = st.stats()["passes"]
+        got2 = st.read()
+        st.close()
+    finally:
+        del os.environ["QTB_PLAN_SEARCH"]
+    assert np.abs(got2 - want).max() <= TOL
+    assert searched < greedy, (searched, greedy)
 
 
 @pytest.mark.gpu
