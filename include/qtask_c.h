@@ -182,7 +182,9 @@ int qt_norm_squared(qt_state* st, double* out);
  * the min(k, 2^n) amplitudes of largest |a|^2 (std::norm; ties: smaller
  * index first), sorted, with their logical indices -- selected on the
  * device, only k records cross PCIe. *count = records written.
- * Single-device and loopback states. */
+ * Sharded states: collective -- every rank selects the k largest of its
+ * shard (read in logical-index order, so ties break as on one GPU), the
+ * ranks all-gather their records and each merges the same global list. */
 int qt_top_k(qt_state* st, uint64_t k, uint64_t* indices, double* amps_interleaved,
              uint64_t* count);
 int qt_sync(qt_state* st);

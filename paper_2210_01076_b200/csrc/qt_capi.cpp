@@ -410,7 +410,7 @@ int qt_sim_top_k(qt_sim* sim, uint64_t k, uint64_t* idx, double* amps, uint64_t*
 
 int qt_top_k(qt_state* st, uint64_t k, uint64_t* idx, double* amps, uint64_t* count) {
   if (!st) return null_arg();
-  return guard([&] { put_topk(st->s->top_k(k), idx, amps, count); });
+  return guard_collective(st, [&] { put_topk(st->s->top_k(k), idx, amps, count); });
 }
 
 int qt_sim_norm_squared(qt_sim* sim, double* outp) {

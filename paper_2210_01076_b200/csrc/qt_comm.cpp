@@ -136,9 +136,9 @@ bool NcclComm::sendrecv(int npeers, const int* peers, const void* const* sends,
   return nccl_ok(api_, api_->GroupEnd(), "ncclGroupEnd", err);
 }
 
-bool NcclComm::allgather_double(const double* in, double* out, cudaStream_t s,
+bool NcclComm::allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                                 std::string* err) {
-  return nccl_ok(api_, api_->AllGather(in, out, 1, ncclFloat64, comm_, s),
+  return nccl_ok(api_, api_->AllGather(in, out, count, ncclFloat64, comm_, s),
                  "ncclAllGather", err);
 }
 
@@ -272,7 +272,7 @@ bool LocalComm::sendrecv(int npeers, const int* peers, const void* const* sends,
   }, err);
 }
 
-bool LocalComm::allgather_double(const double* in, double* out, cudaStream_t s,
+bool LocalComm::allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                                  std::string* err) {
   LocalGroup::Slot& me = g_->slots_[rank_];
   std::vector<int> all(world_);
@@ -283,7 +283,7 @@ bool LocalComm::allgather_double(const double* in, double* out, cudaStream_t s,
   }
   return rendezvous(all, s, [&] {
     for (int r = 0; r < world_; ++r)
-      if (cudaMemcpyAsync(out + r, g_->slots_[r].gather_src, sizeof(double),
+      if (cudaMemcpyAsync(out + r * count, g_->slots_[r].gather_src, sizeof(double) * count,
                           cudaMemcpyDeviceToDevice, s) != cudaSuccess)
         return false;
     return true;

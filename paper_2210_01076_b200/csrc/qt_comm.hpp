@@ -38,8 +38,9 @@ class Comm {
   virtual bool sendrecv(int npeers, const int* peers, const void* const* sends,
                         void* const* recvs, size_t bytes, cudaStream_t s,
                         std::string* err) = 0;
-  // out[r] = in from rank r (one double each), device buffers.
-  virtual bool allgather_double(const double* in, double* out, cudaStream_t s,
+  // out[r * count ...] = the count doubles of rank r's in, device buffers
+  // (bit patterns travel unchanged: also used for packed integer records).
+  virtual bool allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                                 std::string* err) = 0;
   virtual bool check_async(std::string* err) = 0;
   virtual const char* kind() const = 0;
@@ -62,7 +63,7 @@ class NcclComm : public Comm {
   ~NcclComm() override;
   bool sendrecv(int npeers, const int* peers, const void* const* sends, void* const* recvs,
                 size_t bytes, cudaStream_t s, std::string* err) override;
-  bool allgather_double(const double* in, double* out, cudaStream_t s,
+  bool allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                         std::string* err) override;
   bool check_async(std::string* err) override;
   const char* kind() const override { return "nccl"; }
@@ -105,7 +106,7 @@ class LocalComm : public Comm {
   ~LocalComm() override;
   bool sendrecv(int npeers, const int* peers, const void* const* sends, void* const* recvs,
                 size_t bytes, cudaStream_t s, std::string* err) override;
-  bool allgather_double(const double* in, double* out, cudaStream_t s,
+  bool allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                         std::string* err) override;
   bool check_async(std::string*) override { return true; }
   const char* kind() const override { return "local"; }

@@ -953,17 +953,77 @@ void State::exchange(const PlanPass& pass) {
 // uniform superposition) go to the exact threshold and rank its ties in
 // logical index order (two more sweeps). Permuted (loopback) states are
 // streamed in logical-order chunks through the gather kernel.
+// Sharded states (one rank per GPU): every rank selects the k largest of its
+// shard -- read in the order of the full logical index, so ties break exactly
+// as on one GPU -- the ranks all-gather their k (key, index) pairs and each
+// merges them into the same global list. Collective: every rank calls it.
 std::vector<TopkItem> State::top_k(uint64_t k) {
-  if (mode_ == Mode::Sharded) fail(QT_ERR_ARG, "top_k: sharded (NCCL) states are not supported");
+  if (mode_ != Mode::Sharded) {
+    std::vector<int> pm(perm_.begin(), perm_.end());
+    return top_k_local(k, n_, pm);
+  }
+  // local logical qubits (ascending) and the fixed bits of this rank's global ones
+  std::vector<int> local_q, pm;
+  uint64_t fixed = 0;
+  for (int q = 0; q < n_; ++q) {
+    if (perm_[q] < nlocal_) {
+      local_q.push_back(q);
+      pm.push_back(perm_[q]);
+    } else if ((static_cast<uint64_t>(rank_) >> (perm_[q] - nlocal_)) & 1ull) {
+      fixed |= 1ull << q;
+    }
+  }
+  const uint64_t kl = std::min<uint64_t>(k, 1ull << nlocal_);
+  if (kl == 0) return {};
+  std::vector<TopkItem> mine = top_k_local(kl, nlocal_, pm);
+  for (TopkItem& it : mine) {
+    uint64_t full = fixed;
+    for (int i = 0; i < nlocal_; ++i)
+      if ((it.index >> i) & 1ull) full |= 1ull << local_q[i];
+    it.index = full;
+  }
+  TopkItem pad{};
+  pad.index = ~0ull;
+  mine.resize(kl, pad);
+  static_assert(sizeof(TopkItem) == 4 * sizeof(double), "TopkItem travels as four doubles");
+  double *d_in = nullptr, *d_out = nullptr;
+  cuda_check(cudaMalloc(&d_in, sizeof(TopkItem) * kl), "topk gather");
+  cuda_check(cudaMalloc(&d_out, sizeof(TopkItem) * kl * world_), "topk gather");
+  struct Free2 {
+    void *a, *b;
+    ~Free2() {
+      cudaFree(a);
+      cudaFree(b);
+    }
+  } guard_{d_in, d_out};
+  cuda_check(cudaMemcpyAsync(d_in, mine.data(), sizeof(TopkItem) * kl, cudaMemcpyHostToDevice, stream_),
+             "topk gather upload");
+  std::string err;
+  if (!comm_->allgather_double(d_in, d_out, 4 * kl, stream_, &err)) fail(QT_ERR_NCCL, err);
+  std::vector<TopkItem> all(kl * world_);
+  cuda_check(cudaMemcpyAsync(all.data(), d_out, sizeof(TopkItem) * all.size(), cudaMemcpyDeviceToHost, stream_),
+             "topk gather readback");
+  sync();
+  all.erase(std::remove_if(all.begin(), all.end(), [](const TopkItem& a) { return a.index == ~0ull; }), all.end());
+  std::sort(all.begin(), all.end(), [](const TopkItem& a, const TopkItem& b) {
+    return a.key != b.key ? a.key > b.key : a.index < b.index;
+  });
+  if (all.size() > k) all.resize(k);
+  return all;
+}
+
+// The k largest |a|^2 of the 2^bits amplitudes of psi_, read through the bit
+// permutation pm (position i of the returned index <-> physical bit pm[i]).
+std::vector<TopkItem> State::top_k_local(uint64_t k, int bits, const std::vector<int>& perm) {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-  const uint64_t total = 1ull << n_;
+  const uint64_t total = 1ull << bits;
   k = std::min(k, total);
   if (k == 0) return {};
   bool identity = true;
-  for (int q = 0; q < n_; ++q) identity = identity && perm_[q] == q;
+  for (int q = 0; q < bits; ++q) identity = identity && perm[q] == q;
   const uint64_t chunk = 1ull << 22;
-  std::vector<uint8_t> pm(n_);
-  for (int q = 0; q < n_; ++q) pm[q] = static_cast<uint8_t>(perm_[q]);
+  std::vector<uint8_t> pm(bits);
+  for (int q = 0; q < bits; ++q) pm[q] = static_cast<uint8_t>(perm[q]);
   if (!identity && d_tmp_amps_ < std::min(total, chunk)) {
     cudaFree(d_tmp_);
     d_tmp_ = nullptr;
@@ -977,7 +1037,7 @@ std::vector<TopkItem> State::top_k(uint64_t k) {
     }
     for (uint64_t off = 0; off < total; off += chunk) {
       const uint64_t c = std::min(chunk, total - off);
-      cuda_check(launch_gather(psi_, d_tmp_, off, c, pm.data(), n_, stream_), "gather");
+      cuda_check(launch_gather(psi_, d_tmp_, off, c, pm.data(), bits, stream_), "gather");
       fn(static_cast<const double2*>(d_tmp_), c, off);
     }
   };
@@ -1094,7 +1154,7 @@ double State::norm_squared() {
   if (mode_ == Mode::Sharded) {
     std::string err;
     double* gathered = d_scratch_ + kNormBlocks + 1;
-    if (!comm_->allgather_double(out, gathered, stream_, &err)) fail(QT_ERR_NCCL, err);
+    if (!comm_->allgather_double(out, gathered, 1, stream_, &err)) fail(QT_ERR_NCCL, err);
     cuda_check(cudaMemcpyAsync(parts.data(), gathered, sizeof(double) * world_,
                                cudaMemcpyDeviceToHost, stream_),
                "norm readback");

@@ -90,6 +90,7 @@ class State {
   // The k amplitudes of largest |a|^2 (ties: smaller logical index first),
   // sorted; logical indices. Single / loopback states (State::top_k).
   std::vector<TopkItem> top_k(uint64_t k);
+  std::vector<TopkItem> top_k_local(uint64_t k, int bits, const std::vector<int>& perm);
   void sync();  // also raises QT_ERR_NUMERIC if a pass saw a non-finite value
   // a call on this rank failed: release the group's other ranks
   void abort_comm(const std::string& why) {

@@ -211,6 +211,16 @@ class RankGroup:
     def apply(self, gates: np.ndarray):
         self.run(lambda st: st.apply(gates))
 
+    def top_k(self, k: int):
+        """The k largest-|amplitude|^2 basis states of the sharded state
+        (collective: every rank selects in its shard, the ranks all-gather
+        and merge); every rank returns the same list."""
+        vals = self.run(lambda st: st.top_k(k))
+        for v in vals[1:]:
+            assert np.array_equal(v[0], vals[0][0]) and np.array_equal(v[1], vals[0][1]), \
+                "ranks disagree on the top-k list"
+        return vals[0]
+
     def norm_squared(self) -> float:
         vals = self.run(lambda st: st.norm_squared())
         assert all(v == vals[0] for v in vals), "ranks disagree on the norm"

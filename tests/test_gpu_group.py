@@ -94,3 +94,43 @@ def test_group_random_circuits(gpu, seed):
     got, nrm, _ = run_group(n, g, world, basis=basis)
     assert np.abs(got - want).max() <= TOL
     assert abs(nrm - 1.0) <= NORM_TOL
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_top_k_matches_one_gpu(gpu, world):
+    """top_k on a sharded state: every rank selects in its shard (in logical
+    index order), the ranks all-gather and merge; same list (indices and the
+    stored amplitudes) as selecting from the gathered state, on every rank --
+    after a circuit with exchanges, so the qubit map is not the identity."""
+    from tests.test_gpu_topk import expected
+    w = W.config4(n=20, ngates=400)
+    g = RankGroup(w.n, world)
+    try:
+        g.apply(w.gates)
+        psi = g.read()
+        for k in (1, 50, 3000):
+            idx, amps = g.top_k(k)
+            want_i, want_a = expected(psi, k)
+            assert (idx == want_i).all()
+            assert (amps == want_a).all()
+    finally:
+        g.close()
+
+
+def test_sharded_top_k_ties(gpu):
+    """Every |a|^2 equal (H on every qubit, then exchanges through a CX ladder
+    on the top qubits): the ties break by logical index across shards."""
+    from paper_2210_01076_b200.gates import GateKind as K, gate, gate_array
+    from tests.test_gpu_topk import expected
+    n = 16
+    rows = [gate(K.H, q) for q in range(n)] + [gate(K.Rx, n - 1, -1, 0.0), gate(K.H, n - 1), gate(K.H, n - 1)]
+    g = RankGroup(n, 4)
+    try:
+        g.apply(gate_array(rows))
+        psi = g.read()
+        for k in (1, 100, 5000):
+            idx, amps = g.top_k(k)
+            want_i, _ = expected(psi, k)
+            assert (idx == want_i).all()
+    finally:
+        g.close()
