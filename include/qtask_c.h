@@ -119,6 +119,8 @@ typedef struct qt_run_stats {
   double device_ms;             /* device time of the call (CUDA events)   */
   double plan_ms;               /* host planning time                      */
   uint64_t exchange_local_bytes;/* local HBM bytes the exchanges copied    */
+  uint64_t fused_exchanges;     /* exchanges done by the pass before them
+                                   (stores straight into peer memory)     */
 } qt_run_stats;
 
 const char* qt_last_error(void);

@@ -50,7 +50,8 @@ class QtRunStats(ctypes.Structure):
                 ("hbm_bytes", ctypes.c_uint64), ("exchanged_bytes", ctypes.c_uint64),
                 ("swaps", ctypes.c_uint64), ("restart_gate", ctypes.c_uint64),
                 ("segments", ctypes.c_uint64), ("device_ms", ctypes.c_double),
-                ("plan_ms", ctypes.c_double), ("exchange_local_bytes", ctypes.c_uint64)]
+                ("plan_ms", ctypes.c_double), ("exchange_local_bytes", ctypes.c_uint64),
+                ("fused_exchanges", ctypes.c_uint64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_

@@ -857,6 +857,22 @@ int qt_jit_probe(int num_qubits, int tile_qubits, int reg_bits, int low_bits, in
       if (const char* e = std::getenv("QTB_JIT_MINB")) sp.min_blocks = std::atoi(e);
       sp.coalesce_bits = qtb::kJitDirectBits;
       if (const char* e = std::getenv("QTB_DIRECT_BITS")) sp.coalesce_bits = std::atoi(e);
+      // compile checks of the fused-exchange variant: QTB_PROBE_FUSE="v0[,v1[,v2]]"
+      // (the victim bits of a pretended exchange after every pass)
+      if (const char* e = std::getenv("QTB_PROBE_FUSE")) {
+        sp.fuse_k = 0;
+        for (const char* c = e; *c && sp.fuse_k < 3;) {
+          sp.fuse_v[sp.fuse_k++] = std::atoi(c);
+          while (*c && *c != ',') ++c;
+          if (*c == ',') ++c;
+        }
+        if (sp.ring && sp.fuse_k > 0) {
+          sp.tma_store = 0;
+          sp.kparam = false;
+        } else {
+          sp.fuse_k = 0;
+        }
+      }
       const std::string src = qtb::jit_source(sp, mp[i]);
       if (source_pass >= 0) {
         if (static_cast<size_t>(source_pass) == i) {

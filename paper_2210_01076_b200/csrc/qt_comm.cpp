@@ -272,6 +272,23 @@ bool LocalComm::sendrecv(int npeers, const int* peers, const void* const* sends,
   }, err);
 }
 
+bool LocalComm::with_peer_buffers(void* mine, const std::vector<int>& peers, cudaStream_t s,
+                                  const std::function<bool(void* const* table)>& launch,
+                                  std::string* err) {
+  {
+    std::lock_guard<std::mutex> lk(g_->mu_);
+    g_->slots_[rank_].peer_buf = mine;
+  }
+  return rendezvous(peers, s, [&] {
+    std::vector<void*> table(world_, nullptr);
+    {
+      std::lock_guard<std::mutex> lk(g_->mu_);
+      for (int p : peers) table[p] = g_->slots_[p].peer_buf;
+    }
+    return launch(table.data());
+  }, err);
+}
+
 bool LocalComm::allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                                  std::string* err) {
   LocalGroup::Slot& me = g_->slots_[rank_];

@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -42,6 +43,21 @@ class Comm {
   // (bit patterns travel unchanged: also used for packed integer records).
   virtual bool allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                                 std::string* err) = 0;
+  // Peer memory (fused exchanges, qt_state.cpp): true when this rank's kernels
+  // can store straight into the other ranks' buffers (in-process group: same
+  // device; NCCL ranks live in separate processes and would need an IPC or
+  // multicast mapping: not available here, so they keep the send/recv path).
+  virtual bool peer_access() const { return false; }
+  // Collective over `peers` (this rank included): publishes `mine`, waits
+  // (stream order) until every peer's earlier work is done, calls
+  // launch(table) with table[r] = rank r's published pointer (nullptr for
+  // ranks outside `peers`), then makes the stream wait for every peer's launch.
+  virtual bool with_peer_buffers(void* mine, const std::vector<int>& peers, cudaStream_t s,
+                                 const std::function<bool(void* const* table)>& launch,
+                                 std::string* err) {
+    if (err) *err = "transport has no peer access";
+    return false;
+  }
   virtual bool check_async(std::string* err) = 0;
   virtual const char* kind() const = 0;
   // This rank failed mid-call: release peers waiting on it (in-process
@@ -88,6 +104,7 @@ class LocalGroup {
     uint64_t read_seq = 0;   // calls whose reads this rank has issued
     std::vector<std::vector<const void*>> send_to;  // per destination rank, in order (this call)
     const double* gather_src = nullptr;
+    void* peer_buf = nullptr;  // with_peer_buffers: this rank's published buffer
     cudaEvent_t ready = nullptr;  // the rank's stream reached the call
     cudaEvent_t read = nullptr;   // the rank's reads of its peers are issued
     int device = -1;
@@ -108,6 +125,10 @@ class LocalComm : public Comm {
                 size_t bytes, cudaStream_t s, std::string* err) override;
   bool allgather_double(const double* in, double* out, size_t count, cudaStream_t s,
                         std::string* err) override;
+  bool peer_access() const override { return true; }
+  bool with_peer_buffers(void* mine, const std::vector<int>& peers, cudaStream_t s,
+                         const std::function<bool(void* const* table)>& launch,
+                         std::string* err) override;
   bool check_async(std::string*) override { return true; }
   const char* kind() const override { return "local"; }
   void abort(const std::string& why) override;

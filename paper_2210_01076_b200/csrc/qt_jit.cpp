@@ -780,6 +780,40 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
     const char* e = std::getenv("QTB_JIT_ASMSMEM");
     return e && std::atoi(e) != 0;
   }();
+  // Fused exchange: destination of the amplitude at local index x (its thread
+  // part xt = tile base + thread offset at run time, its slot part a literal):
+  //   rank   = peer[v],  v bit i = bit fuse_v[i] of x
+  //   index  = (x with the victim bits cleared) | rfix
+  // emit_fused_ptrs declares one base pointer per pattern of the victim bits
+  // that sit in the slot offsets (literal per slot); fused_ptr(s) names the
+  // pointer of slot s and fused_off(s) its literal byte offset.
+  const bool fuse = sp.fuse_k > 0;
+  uint64_t fuse_vmask = 0;
+  for (int i = 0; i < sp.fuse_k; ++i) fuse_vmask |= 1ull << sp.fuse_v[i];
+  auto fuse_pattern = [&](uint64_t off_bytes) {  // victim bits spelled by a slot's byte offset
+    uint32_t v = 0;
+    for (int i = 0; i < sp.fuse_k; ++i)
+      if ((off_bytes / 16) >> sp.fuse_v[i] & 1ull) v |= 1u << i;
+    return v;
+  };
+  auto emit_fused_ptrs = [&](const std::string& xt, const uint64_t* off) {
+    uint64_t slot_bits = 0;
+    for (int s2 = 0; s2 < NS; ++s2) slot_bits |= off[s2] / 16;
+    os << "      u32 vr = 0;\n";
+    for (int i = 0; i < sp.fuse_k; ++i)
+      if (!((slot_bits >> sp.fuse_v[i]) & 1ull))
+        os << "      vr |= static_cast<u32>((u64(" << xt << ") >> " << sp.fuse_v[i] << ") & 1ull) << " << i << ";\n";
+    os << "      const u64 xk = (u64(" << xt << ") & ~" << hexu(fuse_vmask) << ") | fx.rfix;\n";
+    std::vector<char> seen(8, 0);
+    for (int s2 = 0; s2 < NS; ++s2) {
+      const uint32_t q = fuse_pattern(off[s2]);
+      if (seen[q]) continue;
+      seen[q] = 1;
+      os << "      char* const fp" << q << " = reinterpret_cast<char*>(fx.peer[vr | " << q << "u] + xk);\n";
+    }
+  };
+  auto fused_ptr = [&](uint64_t off_bytes) { return "fp" + std::to_string(fuse_pattern(off_bytes)); };
+  auto fused_off = [&](uint64_t off_bytes) { return off_bytes & ~(fuse_vmask * 16); };
   static const bool early = [] {
     const char* e = std::getenv("QTB_JIT_EARLY");
     return !e || std::atoi(e) != 0;
@@ -796,7 +830,8 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
      // smaller tiles: several CTAs per SM (512 threads of <= 128 registers in all)
      << "extern \"C\" __global__ void __launch_bounds__(" << 2 * T << ", " << std::max(1, 512 / (2 * T)) << ")\n"
      << "qtjit(double2* psi, const double2* src, int* flag, u64 gbase_hi, u64 per"
-     << (sp.kparam ? ", const __grid_constant__ KP K" : "") << ") {\n"
+     << (sp.kparam ? ", const __grid_constant__ KP K" : "")
+     << (fuse ? ", const __grid_constant__ FX fx" : "") << ") {\n"
      << "  extern __shared__ __align__(16) double2 sm[];\n"
      << "  char* const sm0 = reinterpret_cast<char*>(sm);\n"
      << "  const u32 smbase = static_cast<u32>(__cvta_generic_to_shared(sm0));\n"
@@ -1017,6 +1052,18 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
       if (!early_refill)
         os << "      gbar(1 + grp);\n"
            << "      if (j + 3 < cnt) load(j + 3);\n";
+      if (fuse) {
+        os << "      {\n";
+        emit_fused_ptrs("base + off_dl", dl.off);
+        os << "     ";
+        for (int s2 = 0; s2 < NS; ++s2) {
+          if (sp.check) os << " bad = bad || !finite2(v" << s2 << ");";
+          os << " __stcs(reinterpret_cast<double2*>(" << fused_ptr(dl.off[s2]) << " + " << fused_off(dl.off[s2])
+             << "ull), v" << s2 << ");";
+        }
+        os << "\n      }\n    }\n";
+        continue;
+      }
       os << "      { char* gd = reinterpret_cast<char*>(psi + base + off_dl);\n     ";
       if (wdrain && cl_direct >= 3) {
         os << "\n";
@@ -1048,7 +1095,7 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   }
   if (tma) {
     // handled above
-  } else if (!dl.ok && early) {
+  } else if (!dl.ok && (early || fuse)) {
     // copy-out: the whole tile share goes to registers first, so the refill
     // of this buffer starts before the HBM stores are issued
     os << "    {\n      char* d = reinterpret_cast<char*>(psi + base + off_t);\n";
@@ -1061,8 +1108,18 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
       os << " asm volatile(\"\" : \"+d\"(x" << s2 << ".x), \"+d\"(x" << s2 << ".y));";
     os << "\n      gbar(1 + grp);\n"
        << "      if (j + 3 < cnt) load(j + 3);\n";
-    if (wdrain && cl_load >= 3) staged_drain("x", "d", sp.slot_gb, cl_load);
-    for (int s2 = 0; s2 < NS && !(wdrain && cl_load >= 3); ++s2) {
+    if (fuse) {
+      emit_fused_ptrs("base + off_t", sp.slot_gb);
+      for (int s2 = 0; s2 < NS; ++s2) {
+        os << "     ";
+        if (sp.check) os << " bad = bad || !finite2(x" << s2 << ");";
+        os << " __stcs(reinterpret_cast<double2*>(" << fused_ptr(sp.slot_gb[s2]) << " + " << fused_off(sp.slot_gb[s2])
+           << "ull), x" << s2 << ");\n";
+      }
+    } else if (wdrain && cl_load >= 3) {
+      staged_drain("x", "d", sp.slot_gb, cl_load);
+    }
+    for (int s2 = 0; s2 < NS && !fuse && !(wdrain && cl_load >= 3); ++s2) {
       os << "     ";
       if (sp.check) os << " bad = bad || !finite2(x" << s2 << ");";
       os << " " << st_guard << "__stcs(reinterpret_cast<double2*>(d + " << sp.slot_gb[s2] << "ull), x" << s2 << ");\n";
@@ -1085,6 +1142,7 @@ std::string jit_source_ring(const JitPassSpec& sp, const MicroPass& mp, std::vec
   if (sp.check) os << "  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);\n";
   os << "}\n";
   std::string head = kPrelude;
+  if (fuse) head += "struct FX { double2* peer[8]; u64 rfix; };\n";
   if (sp.kparam) {
     if (kc.vals.size() > kMaxKParams) {
       // too many constants for one parameter block: literals instead
@@ -1247,7 +1305,7 @@ std::string jit_key(const JitPassSpec& sp, const MicroPass& mp) {
   // every input of jit_source, as bytes (exact: no hash collisions)
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
-  const int32_t head[] = {sp.device, sp.debug, sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam, sp.tma_store,
+  const int32_t head[] = {sp.device, sp.debug, sp.k, sp.R, sp.check, sp.pipe, sp.pf_bits, sp.min_blocks, sp.ring, sp.kparam, sp.tma_store, sp.fuse_k, sp.fuse_v[0], sp.fuse_v[1], sp.fuse_v[2],
                           sp.coalesce_bits,
                           static_cast<int32_t>(sp.rounds.size()),
                           static_cast<int32_t>(sp.tile_phys.size()),
@@ -1281,6 +1339,7 @@ CacheEntry load_entry(const std::vector<char>& bin, const JitPassSpec& sp,
     cudaGetLastError();
     throw std::runtime_error("loading a compiled pass failed");
   }
+  e.k.fuse_k = sp.fuse_k;
   e.k.threads = (sp.ring ? 2 : 1) << (sp.k - sp.R);
   e.k.smem = sp.ring ? 3 * (sizeof(double2) << sp.k) + 64 : (sp.pipe ? 2 : 1) * (sizeof(double2) << sp.k);
   // warp-staged drain: 2 KiB per warp after the mbarriers (jit_source_ring stage_off)
@@ -1513,12 +1572,17 @@ size_t jit_pending() {
 }
 
 cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* psi,
-                       const double2* src, int* flag, uint64_t gbase_hi, cudaStream_t s) {
+                       const double2* src, int* flag, uint64_t gbase_hi, cudaStream_t s,
+                       const JitFuseParams* fuse) {
+  if ((k.fuse_k > 0) != (fuse != nullptr)) return cudaErrorInvalidValue;
   const uint64_t cap = static_cast<uint64_t>(k.occupancy) * static_cast<uint64_t>(sms);
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, cap));
   uint64_t per = (ntiles + grid - 1) / grid;
+  // parameter 6 is the constant block (kparam passes) or the fused-exchange
+  // table (never both: fused passes keep their constants as literals)
   void* args[] = {&psi, &src, &flag, &gbase_hi, &per,
-                  k.kp ? const_cast<double*>(k.kp->data()) : nullptr};
+                  fuse ? const_cast<JitFuseParams*>(fuse)
+                       : (k.kp ? static_cast<void*>(const_cast<double*>(k.kp->data())) : nullptr)};
   return cudaLaunchKernel(reinterpret_cast<const void*>(k.fn), dim3(grid), dim3(k.threads), args,
                           k.smem, s);
 }

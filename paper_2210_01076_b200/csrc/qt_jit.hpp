@@ -57,6 +57,13 @@ struct JitPassSpec {
   //    later; 2: every warp drains its own results through a 2 KiB staging
   //    area (two halves of 1 KiB), waiting on its own bulk reads only
   int tma_store = 0;
+  // Fused exchange (ring kernel, sharded states with peer memory): the pass
+  // before an exchange of k global bits stores every amplitude straight to
+  // its place after the exchange -- rank and local index decided by the
+  // amplitude's k victim bits (local physical bits fuse_v[i]) -- through a
+  // table of the peers' buffers passed as a kernel parameter.
+  int fuse_k = 0;
+  int fuse_v[3] = {0, 0, 0};
   int min_blocks = 0;   // launch bounds (0 = by R: <= 64 registers for R <= 3, <= 128 for R = 4)
   std::vector<DRound> rounds;  // reg / sreg / sbit per round
   std::vector<int> tile_phys;  // physical bit of each tile bit (ascending)
@@ -65,7 +72,16 @@ struct JitPassSpec {
   int coalesce_bits = 0;
 };
 
+// Kernel parameter of a fused-exchange pass: peer[v] = the buffer of the rank
+// that owns the amplitudes whose victim bits spell v; rfix = this rank's global
+// bits deposited at the victim positions (the local index after the exchange).
+struct JitFuseParams {
+  double2* peer[8];
+  unsigned long long rfix;
+};
+
 struct JitKernel {
+  int fuse_k = 0;  // > 0: a fused-exchange pass (takes a JitFuseParams)
   cudaKernel_t fn = nullptr;
   int threads = 0;
   size_t smem = 0;
@@ -107,7 +123,7 @@ constexpr size_t kJitStackBytes = size_t(256) << 20;  // per compile thread (res
 
 // Launches a compiled pass (grid = occupancy x SMs, capped by the tiles).
 cudaError_t jit_launch(const JitKernel& k, uint64_t ntiles, int sms, double2* psi,
-                       const double2* src, int* flag, uint64_t gbase_hi, cudaStream_t s);
+                       const double2* src, int* flag, uint64_t gbase_hi, cudaStream_t s, const JitFuseParams* fuse = nullptr);
 
 // NVRTC compile only (no device needed): CUBIN bytes of a source.
 std::vector<char> jit_compile_cubin(const std::string& src);

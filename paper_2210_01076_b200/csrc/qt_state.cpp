@@ -377,6 +377,7 @@ void State::apply(const qt_gate* gates, size_t count) {
   }
   fuse_ops(ops, n_);
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  decide_fusion();
   const auto t0 = std::chrono::steady_clock::now();
   last_.valid = false;
   last_.plan = plan(ops);
@@ -569,6 +570,14 @@ State::Prepared State::prepare(const Plan& plan) {
       sp.min_blocks = jit_min_blocks_;
       sp.device = device_;
       sp.coalesce_bits = direct_bits_;
+      if (fuse_ok_ && sp.ring && pi + 1 < plan.passes.size() &&
+          plan.passes[pi + 1].kind == PlanPass::Exchange && plan.passes[pi + 1].exchange.size() <= 3) {
+        const PlanPass& ex = plan.passes[pi + 1];
+        sp.fuse_k = static_cast<int>(ex.exchange.size());
+        for (int i = 0; i < sp.fuse_k; ++i) sp.fuse_v[i] = ex.exchange[i].second;
+        sp.tma_store = 0;
+        sp.kparam = false;
+      }
       if (pf_ && !sp.pipe) {
         int run = 0;
         while (run < sp.k - sp.R && ps.tile_phys[run] == run) ++run;
@@ -641,12 +650,58 @@ void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2*
     if (plan.passes[pi].kind == PlanPass::Tile) last_tile = pi;
   for (size_t pi = 0; pi < plan.passes.size(); ++pi) {
     const PlanPass& ps = plan.passes[pi];
+    if (ps.kind == PlanPass::Exchange && pi > 0 && jk[pi - 1].fuse_k > 0) continue;  // done by the pass before it
     if (ps.kind == PlanPass::Exchange) {
       tstart(1);
       exchange(ps);
       tstop();
       stats.swaps += 1;
       stats.kernel_launches += ps.exchange.size();
+      continue;
+    }
+    if (jk[pi].fn && jk[pi].fuse_k > 0) {
+      // pass + exchange in one kernel: stores go to the peers' second buffers
+      const PlanPass& ex = plan.passes[pi + 1];
+      const int k = static_cast<int>(ex.exchange.size());
+      std::vector<int> group;  // the 2^k ranks that differ from this one in the exchanged rank bits
+      uint64_t rfix = 0;
+      for (uint32_t v = 0; v < (1u << k); ++v) {
+        int r = rank_;
+        for (int i = 0; i < k; ++i) {
+          const int gb = ex.exchange[i].first - nlocal_;
+          r = (r & ~(1 << gb)) | (static_cast<int>((v >> i) & 1u) << gb);
+        }
+        group.push_back(r);
+      }
+      for (int i = 0; i < k; ++i)
+        if ((rank_ >> (ex.exchange[i].first - nlocal_)) & 1) rfix |= 1ull << ex.exchange[i].second;
+      const double2* rd = src ? src : psi_;
+      src = nullptr;
+      tstart(0);
+      std::string err;
+      std::vector<int> sorted_group(group);
+      std::sort(sorted_group.begin(), sorted_group.end());
+      const bool ok = comm_->with_peer_buffers(alt_, sorted_group, stream_, [&](void* const* table) {
+        JitFuseParams fx{};
+        for (uint32_t v = 0; v < (1u << k); ++v) {
+          if (!table[group[v]]) return false;
+          fx.peer[v] = static_cast<double2*>(table[group[v]]);
+        }
+        fx.rfix = rfix;
+        return jit_launch(jk[pi], 1ull << (buf_bits_ - static_cast<int>(ps.tile_phys.size())), sms_, psi_, rd,
+                          d_flag_, static_cast<uint64_t>(rank_) << nlocal_, stream_, &fx) == cudaSuccess;
+      }, &err);
+      if (!ok) fail(QT_ERR_NCCL, err.empty() ? "fused exchange failed" : err);
+      tstop();
+      std::swap(psi_, alt_);
+      pool_[0] = psi_;
+      const uint64_t region = 1ull << (nlocal_ - k);
+      stats.passes += 1;
+      stats.swaps += 1;
+      stats.fused_exchanges += 1;
+      stats.kernel_launches += 1;
+      stats.hbm_bytes += 2ull * sizeof(double2) * buffer_amps();
+      stats.exchanged_bytes += static_cast<uint64_t>((1 << k) - 1) * region * sizeof(double2);
       continue;
     }
     if (jk[pi].fn) {
@@ -854,6 +909,50 @@ void own_region(int rank, int nlocal, const std::vector<std::pair<int, int>>& ex
 
 }  // namespace
 
+// The second shard buffer of the two-buffer exchange, allocated once when it fits.
+void State::ensure_alt() {
+  if (alt_ || alt_tried_ || bound_ != 0) return;
+  // one decision at a time per process (emulated ranks share a device)
+  static std::mutex alloc_mu;
+  std::lock_guard<std::mutex> lk(alloc_mu);
+  alt_tried_ = true;
+  size_t fr = 0, tot = 0;
+  const size_t bytes = sizeof(double2) << nlocal_;
+  if (!no_alt_ && cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > bytes + (size_t(4) << 30)) {
+    if (cudaMalloc(&alt_, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      alt_ = nullptr;
+    }
+  }
+}
+
+// Fused exchanges (compiled mode, transports with peer memory): the pass
+// before an exchange stores every amplitude straight to the rank and index it
+// has after the exchange, so the exchange costs no HBM traffic of its own and
+// its transfer overlaps the pass's arithmetic. Every rank must take the same
+// path: decided once, collectively (all ranks hold a second shard buffer).
+void State::decide_fusion() {
+  if (fuse_decided_) return;
+  fuse_decided_ = true;
+  fuse_ok_ = false;
+  if (mode_ != Mode::Sharded || !comm_ || !comm_->peer_access() || jit_mode_ != 1 || world_ > 8) return;
+  if (const char* e = std::getenv("QTB_FUSE_EXCHANGE"))
+    if (std::atoi(e) == 0) return;
+  ensure_alt();
+  double* mine = d_scratch_ + kNormBlocks;
+  double* all = d_scratch_ + kNormBlocks + 1;
+  const double have = (alt_ && bound_ == 0) ? 1.0 : 0.0;
+  cuda_check(cudaMemcpyAsync(mine, &have, sizeof(double), cudaMemcpyHostToDevice, stream_), "fusion vote");
+  std::string err;
+  if (!comm_->allgather_double(mine, all, 1, stream_, &err)) fail(QT_ERR_NCCL, err);
+  std::vector<double> votes(world_, 0.0);
+  cuda_check(cudaMemcpyAsync(votes.data(), all, sizeof(double) * world_, cudaMemcpyDeviceToHost, stream_),
+             "fusion vote readback");
+  cuda_check(cudaStreamSynchronize(stream_), "fusion vote sync");
+  fuse_ok_ = true;
+  for (double v : votes) fuse_ok_ = fuse_ok_ && v == 1.0;
+}
+
 void State::exchange(const PlanPass& pass) {
   if (mode_ == Mode::Loopback) {
     for (const auto& gv : pass.exchange)
@@ -881,20 +980,7 @@ void State::exchange(const PlanPass& pass) {
   // buffers swap roles -- the only HBM traffic beyond the transfer itself is
   // that 1/2^k of the shard (the receive-buffer scheme below copies the other
   // (2^k-1)/2^k back out of the receive buffer).
-  if (!alt_ && !alt_tried_ && bound_ == 0) {
-    // one decision at a time per process (emulated ranks share a device)
-    static std::mutex alloc_mu;
-    std::lock_guard<std::mutex> lk(alloc_mu);
-    alt_tried_ = true;
-    size_t fr = 0, tot = 0;
-    const size_t bytes = sizeof(double2) << nlocal_;
-    if (!no_alt_ && cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > bytes + (size_t(4) << 30)) {
-      if (cudaMalloc(&alt_, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        alt_ = nullptr;
-      }
-    }
-  }
+  ensure_alt();
   const bool two = alt_ && bound_ == 0;
   if (!two && d_tmp_amps_ < cap) {
     static std::mutex alloc_mu2;

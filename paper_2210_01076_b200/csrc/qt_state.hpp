@@ -193,6 +193,9 @@ class State {
   // compiled passes: first / last round straight from / to HBM when physical
   // bits [0, direct_bits_) stay thread bits (128-B runs); 0 = always stage
   int direct_bits_ = kJitDirectBits;
+  void ensure_alt();
+  void decide_fusion();
+  bool fuse_decided_ = false, fuse_ok_ = false;  // fused exchanges (collective decision, first apply)
   int window_mode_ = -1;  // QTB_WINDOW_SEARCH: -1 auto (plan-search candidate), 0 never, 1 always
   int occupancy_ = 1, sms_ = 148;
   bool timing_ = false;

@@ -83,6 +83,32 @@ def test_group_compiled_passes(gpu, world):
     assert abs(nrm - 1.0) <= NORM_TOL
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_fused_exchange_equals_send_recv(gpu, world, monkeypatch):
+    """Compiled mode on a transport with peer memory fuses every exchange into
+    the pass before it (the pass stores each amplitude straight to the rank
+    and index it has after the exchange): no exchange step, no local copy
+    traffic, and bit for bit the state of the send/recv path
+    (QTB_FUSE_EXCHANGE=0) -- both against the oracle."""
+    w = W.config4(n=22, ngates=600)
+    want = oracle.simulate(w.n, lower_to_reference(w.gates))
+    fused, nrm, stats = run_group(w.n, w.gates, world, compiled=True)
+    assert np.abs(fused - want).max() <= TOL
+    assert abs(nrm - 1.0) <= NORM_TOL
+    assert stats[0]["swaps"] > 0
+    # exchanges whose preceding pass is a compiled tile pass are fused
+    assert stats[0]["fused_exchanges"] > 0
+    assert len({s["fused_exchanges"] for s in stats}) == 1
+    monkeypatch.setenv("QTB_FUSE_EXCHANGE", "0")
+    plain, nrm2, stats2 = run_group(w.n, w.gates, world, compiled=True)
+    assert stats2[0]["fused_exchanges"] == 0
+    assert stats2[0]["swaps"] == stats[0]["swaps"]
+    assert stats2[0]["exchanged_bytes"] == stats[0]["exchanged_bytes"]
+    assert stats[0]["exchange_local_bytes"] < stats2[0]["exchange_local_bytes"]
+    assert np.array_equal(fused, plain)
+    assert nrm == nrm2
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_group_random_circuits(gpu, seed):
     rng = np.random.default_rng(700 + seed)
