@@ -287,6 +287,23 @@ double plan_cost_ms(const Plan& p, int reg_bits, int nlocal) {
 // built in parallel and the one with the least estimated time (plan_cost_ms)
 // wins (C3: 22 -> 18 passes, 196 -> 180 ms).
 Plan State::plan(const std::vector<LOp>& ops) const {
+  if (jit_mode_ == 0 && nlocal_ >= kPlanSearchMinBits && opt_.max_pass_fp64 <= 0.0 && plan_search_ &&
+      window_mode_ < 0) {
+    // interpreter (one-shot applies): the first-need greedy plan against the
+    // beam-searched window plan, by the same cost model (C3: 37 -> 18 passes,
+    // 346 -> 305 ms; random circuits keep the greedy plan)
+    Plan greedy, window;
+    PlanOptions ow = opt_;
+    ow.window_search = true;
+    ow.window_beam = kPlanBeamWidth;
+    std::thread tw([&] { window = make_plan(ops, n_, nlocal_, perm_, ow); });
+    greedy = make_plan(ops, n_, nlocal_, perm_, opt_);
+    tw.join();
+    if (window.passes.size() >= greedy.passes.size()) return greedy;
+    return plan_cost_ms(window, opt_.reg_bits, nlocal_) < plan_cost_ms(greedy, opt_.reg_bits, nlocal_) - 1e-9
+               ? window
+               : greedy;
+  }
   if (jit_mode_ != 1 || nlocal_ < kPlanSearchMinBits || opt_.max_pass_fp64 > 0.0 || !plan_search_)
     return make_plan(ops, n_, nlocal_, perm_, opt_);
   // Phase 1 candidates: every cap with the first-need greedy tiles and with
