@@ -218,6 +218,37 @@ def test_plan_search_window_plan_vs_oracle(gpu):
 
 
 @pytest.mark.gpu
+def test_config3_full_size_two_independent_paths(gpu, monkeypatch):
+    """The headline config at its full 30 qubits through two device paths that
+    share no plan, tile geometry or kernel: the compiled ring passes of the
+    searched plan (R = 4, 2^12 tiles, window + beam) and the layer-word
+    interpreter on the first-need greedy plan (R = 3, 2^10 tiles,
+    QTB_PLAN_SEARCH=0). 2^18 amplitudes sampled in 64 runs across the state
+    and the norms must agree to 1e-12 (each path matches the oracle at 24
+    qubits in test_plan_search_window_plan_vs_oracle / test_gpu_state)."""
+    w = W.config3()
+    rng = np.random.default_rng(30)
+    starts = np.sort(rng.integers(0, (1 << 30) - (1 << 12), size=64))
+
+    def sample(st):
+        return np.concatenate([st.read(int(a), 1 << 12) for a in starts])
+
+    st = StateVector(30, compiled=True)
+    st.apply(w.gates)
+    a, na, pa = sample(st), st.norm_squared(), st.stats()["passes"]
+    st.close()
+    monkeypatch.setenv("QTB_PLAN_SEARCH", "0")
+    st = StateVector(30, compiled=False)
+    st.apply(w.gates)
+    b, nb, pb = sample(st), st.norm_squared(), st.stats()["passes"]
+    st.close()
+    assert pa < pb
+    assert np.abs(a - b).max() <= 1e-12
+    assert abs(na - 1) <= NORM_TOL and abs(nb - 1) <= NORM_TOL
+    assert np.abs(a).max() > 0
+
+
+@pytest.mark.gpu
 def test_compiled_config3_full_size_mirror(gpu):
     """The headline config at its full size (30 q, 16 GiB) in compiled mode:
     C then C^dagger returns |0...0> (no CPU state needed), norm after C."""
