@@ -45,6 +45,7 @@ constexpr double kPlanFp64PerS = 1.67e13;
 constexpr double kPlanHbmBytesPerS = 5.87e12;
 constexpr double kPlanExposedHbm = 0.56;  // share of a pass's HBM time not hidden under its FP64 time
 constexpr int kPlanSearchMinBits = 24;
+constexpr size_t kPlanBeamMaxOps = 20000;  // fused ops; larger circuits keep the phase-1 plan
 constexpr int kPlanBeamWidth = 16;  // window beam of the plan search's second phase
 
 // Merges runs of uncontrolled single-qubit ops on the same qubit into one

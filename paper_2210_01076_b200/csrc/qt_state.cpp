@@ -287,6 +287,9 @@ double plan_cost_ms(const Plan& p, int reg_bits, int nlocal) {
 // built in parallel and the one with the least estimated time (plan_cost_ms)
 // wins (C3: 22 -> 18 passes, 196 -> 180 ms).
 Plan State::plan(const std::vector<LOp>& ops) const {
+  // the beam search visits (beam x windows x passes) fills: bounded to circuits
+  // it finishes on in well under a second
+  const bool beam_ok = ops.size() <= kPlanBeamMaxOps;
   if (jit_mode_ == 0 && nlocal_ >= kPlanSearchMinBits && opt_.max_pass_fp64 <= 0.0 && plan_search_ &&
       window_mode_ < 0) {
     // interpreter (one-shot applies): the first-need greedy plan against the
@@ -295,7 +298,7 @@ Plan State::plan(const std::vector<LOp>& ops) const {
     Plan greedy, window;
     PlanOptions ow = opt_;
     ow.window_search = true;
-    ow.window_beam = kPlanBeamWidth;
+    ow.window_beam = beam_ok ? kPlanBeamWidth : 0;
     std::thread tw([&] { window = make_plan(ops, n_, nlocal_, perm_, ow); });
     greedy = make_plan(ops, n_, nlocal_, perm_, opt_);
     tw.join();
@@ -355,7 +358,7 @@ Plan State::plan(const std::vector<LOp>& ops) const {
   double best_cost = std::numeric_limits<double>::infinity();
   Cand best_cand{0.0, false, 0, opt_.low_bits};
   run(c1, &best, &best_cost, &best_cand);
-  if (best_cand.window && window_mode_ < 0 && opt_.window_beam <= 1) {
+  if (best_cand.window && window_mode_ < 0 && opt_.window_beam <= 1 && beam_ok) {
     std::vector<Cand> c2;
     for (double c : caps) {
       c2.push_back(Cand{c, true, kPlanBeamWidth, opt_.low_bits});
