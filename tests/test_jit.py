@@ -48,6 +48,43 @@ def test_generated_passes_compile(name):
         assert js["lowered"] >= 1 and js["cubin_bytes"] > 0
 
 
+_VARIANT_SCRIPT = """
+import json, sys
+sys.path.insert(0, %r)
+from paper_2210_01076_b200 import workloads as W
+from paper_2210_01076_b200._ffi import jit_probe
+out = []
+for w in (W.config3(n=16, layers=3), W.config5(n=16, ngates=120, nmods=0)):
+    js = json.loads(jit_probe(w.n, w.gates, tile_qubits=12, reg_bits=4, compile=True))
+    src = jit_probe(w.n, w.gates, tile_qubits=12, reg_bits=4, source_pass=0)
+    out.append({"lowered": js["lowered"], "compiled": js["compiled"], "fuse": "fx.peer[" in src and "fx.rfix" in src,
+                "bulk": "cp.async.bulk.global.shared::cta" in src})
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{"QTB_PROBE_FUSE": "13,12"}, {"QTB_PROBE_FUSE": "13,12,5"},
+                                 {"QTB_JIT_TMA": "1"}, {"QTB_JIT_TMA": "2"}, {"QTB_JIT_EARLY": "0"},
+                                 {"QTB_SHRINK_MIN": "10"}])
+def test_ring_kernel_variants_compile(env):
+    """The ring kernel's variants keep compiling for sm_100a (each in its own
+    process: the switches are read once): the fused-exchange stores (victim
+    bits on outer, thread and register positions), the two TMA-store
+    experiments, the late refill and the shrunk tiles."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    run = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT % root], capture_output=True, text=True,
+                         env=dict(os.environ, QTB_JIT_CACHE_DIR="off", **env), timeout=600)
+    assert run.returncode == 0, run.stderr[-2000:]
+    for rec in json.loads(run.stdout.strip().splitlines()[-1]):
+        assert rec["lowered"] >= 1 and rec["compiled"] == rec["lowered"]
+        if "QTB_PROBE_FUSE" in env:
+            assert rec["fuse"]
+        if env.get("QTB_JIT_TMA"):
+            assert rec["bulk"]
+
+
 _DISK_SCRIPT = """
 import json, sys
 sys.path.insert(0, %r)
