@@ -249,9 +249,14 @@ def jit_probe(n: int, gates, tile_qubits: int = 0, reg_bits: int = 0, low_bits: 
     need = ctypes.c_size_t(0)
     args = (n, tile_qubits, reg_bits, low_bits, 1 if compile else 0, source_pass, g.ctypes.data, len(g))
     check(lib().qt_jit_probe(*args, None, 0, ctypes.byref(need)))
-    buf = ctypes.create_string_buffer(need.value)
-    check(lib().qt_jit_probe(*args, buf, need.value, ctypes.byref(need)))
-    return buf.value.decode()
+    while True:
+        # the text carries timings (compile_ms): its length can differ by a few
+        # bytes between the sizing call and the filling one
+        cap = need.value + 64
+        buf = ctypes.create_string_buffer(cap)
+        check(lib().qt_jit_probe(*args, buf, cap, ctypes.byref(need)))
+        if need.value <= cap:
+            return buf.value.decode()
 
 
 def jit_stats() -> dict:
