@@ -323,6 +323,8 @@ def main():
                          "(built during warm-up, cached by source); interpreted: the lean "
                          "kernel interprets layer words")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-hbm-bound", action="store_true",
+                    help="skip the HBM-bound context measurement (config 5 as one full simulation)")
     ap.add_argument("--incremental-mods", type=int, default=24,
                     help="config-5 modifiers measured after the headline (0: skip)")
     args = ap.parse_args()
@@ -550,6 +552,31 @@ def main():
         sti.close()
         line["interpreted"] = {"ms_per_step": ims, "value": G * amps / (ims * 1e-3),
                                "kernel": "tile_pass_kernel (qt_tilepass.cu, layer-word interpreter)"}
+    if compiled and world == 1 and args.workload == "c3" and not args.no_hbm_bound:
+        # the HBM-bound workload class beside the FP64-bound headline: BASELINE
+        # config 5's circuit (28 q, 5000 random gates) as one full simulation;
+        # its passes are light, so their time is the streaming time plus what
+        # the kernel fails to hide
+        try:
+            w5 = workload("c5")
+            s5 = StateVector(w5.n, device=local, compiled=True)
+            s5.set_timing(True)
+            for _ in range(2):
+                s5.set_basis(w5.basis)
+                s5.apply(w5.gates)
+                s5.sync()
+                t5 = [ms for kind, ms in s5.last_timings() if kind == 0]
+            s5.close()
+            avg5 = statistics.mean(t5)
+            gbs5 = 32.0 * float(1 << w5.n) / (avg5 * 1e-3) / 1e9
+            line["roofline_hbm_bound"] = {
+                "workload": w5.name, "qubits": w5.n, "passes": len(t5), "ms_per_step": sum(t5),
+                "avg_launch_ms": avg5, "achieved": gbs5, "peak": hbm_peak, "unit": "GB/s",
+                "frac": gbs5 / hbm_peak,
+                "note": "same ring kernel on a random circuit (about 66 gates per pass): the passes "
+                        "are HBM-bound; second apply, CUDA events per pass"}
+        except Exception as e:  # context only, never fatal for the headline line
+            line["roofline_hbm_bound"] = {"error": f"{type(e).__name__}: {e}"}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_reference(w)
         line["cpu_multicore"] = cpu_port_multicore(w)
