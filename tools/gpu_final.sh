@@ -6,4 +6,5 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; 
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc=$?
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref rc=$?
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline --incremental-mods 0 > gpurun_out/bench_torchrun1.json 2> gpurun_out/bench_torchrun1.err; echo torchrun rc=$?
-cut -c1-300 gpurun_out/bench_torchrun1.json
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-hbm-bound --incremental-mods 0 > gpurun_out/bench_small.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-hbm-bound --incremental-mods 0 > gpurun_out/ncu_launch.log 2>&1; echo launches rc=$?
