@@ -9,15 +9,16 @@ from paper_2210_01076_b200 import Config, Simulator, jit_wait, workloads as W  #
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=30)
+ap.add_argument("--seg", type=int, default=0)
 args = ap.parse_args()
 w = W.config3(n=args.n, layers=20)
-sim = Simulator(w.n, Config())
+sim = Simulator(w.n, Config(segment_gates=args.seg))
 drv = W.NetDriver(sim)
 drv.build(w.gates)
 t0 = time.perf_counter(); sim.update_state(); cold = (time.perf_counter() - t0) * 1e3
 st = sim.last_update()
 jit_wait(300)
-out = {"n": w.n, "gates": len(w.gates), "cold_full_ms": cold, "passes": st.passes, "segments": st.segments}
+out = {"seg": args.seg, "n": w.n, "gates": len(w.gates), "cold_full_ms": cold, "passes": st.passes, "segments": st.segments}
 from paper_2210_01076_b200.gates import GateKind as K
 lat = []
 for rep in range(4):
