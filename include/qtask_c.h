@@ -356,6 +356,15 @@ int qt_exchange_schedule(int rank, int nlocal, int k, const int* gbit, const int
                          uint64_t tmp_amps, uint64_t* rows, size_t cap, size_t* count,
                          uint64_t* piece);
 
+/* Host-only audit of a fused exchange (the compiled pass in front of an
+ * exchange stores straight into the peers' buffers): for `rank` and the k
+ * pairs (global bit gbit[j] above the local bits, local victim bit vbit[j]),
+ * peer_rank[v] (2^k entries) = the rank that receives the amplitudes whose
+ * victim bits spell v, *rfix = the bits set at the victim positions of the
+ * index they land at: local index x -> (x with the victim bits cleared) | rfix. */
+int qt_fused_exchange_map(int rank, int nlocal, int k, const int* gbit, const int* vbit,
+                          int* peer_rank, uint64_t* rfix);
+
 /* Host-only audit of the circuit's net order index (csrc/qt_netindex.hpp, the
  * O(log nets) replacement of the list walks of circuit.cpp:67-120): drives
  * `ops` seeded random net inserts / removals and gate-count changes into the

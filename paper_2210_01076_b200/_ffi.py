@@ -73,7 +73,7 @@ HEADER_SYMBOLS = [
     "qt_sim_amplitudes", "qt_sim_norm_squared", "qt_sim_last_update",
     "qt_sim_num_gates", "qt_sim_num_nets", "qt_sim_net_order", "qt_sim_net_gates",
     "qt_sim_gate_info", "qt_sim_export_gates", "qt_qasm_parse", "qt_qasm_build",
-    "qt_exchange_schedule", "qt_top_k", "qt_sim_top_k", "qt_netindex_audit",
+    "qt_exchange_schedule", "qt_top_k", "qt_sim_top_k", "qt_netindex_audit", "qt_fused_exchange_map",
     "qt_sim_update_account", "qt_sim_model_snapshot", "qt_sim_node_name", "qt_sim_dump_graph",
     "qt_gate_matrix", "qt_classify_gate",
     "qt_pm_create", "qt_pm_destroy", "qt_pm_insert_net", "qt_pm_remove_net", "qt_pm_insert_gate",
@@ -169,6 +169,7 @@ _SIGS = {
                        _c.POINTER(_c.c_int)], _c.c_int),
     "qt_top_k": ([_vp, _c.c_uint64, _vp, _vp, _c.POINTER(_c.c_uint64)], _c.c_int),
     "qt_sim_top_k": ([_vp, _c.c_uint64, _vp, _vp, _c.POINTER(_c.c_uint64)], _c.c_int),
+    "qt_fused_exchange_map": ([_c.c_int, _c.c_int, _c.c_int, _vp, _vp, _vp, _c.POINTER(_c.c_uint64)], _c.c_int),
     "qt_netindex_audit": ([_c.c_uint64, _c.c_uint32, _c.POINTER(_c.c_uint64)], _c.c_int),
     "qt_exchange_schedule": ([_c.c_int, _c.c_int, _c.c_int, _vp, _vp, _c.c_uint64, _vp,
                               _c.c_size_t, _c.POINTER(_c.c_size_t),
@@ -283,6 +284,19 @@ def jit_wait(timeout_s: float = 120.0) -> bool:
         if time.time() > t_end:
             return False
         time.sleep(0.05)
+
+
+def fused_exchange_map(rank: int, nlocal: int, pairs):
+    """(peer ranks by victim-bit pattern, rfix) of a fused exchange on `rank`
+    (qt_fused_exchange_map); pairs: (global bit above the local bits, victim bit)."""
+    k = len(pairs)
+    g = np.array([p[0] for p in pairs], dtype=np.int32)
+    v = np.array([p[1] for p in pairs], dtype=np.int32)
+    peers = np.zeros(1 << k, dtype=np.int32)
+    rfix = ctypes.c_uint64(0)
+    check(lib().qt_fused_exchange_map(rank, nlocal, k, g.ctypes.data, v.ctypes.data, peers.ctypes.data,
+                                      ctypes.byref(rfix)))
+    return peers, rfix.value
 
 
 def netindex_audit(seed: int, ops: int) -> int:

@@ -917,6 +917,21 @@ int qt_jit_disk_stats(uint64_t* disk_hits, uint64_t* disk_writes) {
   return QT_OK;
 }
 
+int qt_fused_exchange_map(int rank, int nlocal, int k, const int* gbit, const int* vbit,
+                          int* peer_rank, uint64_t* rfix) {
+  if (!gbit || !vbit || !peer_rank || !rfix) return null_arg();
+  return guard([&] {
+    if (k < 1 || k > 3 || nlocal < 1) qtb::fail(QT_ERR_ARG, "fused exchange of 1..3 bits");
+    std::vector<std::pair<int, int>> ex;
+    for (int i = 0; i < k; ++i) ex.emplace_back(nlocal + gbit[i], vbit[i]);
+    std::vector<int> group;
+    uint64_t fix = 0;
+    qtb::fused_exchange_map(rank, nlocal, ex, &group, &fix);
+    for (size_t v = 0; v < group.size(); ++v) peer_rank[v] = group[v];
+    *rfix = fix;
+  });
+}
+
 int qt_netindex_audit(uint64_t seed, uint32_t ops, uint64_t* mismatches) {
   if (!mismatches) return null_arg();
   return guard([&] {

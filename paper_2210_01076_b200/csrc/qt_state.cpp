@@ -685,16 +685,7 @@ void State::launch_prepared(const Plan& plan, const Prepared& pr, const double2*
       const int k = static_cast<int>(ex.exchange.size());
       std::vector<int> group;  // the 2^k ranks that differ from this one in the exchanged rank bits
       uint64_t rfix = 0;
-      for (uint32_t v = 0; v < (1u << k); ++v) {
-        int r = rank_;
-        for (int i = 0; i < k; ++i) {
-          const int gb = ex.exchange[i].first - nlocal_;
-          r = (r & ~(1 << gb)) | (static_cast<int>((v >> i) & 1u) << gb);
-        }
-        group.push_back(r);
-      }
-      for (int i = 0; i < k; ++i)
-        if ((rank_ >> (ex.exchange[i].first - nlocal_)) & 1) rfix |= 1ull << ex.exchange[i].second;
+      fused_exchange_map(rank_, nlocal_, ex.exchange, &group, &rfix);
       const double2* rd = src ? src : psi_;
       src = nullptr;
       tstart(0);
@@ -928,6 +919,28 @@ void own_region(int rank, int nlocal, const std::vector<std::pair<int, int>>& ex
 }
 
 }  // namespace
+
+// Destination map of a fused exchange on `rank`: group[v] = the rank that owns,
+// after the exchange, the amplitudes whose k victim bits spell v (bit i of v =
+// bit exchange[i].second of the local index); rfix = this rank's exchanged
+// rank bits deposited at the victim positions -- the amplitude at local index x
+// moves to rank group[v(x)], local index (x with the victim bits cleared) | rfix.
+void fused_exchange_map(int rank, int nlocal, const std::vector<std::pair<int, int>>& exchange,
+                        std::vector<int>* group, uint64_t* rfix) {
+  const int k = static_cast<int>(exchange.size());
+  group->clear();
+  *rfix = 0;
+  for (uint32_t v = 0; v < (1u << k); ++v) {
+    int r = rank;
+    for (int i = 0; i < k; ++i) {
+      const int gb = exchange[i].first - nlocal;
+      r = (r & ~(1 << gb)) | (static_cast<int>((v >> i) & 1u) << gb);
+    }
+    group->push_back(r);
+  }
+  for (int i = 0; i < k; ++i)
+    if ((rank >> (exchange[i].first - nlocal)) & 1) *rfix |= 1ull << exchange[i].second;
+}
 
 // The second shard buffer of the two-buffer exchange, allocated once when it fits.
 void State::ensure_alt() {

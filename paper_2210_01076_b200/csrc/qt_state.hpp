@@ -18,6 +18,10 @@
 
 namespace qtb {
 
+// Destination map of a fused exchange (qt_state.cpp; audited by qt_fused_exchange_map).
+void fused_exchange_map(int rank, int nlocal, const std::vector<std::pair<int, int>>& exchange,
+                        std::vector<int>* group, uint64_t* rfix);
+
 // Thrown inside the library; the C API converts it to a status code.
 struct QtError {
   int code;

@@ -181,3 +181,82 @@ def test_exchange_schedule_all_ranks(g, k, tmp_div):
         perm = perm & ~((1 << G) | (1 << vb)) | (bg << vb) | (bv << G)
     want = full[perm]
     assert np.abs(got - want).max() == 0.0
+
+
+def _fused_worker(rank, world, port, nlocal, pairs, seed, q):
+    """Every rank scatters its shard as the fused pass would (amplitude x goes
+    to rank peer[v(x)], index (x & ~V) | rfix, from the library's own map) and
+    compares what it receives with the send/recv exchange of the same shards."""
+    from paper_2210_01076_b200._ffi import fused_exchange_map
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        rng = np.random.default_rng(seed + rank)
+        shard = rng.normal(size=1 << nlocal) + 1j * rng.normal(size=1 << nlocal)
+        want = exchange_gloo(shard, pairs, rank, nlocal)
+        peers, rfix = fused_exchange_map(rank, nlocal, [(g - nlocal, v) for g, v in pairs])
+        x = np.arange(1 << nlocal, dtype=np.uint64)
+        vmask = 0
+        vpat = np.zeros(1 << nlocal, dtype=np.int64)
+        for i, (_, vb) in enumerate(pairs):
+            vmask |= 1 << vb
+            vpat |= (((x >> np.uint64(vb)) & np.uint64(1)).astype(np.int64) << i)
+        dest_rank = peers[vpat]
+        dest_idx = (x & np.uint64(~vmask & ((1 << nlocal) - 1))) | np.uint64(rfix)
+        # the "peer stores": one (indices, values) message per destination rank
+        send = []
+        for r in range(world):
+            sel = dest_rank == r
+            idx = dest_idx[sel].astype(np.int64)
+            val = shard[sel]
+            send.append(torch.from_numpy(np.concatenate([idx.astype(np.float64), val.view(np.float64)])))
+        # ragged messages: exchanged pairwise (sizes first)
+        got = np.zeros(1 << nlocal, dtype=np.complex128)
+        filled = np.zeros(1 << nlocal, dtype=bool)
+        for r in range(world):
+            if r == rank:
+                msg = send[r]
+            else:
+                n_out = torch.tensor([len(send[r])], dtype=torch.int64)
+                n_in = torch.zeros(1, dtype=torch.int64)
+                reqs = [dist.isend(n_out, r), dist.irecv(n_in, r)]
+                for rq in reqs:
+                    rq.wait()
+                msg = torch.empty(int(n_in.item()), dtype=torch.float64)
+                reqs = []
+                if len(send[r]):
+                    reqs.append(dist.isend(send[r], r))
+                if len(msg):
+                    reqs.append(dist.irecv(msg, r))
+                for rq in reqs:
+                    rq.wait()
+            m = msg.numpy()
+            cnt = len(m) // 3
+            idx = m[:cnt].astype(np.int64)
+            got[idx] = m[cnt:].view(np.complex128)
+            assert not filled[idx].any()
+            filled[idx] = True
+        assert filled.all()
+        q.put((rank, bool(np.array_equal(got, want))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,pairs", [(2, [(8, 7)]), (2, [(8, 2)]), (4, [(9, 7), (8, 3)]), (4, [(9, 0)]),
+                                         (8, [(10, 7), (9, 6), (8, 1)])])
+def test_fused_exchange_map_equals_send_recv(world, pairs):
+    """The destination map of the fused exchange (qt_fused_exchange_map: what
+    the compiled pass's stores follow) moves every amplitude exactly where the
+    send/recv exchange does, on every rank of a gloo world."""
+    nlocal = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, nlocal, pairs, 77, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=5) for _ in range(world))
+    assert all(res[r] for r in range(world)), res
