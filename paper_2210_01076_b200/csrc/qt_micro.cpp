@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace qtb {
@@ -201,7 +202,50 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
           gterms.clear();
         }
         uint32_t x = off;
-        if (tab) {
+        // A partial table keeps its identity entries. The round compiler's
+        // tables carry the phases in front of the layer's rotations: a layer
+        // with m of R slots rotating has exact ones on the 2^(R-m) slots whose
+        // rotating bits are all 0 (C3: 150 of 232 tables). Identity entries
+        // cost nothing in the compiled kernels, so such a table is not centred
+        // (that would turn the ones into a common phase) and the sign flips
+        // are not folded into it; entries beyond a quarter turn give their -1
+        // to the flip mask instead, so every shear factor stays <= 1
+        // (C3: 1864 -> 1736 FP64 ops per amplitude). QTB_PARTIAL_TABLES=0:
+        // every table centred as a whole.
+        int n_ident = 0;
+        bool unit = tab;
+        for (int s = 0; tab && s < NS; ++s) {
+          n_ident += (t[s].re == 1.0 && t[s].im == 0.0) ? 1 : 0;
+          unit = unit && std::fabs(std::hypot(t[s].re, t[s].im) - 1.0) <= 1e-12;
+        }
+        static const bool partial_on = [] {
+          const char* e = std::getenv("QTB_PARTIAL_TABLES");
+          return !e || std::atoi(e) != 0;
+        }();
+        const bool partial = partial_on && tab && unit && n_ident >= 2 && n_ident < NS;
+        if (partial) {
+          const size_t nv = gterms.size();
+          for (const SignTerm& g : gterms) {
+            P.push_back(bits_as_double(g.gcond));
+            P.push_back(bits_as_double(g.slots));
+          }
+          const size_t toff = P.size();
+          for (int s = 0; s < NS; ++s) {
+            if (t[s].re == 1.0 && t[s].im == 0.0) {
+              P.push_back(0.0);
+              P.push_back(0.0);
+              continue;
+            }
+            if (t[s].re < 0.0) {  // |phi| > pi/2: -1 to the flips
+              t[s] = cplx{-t[s].re, -t[s].im};
+              base ^= 1u << s;
+            }
+            push_shear(P, t[s]);
+          }
+          pass_last = TableRef{pi, mp.words.size(), toff, t};
+          pass_have_last = true;
+          x |= M_STAB | (static_cast<uint32_t>(nv) << M_NV_SHIFT);
+        } else if (tab) {
           // unconditional flips join the table; each tile-uniform term
           // becomes (condition, slot mask): the table's output is negated on
           // those slots when the tile's global bits meet the condition
