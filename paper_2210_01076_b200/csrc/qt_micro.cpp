@@ -222,7 +222,23 @@ std::vector<MicroPass> lower_plan_micro(const Plan& plan, int reg_bits, const Mi
           const char* e = std::getenv("QTB_PARTIAL_TABLES");
           return !e || std::atoi(e) != 0;
         }();
-        const bool partial = partial_on && tab && unit && n_ident >= 2 && n_ident < NS;
+        bool partial = partial_on && tab && unit && n_ident >= 2 && n_ident < NS;
+        if (partial_on && tab && unit && n_ident == 0) {
+          // a full table of unit phases: its slot-0 phase is a scalar of the
+          // whole state (carried like the centring phases), which leaves an
+          // exact 1 on slot 0 -- one entry less to apply
+          const double phi0 = std::atan2(t[0].im, t[0].re);
+          const cplx ph{std::cos(phi0), std::sin(phi0)};  // the phase only (like centre_tables)
+          const cplx inv{ph.re, -ph.im};
+          pass_carried = cmul(pass_carried, ph);
+          for (int s = NS - 1; s >= 0; --s) t[s] = s == 0 ? cplx{1.0, 0.0} : cmul(t[s], inv);
+          n_ident = 1;
+          for (int s = 1; s < NS; ++s) n_ident += (t[s].re == 1.0 && t[s].im == 0.0) ? 1 : 0;
+          partial = n_ident < NS || !gterms.empty();
+          if (!partial) {  // it was a pure scalar: no table at all
+            tab = false;
+          }
+        }
         if (partial) {
           const size_t nv = gterms.size();
           for (const SignTerm& g : gterms) {
